@@ -1,0 +1,308 @@
+/*
+ * df11_oracle.c — plain, slow, obviously-correct CPU oracle for DFloat11 (arXiv 2504.11651).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path (paper_2504_11651_b200/) never
+ * does, and this file shares no code, header, table or constant generator with it.
+ *
+ * Citations: "P:n" = PAPER.md line n (section / algorithm in brackets).  Readings where the paper is
+ * silent are numbered R1..R24 and listed in DESIGN.md §3 ("Readings").
+ *
+ * Contents (bulk loops only; the small per-codebook steps E3-E5 are pure Python in huffman.py):
+ *   E1 split                 P:50-52 [§2.1, Eq. 1]; inverse of Alg. 1 compose P:429-434
+ *   E2 histogram             P:97 [§2.3] "distribution of exponents"
+ *   E6 bit packing           P:97 "tightly bit-packed into a byte array, EncodedExponent"; MSB-first (R1)
+ *   E7 gaps                  P:146 [§2.3.2] "offset of the first valid Huffman code relative to the
+ *                            thread's assigned starting byte ... stored using only 5 bits" (R12, R13)
+ *   E8 BlockOutputPos        P:148 [§2.3.2] "output position only for the first element of each
+ *                            thread block"; B+1 entries (R14)
+ *   D1 sequential decoder    P:108 [§2.3] / P:533-546 [App. I.1]: canonical bit-by-bit decode that uses
+ *                            only CodeLengths, the stream and PackedSignMantissa
+ *   D2 Alg. 1 emulator       P:376-446 [App. Alg. 1 DF11ToBF16], block by block, thread by thread
+ *
+ * Every function is single-threaded scalar C with no blocking, fusion or reordering beyond the
+ * definition it follows.
+ */
+#include <stdint.h>
+#include <string.h>
+#include <stdlib.h>
+
+/* ---------------------------------------------------------------- E1: split / compose
+ * P:50-52 [§2.1]: a BF16 word is 1 sign bit (15), 8 exponent bits (14..7), 7 mantissa bits (6..0).
+ * P:430-431 [Alg. 1]: PackedSignMantissa holds the sign in bit 7 (mask 0b10000000) and the mantissa
+ * in bits 6..0 (mask 0b01111111). */
+void df11o_split(const uint16_t *w, uint64_t n, uint8_t *exponent, uint8_t *packed_sign_mantissa)
+{
+    for (uint64_t i = 0; i < n; i++) {
+        uint16_t word = w[i];
+        uint8_t sign = (uint8_t)((word >> 15) & 1u);
+        uint8_t expo = (uint8_t)((word >> 7) & 0xFFu);
+        uint8_t mant = (uint8_t)(word & 0x7Fu);
+        exponent[i] = expo;
+        packed_sign_mantissa[i] = (uint8_t)((sign << 7) | mant);
+    }
+}
+
+/* P:429-434 [Alg. 1]: (Sign << 8) | (Exponent << 7) | Mantissa, with Sign = Byte & 0x80 and
+ * Mantissa = Byte & 0x7F.  (Sign is already the masked high bit, so Sign << 8 == 0x8000.) */
+uint16_t df11o_compose(uint8_t exponent, uint8_t packed_sign_mantissa)
+{
+    uint16_t sign = (uint16_t)(packed_sign_mantissa & 0x80u);
+    uint16_t mant = (uint16_t)(packed_sign_mantissa & 0x7Fu);
+    return (uint16_t)((sign << 8) | ((uint16_t)exponent << 7) | mant);
+}
+
+/* ---------------------------------------------------------------- E2: histogram */
+void df11o_histogram(const uint8_t *exponent, uint64_t n, uint64_t *hist /*256*/)
+{
+    for (int s = 0; s < 256; s++) hist[s] = 0;
+    for (uint64_t i = 0; i < n; i++) hist[exponent[i]]++;
+}
+
+/* ---------------------------------------------------------------- bit helpers (MSB-first, R1)
+ * Stream bit i is bit 7-(i mod 8) of byte floor(i/8). */
+static int get_bit(const uint8_t *buf, uint64_t nbytes, uint64_t bit)
+{
+    uint64_t byte = bit >> 3;
+    if (byte >= nbytes) return 0;                 /* zero-extended past the end (R16) */
+    return (buf[byte] >> (7 - (bit & 7))) & 1;
+}
+
+static void set_bit(uint8_t *buf, uint64_t bit)
+{
+    buf[bit >> 3] |= (uint8_t)(1u << (7 - (bit & 7)));
+}
+
+/* ---------------------------------------------------------------- E6: bit packing
+ * Concatenate the codeword of every element, MSB of each codeword first (R1).  `out` must be zeroed
+ * by the caller and hold at least ceil(sum(len)/8) bytes.  Returns the number of bits written. */
+uint64_t df11o_pack_bits(const uint8_t *exponent, uint64_t n, const uint8_t *code_len /*256*/,
+                         const uint32_t *code /*256*/, uint8_t *out)
+{
+    uint64_t bit = 0;
+    for (uint64_t i = 0; i < n; i++) {
+        uint8_t e = exponent[i];
+        int len = code_len[e];
+        uint32_t c = code[e];
+        for (int j = len - 1; j >= 0; j--) {      /* most significant code bit first */
+            if ((c >> j) & 1u) set_bit(out, bit);
+            bit++;
+        }
+    }
+    return bit;
+}
+
+/* ---------------------------------------------------------------- E7 + E8: gaps and BlockOutputPos
+ * Thread g (global index bT+t, R23) owns stream bits [8n*g, 8n*(g+1)).
+ *   gap[g] = (first codeword start >= 8n*g) - 8n*g   if that start is < 8n*(g+1), else 0  (R13)
+ *   bop[b] = number of codewords that start before bit 8nT*b  (b < B);  bop[B] = N      (R14)
+ * Computed directly from the definition by walking the codeword start positions once. */
+int df11o_gaps_bop(const uint8_t *exponent, uint64_t n, const uint8_t *code_len /*256*/,
+                   uint32_t T, uint32_t n_bytes, uint32_t B,
+                   uint8_t *gap_values /*B*T*/, uint32_t *bop /*B+1*/)
+{
+    uint64_t chunk_bits = 8ull * n_bytes;
+    uint64_t block_bits = chunk_bits * T;
+    uint64_t threads = (uint64_t)B * T;
+    for (uint64_t g = 0; g < threads; g++) gap_values[g] = 0;
+    for (uint32_t b = 0; b <= B; b++) bop[b] = 0;
+
+    /* starts[i] = sum of code lengths of elements before i */
+    uint64_t start = 0;
+    uint64_t next_chunk = 0;    /* smallest chunk index whose gap is not yet assigned */
+    uint64_t next_block = 0;    /* smallest block index whose bop is not yet assigned */
+    for (uint64_t i = 0; i < n; i++) {
+        /* every chunk g with 8n*g <= start and not yet assigned: this is its first start >= 8n*g */
+        while (next_chunk < threads && next_chunk * chunk_bits <= start) {
+            uint64_t c0 = next_chunk * chunk_bits;
+            uint64_t gap = start - c0;
+            gap_values[next_chunk] = (gap < chunk_bits) ? (uint8_t)gap : 0;
+            if (gap < chunk_bits && gap > 31) return -1;    /* cannot be stored in 5 bits */
+            next_chunk++;
+        }
+        while (next_block < B && next_block * block_bits <= start) {
+            bop[next_block] = (uint32_t)i;               /* codes starting before 8nT*b: elements 0..i-1 */
+            next_block++;
+        }
+        start += code_len[exponent[i]];
+    }
+    /* remaining chunks have no codeword start at or after their beginning: gap 0 (R13) */
+    while (next_block < B) { bop[next_block] = (uint32_t)n; next_block++; }
+    bop[B] = (uint32_t)n;
+    return 0;
+}
+
+/* Pack 5-bit gap values MSB-first: field g occupies stream bits [5g, 5g+5) (R12).
+ * `out` must be zeroed and hold ceil(5*count/8) bytes. */
+void df11o_pack_gaps(const uint8_t *gap_values, uint64_t count, uint8_t *out)
+{
+    for (uint64_t g = 0; g < count; g++) {
+        uint8_t v = gap_values[g];
+        for (int j = 4; j >= 0; j--)
+            if ((v >> j) & 1u) set_bit(out, 5 * g + (uint64_t)(4 - j));
+    }
+}
+
+/* Read back one 5-bit field (used by D2). */
+static uint32_t read_gap(const uint8_t *gaps, uint64_t gaps_bytes, uint64_t g)
+{
+    uint32_t v = 0;
+    for (int j = 0; j < 5; j++) v = (v << 1) | (uint32_t)get_bit(gaps, gaps_bytes, 5 * g + (uint64_t)j);
+    return v;
+}
+
+/* ---------------------------------------------------------------- D1: sequential canonical decoder
+ * Uses only CodeLengths (canonical reconstruction, R3/E4), the stream, PackedSignMantissa and N.
+ * Canonical codes: symbols sorted by (length, symbol); code_0 = 0, code_i = (code_{i-1}+1) << (l_i - l_{i-1}).
+ * Bit by bit: append the next stream bit to `code`; after l bits, if code - first_code[l] < count[l]
+ * the codeword is complete and names symbol sorted[offset[l] + code - first_code[l]].
+ * Returns 0 on success, -1 if the stream runs out (corrupt), -2 on a malformed codebook. */
+int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const uint8_t *code_len /*256*/,
+                            const uint8_t *packed_sign_mantissa, uint64_t n, uint16_t *out)
+{
+    uint32_t count[33] = {0};
+    uint32_t first_code[33] = {0};
+    uint32_t offset[33] = {0};
+    uint8_t sorted[256];
+    int nsym = 0;
+    for (int l = 1; l <= 32; l++) {
+        offset[l] = (uint32_t)nsym;
+        for (int s = 0; s < 256; s++)
+            if (code_len[s] == l) { sorted[nsym++] = (uint8_t)s; count[l]++; }
+    }
+    for (int s = 0; s < 256; s++) if (code_len[s] > 32) return -2;
+    if (n > 0 && nsym == 0) return -2;
+    /* first canonical code of each length */
+    uint64_t code = 0;
+    int prev_len = 0;
+    int have_prev = 0;
+    for (int l = 1; l <= 32; l++) {
+        if (count[l] == 0) continue;
+        if (have_prev) code = (code + 1) << (l - prev_len);
+        else code = 0;
+        /* code is now the first code of length l; the last one is code + count - 1 */
+        first_code[l] = (uint32_t)code;
+        code = code + count[l] - 1;
+        prev_len = l;
+        have_prev = 1;
+    }
+
+    uint64_t total_bits = stream_bytes * 8;
+    uint64_t bit = 0;
+    for (uint64_t i = 0; i < n; i++) {
+        uint64_t c = 0;
+        int l = 0;
+        int found = -1;
+        while (found < 0) {
+            if (bit >= total_bits) return -1;
+            c = (c << 1) | (uint64_t)get_bit(stream, stream_bytes, bit);
+            bit++;
+            l++;
+            if (l > 32) return -1;
+            if (count[l] && c >= first_code[l] && c - first_code[l] < count[l])
+                found = sorted[offset[l] + (uint32_t)(c - first_code[l])];
+        }
+        out[i] = df11o_compose((uint8_t)found, packed_sign_mantissa[i]);
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- D2: Alg. 1 emulator
+ * P:382-443.  "Read the next 4 bytes ... starting from the BitOffset-th bit, into Byte_{1..4}":
+ * a big-endian 32-bit window at the absolute stream bit chunk_start + BitOffset (R2), zero-extended
+ * past the buffer end (R16).  Exponent >= 240 is a pointer to LUT_{257-Exponent} (1-based), i.e. the
+ * 0-based table 256-Exponent (narrow, entry_bytes = 1); wide tables (entry_bytes = 2, R8) use
+ * entries >= 256 as pointers to table (entry-256).  Outputs are clipped to [BOP[b], BOP[b+1]) (R15).
+ * check_counts = 1 additionally asserts that every non-final block decodes exactly
+ * BOP[b+1]-BOP[b] elements (returns -3 if not).  Returns 0 on success, -4 on a malformed LUT walk. */
+static uint32_t window32(const uint8_t *stream, uint64_t stream_bytes, uint64_t bit)
+{
+    uint32_t w = 0;
+    for (int j = 0; j < 32; j++) w = (w << 1) | (uint32_t)get_bit(stream, stream_bytes, bit + (uint64_t)j);
+    return w;
+}
+
+static int lut_entry(const uint8_t *luts, uint32_t entry_bytes, uint32_t table, uint32_t idx)
+{
+    if (entry_bytes == 1) return luts[(uint64_t)table * 256 + idx];
+    const uint8_t *p = luts + ((uint64_t)table * 256 + idx) * 2;
+    return (int)p[0] | ((int)p[1] << 8);           /* little-endian uint16 entries */
+}
+
+static int is_pointer(int e, uint32_t entry_bytes) { return entry_bytes == 1 ? e >= 240 : e >= 256; }
+static uint32_t pointer_target(int e, uint32_t entry_bytes)
+{
+    return entry_bytes == 1 ? (uint32_t)(256 - e) : (uint32_t)(e - 256);
+}
+
+/* One LUT walk: returns the decoded exponent or -1 on a malformed walk. */
+static int alg1_decode_one(uint32_t window, const uint8_t *luts, uint32_t entry_bytes, uint32_t k)
+{
+    int i = 1;
+    uint32_t byte_i = (window >> 24) & 0xFFu;
+    int e = lut_entry(luts, entry_bytes, 0, byte_i);        /* LUT_1 = root */
+    while (is_pointer(e, entry_bytes)) {
+        i = i + 1;
+        if (i > 4) return -1;
+        uint32_t table = pointer_target(e, entry_bytes);
+        if (table >= k) return -1;
+        byte_i = (window >> (8 * (4 - i))) & 0xFFu;
+        e = lut_entry(luts, entry_bytes, table, byte_i);
+    }
+    return e;
+}
+
+int df11o_decode_alg1(const uint8_t *luts, uint32_t entry_bytes, uint32_t k, const uint8_t *code_len,
+                      const uint8_t *stream, uint64_t stream_bytes,
+                      const uint8_t *gaps, uint64_t gaps_bytes, const uint32_t *bop,
+                      const uint8_t *packed_sign_mantissa, uint32_t B, uint32_t T, uint32_t n_bytes,
+                      uint64_t N, int check_counts, uint16_t *out)
+{
+    uint64_t chunk_bits = 8ull * n_bytes;
+    uint32_t *num_elements = (uint32_t *)calloc(T ? T : 1, sizeof(uint32_t));
+    uint64_t *thread_output_pos = (uint64_t *)calloc(T ? T : 1, sizeof(uint64_t));
+    if (!num_elements || !thread_output_pos) { free(num_elements); free(thread_output_pos); return -5; }
+    int rc = 0;
+    for (uint32_t b = 0; b < B && rc == 0; b++) {
+        /* Phase 1: each thread counts the codewords that start in its chunk. */
+        for (uint32_t t = 0; t < T; t++) {
+            uint64_t g = (uint64_t)b * T + t;
+            uint64_t chunk_start = g * chunk_bits;
+            uint64_t bit_offset = read_gap(gaps, gaps_bytes, g);
+            num_elements[t] = 0;
+            while (bit_offset < chunk_bits) {
+                uint32_t w = window32(stream, stream_bytes, chunk_start + bit_offset);
+                int e = alg1_decode_one(w, luts, entry_bytes, k);
+                if (e < 0 || code_len[e] == 0) { rc = -4; break; }
+                bit_offset += code_len[e];
+                num_elements[t]++;
+            }
+            if (rc) break;
+        }
+        if (rc) break;
+        /* Prefix sum: ThreadOutputPos[t] = BlockOutputPos[b] + sum_{i<t} NumElements[i]. */
+        uint64_t running = 0;
+        for (uint32_t t = 0; t < T; t++) { thread_output_pos[t] = bop[b] + running; running += num_elements[t]; }
+        if (check_counts && b + 1 < B && running != (uint64_t)bop[b + 1] - bop[b]) { rc = -3; break; }
+        /* Phase 2: re-decode and write, clipped to [BOP[b], BOP[b+1]) and N (R15). */
+        for (uint32_t t = 0; t < T; t++) {
+            uint64_t g = (uint64_t)b * T + t;
+            uint64_t chunk_start = g * chunk_bits;
+            uint64_t bit_offset = read_gap(gaps, gaps_bytes, g);
+            uint64_t pos = thread_output_pos[t];
+            while (bit_offset < chunk_bits) {
+                uint32_t w = window32(stream, stream_bytes, chunk_start + bit_offset);
+                int e = alg1_decode_one(w, luts, entry_bytes, k);
+                if (e < 0 || code_len[e] == 0) { rc = -4; break; }
+                if (pos < bop[b + 1] && pos < N)
+                    out[pos] = df11o_compose((uint8_t)e, packed_sign_mantissa[pos]);
+                bit_offset += code_len[e];
+                pos++;
+            }
+            if (rc) break;
+        }
+    }
+    free(num_elements);
+    free(thread_output_pos);
+    return rc;
+}
