@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""DF11 decompression benchmark (BASELINE.json metric: GB/s of BF16 produced; % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama8b_block] [--kernel auto]
+    torchrun --nproc-per-node N bench.py --gpus N ...        # one rank per GPU, weak scaling
+    python bench.py --impl reference ...                     # the CPU oracle as the reference arm
+
+A step = one df11_decompress_block call over every tensor of one transformer block (all §8(a) rows:
+tile map, LUT staging, chunk staging, gaps, phase 1, scan, phase 2, write-back), inputs resident in
+HBM.  Each rank decodes its own block (different seeds): no collective on the data path; NCCL is
+used only for the start barrier and the max-over-ranks of the timings.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "DF11 decompress GB/s (BF16 out) per GPU and 8-GPU aggregate; % of HBM roofline"
+UNIT = "GB/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=400)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default=workloads.BASELINE_CONFIGS[1])
+    p.add_argument("--kernel", choices=["auto", "alg1", "fast"], default="auto")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=5)
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks (NVML)
+class ClockSampler:
+    """Samples SM clock and throttle reasons every 10 ms during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config: str, kernel: str):
+    """Per-launch dram bytes from the committed ncu summary (profiles/ncu_summary.json), if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(f"{config}/{kernel}")
+    return None if e is None else e.get("dram_bytes_per_launch")
+
+
+# --------------------------------------------------------------------------- CPU oracle timing
+def oracle_decode_rate(tensors_np, budget_s: float = 12.0):
+    """Time the oracle's sequential decoder (D1) on a bounded sample of this workload: whole tensors
+    in config order until ~budget_s of CPU work.  One thread per tensor (the oracle is single-
+    threaded); returns (GB/s of BF16, cores, sample description, seconds)."""
+    import concurrent.futures as cf
+
+    import oracle
+    fmts = []
+    spent = 0.0
+    est_rate = 60e6                                      # el/s, refined after the first tensor
+    for name, w in tensors_np:
+        if fmts and spent + w.size / est_rate > budget_s:
+            break
+        fmts.append((name, oracle.encode(w.reshape(-1)), w))
+        spent += w.size / est_rate
+    cores = min(len(fmts), os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
+        outs = list(ex.map(lambda f: oracle.decode_sequential(f[1]), fmts))
+    dt = time.perf_counter() - t0
+    for (name, _, w), o in zip(fmts, outs):
+        assert np.array_equal(o, w.reshape(-1)), name
+    elems = sum(w.size for _, _, w in fmts)
+    sample = f"D1 sequential decode of {len(fmts)} tensor(s) ({elems} elements: " + \
+        ", ".join(n for n, _, _ in fmts) + f") of {tensors_np and 'the workload'}, {cores} thread(s)"
+    return 2 * elems / dt / 1e9, cores, sample, dt
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (D1) timed as the reference arm on this workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build_oracle()
+    name, shape = workloads.CONFIGS[args.config][0]
+    w = workloads.gaussian_bf16(shape, workloads.seed_for(args.config, 0, name)).reshape(-1)
+    w = w[: 1 << 22]                                       # bounded sample per step: 4 Mi elements
+    fmt = oracle.encode(w)
+    for _ in range(args.warmup):
+        oracle.decode_sequential(fmt)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = oracle.decode_sequential(fmt)
+    dt = time.perf_counter() - t0
+    assert np.array_equal(out, w)
+    value = 2 * w.size * args.steps / dt / 1e9
+    sample = f"D1 sequential decode of the first {w.size} elements of {args.config}/{name} per step, 1 thread"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic", "config": {"workload": args.config, "elements_per_step": int(w.size)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_11651_b200 import df11
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- this rank's shard: one transformer block (seeded by rank -> distinct weights per GPU)
+    tensors = workloads.config_tensors(args.config, layer=rank)
+    hs = [df11.encode(w) for _, w in tensors]
+    N = sum(h.num_elements for h in hs)
+    scratch = torch.empty(N + 64, dtype=torch.bfloat16, device=dev)        # reused BF16 scratch
+    outs, o = [], 0
+    for h in hs:
+        outs.append(scratch[o:o + h.num_elements])
+        o += (h.num_elements + 7) // 8 * 8                                 # keep views 16-byte aligned
+    assert o <= scratch.numel()
+    dts = [df11.to_device(h, dev) for h in hs]
+    plan = df11.BlockPlan(dts, outs)
+    kernel_used = args.kernel
+    if args.kernel == "auto":
+        try:
+            plan.run(kernel="fast")
+            kernel_used = "fast"
+        except df11.Df11Error:
+            kernel_used = "alg1"
+    # ---- verify once: bit-exact against the original weights (kept on the GPU for the check)
+    plan.run(kernel=kernel_used)
+    torch.cuda.synchronize()
+    for (name, w), out in zip(tensors, plan.outputs()):
+        ref = torch.from_numpy(w.reshape(-1).view(np.int16)).to(dev)
+        if not torch.equal(out.reshape(-1).view(torch.int16), ref):
+            raise SystemExit(f"bit-exact check failed on {name}")
+        del ref
+    bf16_bytes = 2 * N
+    algo_bytes = sum(dt.compressed_bytes for dt in dts) + bf16_bytes       # read DF11 + write BF16
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.run(stream, kernel_used)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    df11.launch_count(reset=True)
+    with ClockSampler(local) as clocks:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            plan.run(stream, kernel_used)
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = df11.launch_count()
+    barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([total_ms, float(np.mean(launch_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, avg_launch_ms = float(t[0]), float(t[1])
+    value = world * bf16_bytes * args.steps / (total_ms / 1e3) / 1e9
+
+    peak, peak_src = measured_peaks()
+    achieved = algo_bytes / (avg_launch_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(args.config, kernel_used), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": algo_bytes,
+                "note": "achieved = (DF11 bytes read + BF16 bytes written) / mean launch time (CUDA events)"}
+
+    # ---- e2e: through the C ABI with host buffers (pinned H2D of the DF11 arrays, decode, D2H of BF16)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(df11, hs, dts, dev, args.e2e_steps, world, barrier, tensors)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        try:
+            v, cores, sample, secs = oracle_decode_rate(tensors)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                   "seconds": round(secs, 2)}
+        except Exception as exc:                                           # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": args.config, "tensors": len(hs), "elements_per_gpu": N,
+                       "bf16_bytes_per_gpu": bf16_bytes, "df11_bytes_per_gpu": algo_bytes - bf16_bytes,
+                       "bits_per_weight": 8 * (algo_bytes - bf16_bytes) / N, "T": hs[0].T, "n": hs[0].n,
+                       "kernel": kernel_used, "parallelism": f"shard{world} (one block per GPU, no collective)",
+                       "l2": f"inputs larger than L2: {algo_bytes / 1e6:.0f} MB moved per step vs 126 MB L2"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "per_gpu_gbs": value / world,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(df11, hs, dts, dev, steps, world, barrier, tensors):
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream()
+    pinned_in, host_views, host_outs = [], [], []
+    for h in hs:
+        arrs = h.arrays()
+        keep = {}
+        for key in ("luts", "encoded_exponent", "packed_sign_mantissa", "gaps", "block_output_pos"):
+            a = np.ascontiguousarray(arrs[key]).view(np.uint8)
+            t = torch.empty(max(a.size, 1), dtype=torch.uint8, pin_memory=True)
+            t[: a.size].copy_(torch.from_numpy(a))
+            keep[key] = t
+        c = df11.HostTensorC()
+        import ctypes
+        ctypes.memmove(ctypes.byref(c), ctypes.byref(h._c), ctypes.sizeof(c))
+        c.luts = ctypes.cast(keep["luts"].data_ptr(), ctypes.POINTER(ctypes.c_uint8))
+        c.encoded_exponent = ctypes.cast(keep["encoded_exponent"].data_ptr(), ctypes.POINTER(ctypes.c_uint8))
+        c.packed_sign_mantissa = ctypes.cast(keep["packed_sign_mantissa"].data_ptr(), ctypes.POINTER(ctypes.c_uint8))
+        c.gaps = ctypes.cast(keep["gaps"].data_ptr(), ctypes.POINTER(ctypes.c_uint8))
+        c.block_output_pos = ctypes.cast(keep["block_output_pos"].data_ptr(), ctypes.POINTER(ctypes.c_uint32))
+        pinned_in.append(keep)
+        host_views.append(c)
+        host_outs.append(torch.empty(max(h.num_elements, 1), dtype=torch.bfloat16, pin_memory=True))
+    h2d = sum(dt.staging_bytes() for dt in dts)
+    d2h = sum(2 * h.num_elements for h in hs)
+    N = sum(h.num_elements for h in hs)
+
+    def step():
+        for c, dt, ho in zip(host_views, dts, host_outs):
+            d = dt.descriptor()
+            st = df11.lib().df11_decompress_host(ctypes.byref(c), ctypes.byref(d),
+                                                 ctypes.c_void_p(ho.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+            if st != 0:
+                raise df11.Df11Error(st, df11.lib().df11_last_error_message().decode())
+
+    import ctypes
+    step()
+    torch.cuda.synchronize()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # the last step's host output must be the original weights
+    for ho, h, (name, w) in zip(host_outs, hs, tensors):
+        got = ho[: h.num_elements].view(torch.int16).numpy().view(np.uint16)
+        if not np.array_equal(got, w.reshape(-1)):
+            raise SystemExit(f"e2e bit-exact check failed on {name}")
+    value = world * 2 * N * steps / (float(ms[0]) / 1e3) / 1e9
+    return {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": steps, "path": "df11_decompress_host per tensor (pinned H2D + decode + D2H), one stream"}
+
+
+if __name__ == "__main__":
+    main()

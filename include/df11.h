@@ -1,0 +1,133 @@
+/*
+ * df11.h — C ABI of the B200-native DFloat11 library (arXiv 2504.11651).
+ *
+ * Citations: "P:n" = PAPER.md line n.  The bit-exact format is DESIGN.md §2; the readings where the
+ * paper is silent are DESIGN.md §3 (R1..R24).
+ *
+ * Conventions
+ *  - Every call returns df11_status; no C++ exception crosses the ABI.
+ *  - Host encode calls allocate their outputs; free them with df11_host_tensor_free().
+ *  - Device calls take device pointers OWNED BY THE CALLER (e.g. torch tensors) and a cudaStream_t
+ *    (passed as void*; NULL = the legacy default stream).  They only enqueue work: device faults
+ *    surface at the caller's next synchronisation (CUDA semantics).  They never allocate, never copy
+ *    host<->device and are CUDA-graph capturable.
+ *  - Robustness: malformed device metadata may produce wrong output but never an out-of-bounds
+ *    access: every write is clipped to [BlockOutputPos[b], BlockOutputPos[b+1]) ∩ [0, N), LUT walks
+ *    are bounded to 4 levels and k tables, and every code step advances at least one bit.
+ *  - Thread safety: no mutable global state except cached device attributes and the last CUDA error.
+ */
+#ifndef DF11_H
+#define DF11_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DF11_OK = 0,
+    DF11_E_INVALID_ARGUMENT = 1,   /* null pointer, bad T/n/mode, inconsistent descriptor */
+    DF11_E_RESERVED_EXPONENT = 2,  /* exponent >= 240 present with lut_mode NARROW (R8) */
+    DF11_E_LUT_OVERFLOW = 3,       /* > 16 child LUTs with lut_mode NARROW (R9) */
+    DF11_E_TOO_LARGE = 4,          /* N >= 2^32 per tensor: BlockOutputPos is uint32 */
+    DF11_E_CORRUPT = 5,            /* host-side metadata check failed */
+    DF11_E_CUDA = 6,               /* launch/config error; see df11_last_cuda_error() */
+    DF11_E_ALLOC = 7,              /* host allocation failed */
+    DF11_E_UNSUPPORTED = 8         /* a forced kernel variant cannot handle these parameters */
+} df11_status;
+
+enum { DF11_LUT_AUTO = 0, DF11_LUT_NARROW = 1, DF11_LUT_WIDE = 2 };
+
+/* Kernel selection for df11_decompress_block_ex (AUTO = fast kernel when eligible). */
+enum { DF11_KERNEL_AUTO = 0, DF11_KERNEL_ALG1 = 1, DF11_KERNEL_FAST = 2 };
+
+#define DF11_MAX_BATCH 64          /* tensors per df11_decompress_block call */
+
+typedef struct {
+    uint32_t threads_per_block;    /* T: multiple of 32 in [32, 1024]; default 256 (R17) */
+    uint32_t bytes_per_thread;     /* n: [4, 32]; default 8 */
+    uint32_t lut_mode;             /* DF11_LUT_AUTO | NARROW (paper format) | WIDE */
+    uint32_t num_threads;          /* host encoder threads; 0 = all hardware threads */
+} df11_encode_opts;
+
+/* Host-side DF11 tensor.  All arrays are library-owned, zero-padded as stated. */
+typedef struct {
+    uint64_t num_elements;                 /* N */
+    uint64_t encoded_bits;                 /* sum of code lengths */
+    uint32_t T, n, B, k;                   /* threads/block, bytes/thread, #blocks, #LUTs */
+    uint32_t lut_entry_bytes;              /* 1 = narrow (paper), 2 = wide (R8) */
+    uint32_t max_code_len;                 /* L <= 32 */
+    uint8_t  code_lengths[256];            /* CodeLengths */
+    uint8_t  *luts;              uint64_t luts_bytes;                  /* k*256*lut_entry_bytes; table 0 = root */
+    uint8_t  *encoded_exponent;  uint64_t encoded_exponent_bytes;      /* B*T*n + 16 */
+    uint8_t  *packed_sign_mantissa; uint64_t packed_sign_mantissa_bytes; /* roundup(N,16) + 16 */
+    uint8_t  *gaps;              uint64_t gaps_bytes;                  /* roundup(ceil(5BT/8),16) + 16 */
+    uint32_t *block_output_pos;                                        /* B+1 entries, [B] = N */
+} df11_host_tensor;
+
+/* Device view of one DF11 tensor.  Every pointer is a device pointer owned by the caller; arrays
+ * must have the sizes of df11_host_tensor (including the zero padding).  `code_lengths` points at
+ * 256 device bytes.  `out` receives N BF16 words (16-byte alignment recommended: the fast kernel
+ * then writes 128-bit stores). */
+typedef struct {
+    const uint8_t  *encoded_exponent;
+    const uint8_t  *packed_sign_mantissa;
+    const uint8_t  *gaps;
+    const uint8_t  *luts;
+    const uint8_t  *code_lengths;
+    const uint32_t *block_output_pos;
+    uint16_t       *out;
+    uint64_t        num_elements;
+    uint32_t        T, n, B, k, lut_entry_bytes;
+    uint32_t        reserved;              /* must be 0 */
+} df11_device_tensor;
+
+/* ---- host encoder --------------------------------------
+ * df11_encode: one BF16 tensor (uint16 bit patterns, row-major) -> DF11 with a per-tensor codebook.
+ * opts may be NULL (defaults).  N = 0 is legal (B = 0).  Errors: DF11_E_INVALID_ARGUMENT,
+ * DF11_E_RESERVED_EXPONENT / DF11_E_LUT_OVERFLOW (NARROW only), DF11_E_TOO_LARGE, DF11_E_ALLOC.
+ * On error *out is left zeroed. */
+df11_status df11_encode(const uint16_t *bf16, uint64_t n_elems, const df11_encode_opts *opts,
+                        df11_host_tensor *out);
+
+/* df11_encode_group: `count` tensors; shared_codebook != 0 builds one codebook from the summed
+ * histogram of the group (R5: "a Huffman tree based on the distribution of exponents in model
+ * weights") and stores a copy of it in every output; otherwise one codebook per tensor. */
+df11_status df11_encode_group(const uint16_t *const *tensors, const uint64_t *n_elems, uint32_t count,
+                              const df11_encode_opts *opts, int shared_codebook, df11_host_tensor *outs);
+
+void df11_host_tensor_free(df11_host_tensor *t);
+
+/* ---- device decoder (rows a1-a9; Alg. 1; block batching P:153-157) --------------------
+ * df11_decompress: one tensor, one launch.  df11_decompress_block: every tensor of a transformer
+ * block in ONE launch (count <= DF11_MAX_BATCH; empty tensors allowed).  On a validation error the
+ * message names the offending descriptor index (df11_last_error_message()).  `stream` is a
+ * cudaStream_t. */
+df11_status df11_decompress(const df11_device_tensor *t, void *stream);
+df11_status df11_decompress_block(const df11_device_tensor *ts, uint32_t count, void *stream);
+/* Same with an explicit kernel: DF11_KERNEL_ALG1 (literal Alg. 1, any valid T/n) or DF11_KERNEL_FAST
+ * (persistent sm_100a kernel; DF11_E_UNSUPPORTED if a tensor is outside its parameter range). */
+df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream,
+                                     int kernel);
+
+/* ---- end-to-end from host memory --------------------------------------------------------------
+ * df11_decompress_host: copies the host arrays of `h` into the caller-provided device staging
+ * buffers described by `d` (same sizes as h's arrays), decodes into d->out and copies the BF16
+ * result into `host_out` (N words; pinned memory recommended), all enqueued on `stream`.
+ * Returns after enqueueing; synchronise the stream before reading host_out. */
+df11_status df11_decompress_host(const df11_host_tensor *h, const df11_device_tensor *d,
+                                 uint16_t *host_out, void *stream);
+
+/* ---- diagnostics ------------------------------------------------------------------------------ */
+const char *df11_status_string(df11_status s);
+int         df11_last_cuda_error(void);            /* cudaError_t of the last failing CUDA call */
+const char *df11_last_error_message(void);         /* thread-local, human readable */
+const char *df11_version(void);
+/* Number of kernel launches enqueued by this thread since the last reset (for bench accounting). */
+uint64_t    df11_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DF11_H */

@@ -1,0 +1,203 @@
+// api.cu — the C ABI (include/df11.h): validation, kernel selection, launches, diagnostics.
+//
+// df11_decompress_block: all tensors of a transformer block are described in ONE
+// __grid_constant__ Batch and decoded by ONE launch of the fast kernel (decode_fast.cu).  Tensors whose
+// format parameters the fast kernel does not specialise go through the literal Algorithm 1 kernel
+// (decode_alg1.cu), one launch per distinct T.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "decode_common.cuh"
+#include "df11_internal.h"
+
+namespace df11 {
+cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream_t stream, uint64_t *launches);
+cudaError_t launch_fast(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
+bool fast_supports(const df11_device_tensor &t);
+}  // namespace df11
+
+namespace {
+thread_local char g_msg[512] = "";
+thread_local int g_cuda_err = 0;
+thread_local uint64_t g_launches = 0;
+
+int g_max_smem[64];
+int g_num_sms[64];
+std::once_flag g_attr_once[64];
+
+void device_attrs(int dev, int &max_smem, int &num_sms) {
+    if (dev < 0 || dev >= 64) { max_smem = 48 * 1024; num_sms = 1; return; }
+    std::call_once(g_attr_once[dev], [dev] {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        g_max_smem[dev] = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev] = v;
+    });
+    max_smem = g_max_smem[dev];
+    num_sms = g_num_sms[dev];
+}
+
+df11_status cuda_fail(cudaError_t e, const char *what) {
+    g_cuda_err = (int)e;
+    std::snprintf(g_msg, sizeof(g_msg), "%s: %s", what, cudaGetErrorString(e));
+    return DF11_E_CUDA;
+}
+
+df11_status validate(const df11_device_tensor &t, uint32_t idx) {
+    char buf[160];
+    auto bad = [&](const char *why) {
+        std::snprintf(buf, sizeof(buf), "descriptor %u: %s", idx, why);
+        return df11_fail(DF11_E_INVALID_ARGUMENT, buf);
+    };
+    if (t.reserved != 0) return bad("reserved field must be 0");
+    if (t.num_elements >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "N >= 2^32");
+    if (t.num_elements == 0) return DF11_OK;                     // empty tensor: no-op (R11)
+    if (t.B == 0) return bad("B == 0 with N > 0");
+    if (t.T < 32 || t.T > 1024 || t.T % 32) return bad("T must be a multiple of 32 in [32, 1024]");
+    if (t.n < 4 || t.n > 32) return bad("n must be in [4, 32]");
+    if (t.lut_entry_bytes != 1 && t.lut_entry_bytes != 2) return bad("lut_entry_bytes must be 1 or 2");
+    if (t.k == 0) return bad("k == 0 with N > 0");
+    if (t.lut_entry_bytes == 1 && t.k > 17) return bad("narrow LUTs allow at most 17 tables");
+    if ((uint64_t)t.B * t.T * t.n * 8 > (uint64_t)t.num_elements * 32 + (uint64_t)t.T * t.n * 8)
+        return bad("B too large for N (codes are at most 32 bits)");
+    if (!t.encoded_exponent || !t.packed_sign_mantissa || !t.gaps || !t.luts || !t.code_lengths ||
+        !t.block_output_pos || !t.out)
+        return bad("NULL device pointer");
+    return DF11_OK;
+}
+}  // namespace
+
+extern "C" df11_status df11_fail(df11_status st, const char *msg) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s", msg ? msg : "");
+    return st;
+}
+
+extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream_v,
+                                                int kernel) {
+    if (count > DF11_MAX_BATCH) return df11_fail(DF11_E_INVALID_ARGUMENT, "count > DF11_MAX_BATCH");
+    if (count && !ts) return df11_fail(DF11_E_INVALID_ARGUMENT, "descriptor array is NULL");
+    if (kernel < DF11_KERNEL_AUTO || kernel > DF11_KERNEL_FAST) return df11_fail(DF11_E_INVALID_ARGUMENT, "bad kernel");
+    bool all_fast = true;
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        df11_status st = validate(ts[i], i);
+        if (st != DF11_OK) return st;
+        if (ts[i].num_elements) {
+            total += ts[i].B;
+            if (!df11::fast_supports(ts[i])) all_fast = false;
+        }
+    }
+    if (total == 0) return DF11_OK;
+    if (total >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "batch has >= 2^32 format blocks");
+    if (kernel == DF11_KERNEL_FAST && !all_fast)
+        return df11_fail(DF11_E_UNSUPPORTED, "fast kernel: a tensor is outside its parameter range (T=256, n=8)");
+    cudaStream_t stream = (cudaStream_t)stream_v;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int max_smem = 0, num_sms = 0;
+    device_attrs(dev, max_smem, num_sms);
+
+    static thread_local df11::Batch bt;   // ~6 KB: keep it off the stack
+    bool use_fast = all_fast && kernel != DF11_KERNEL_ALG1;
+    if (use_fast) {
+        std::memset(&bt, 0, sizeof(bt));
+        uint32_t acc = 0;
+        for (uint32_t i = 0; i < count; i++) {
+            if (!ts[i].num_elements) continue;
+            bt.t[bt.count] = ts[i];
+            bt.tile_start[bt.count] = acc;
+            acc += ts[i].B;
+            bt.count++;
+        }
+        bt.tile_start[bt.count] = acc;
+        bt.total_tiles = acc;
+        e = df11::launch_fast(bt, dev, stream, &g_launches);
+        if (e != cudaSuccess) return cuda_fail(e, "fast decode launch");
+        return DF11_OK;
+    }
+    // Algorithm 1: one launch per distinct T
+    bool done[DF11_MAX_BATCH] = {};
+    for (uint32_t i = 0; i < count; i++) {
+        if (done[i] || !ts[i].num_elements) continue;
+        const uint32_t T = ts[i].T;
+        std::memset(&bt, 0, sizeof(bt));
+        uint32_t acc = 0;
+        for (uint32_t j = i; j < count; j++) {
+            if (done[j] || !ts[j].num_elements || ts[j].T != T) continue;
+            done[j] = true;
+            bt.t[bt.count] = ts[j];
+            bt.tile_start[bt.count] = acc;
+            acc += ts[j].B;
+            bt.count++;
+        }
+        bt.tile_start[bt.count] = acc;
+        bt.total_tiles = acc;
+        e = df11::launch_alg1(bt, T, (size_t)max_smem, stream, &g_launches);
+        if (e != cudaSuccess) return cuda_fail(e, "Alg. 1 decode launch");
+    }
+    return DF11_OK;
+}
+
+extern "C" df11_status df11_decompress_block(const df11_device_tensor *ts, uint32_t count, void *stream) {
+    return df11_decompress_block_ex(ts, count, stream, DF11_KERNEL_AUTO);
+}
+
+extern "C" df11_status df11_decompress(const df11_device_tensor *t, void *stream) {
+    if (!t) return df11_fail(DF11_E_INVALID_ARGUMENT, "descriptor is NULL");
+    return df11_decompress_block_ex(t, 1, stream, DF11_KERNEL_AUTO);
+}
+
+extern "C" df11_status df11_decompress_host(const df11_host_tensor *h, const df11_device_tensor *d,
+                                            uint16_t *host_out, void *stream_v) {
+    if (!h || !d || (!host_out && h->num_elements)) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL argument");
+    if (d->num_elements != h->num_elements || d->B != h->B || d->T != h->T || d->n != h->n || d->k != h->k ||
+        d->lut_entry_bytes != h->lut_entry_bytes)
+        return df11_fail(DF11_E_INVALID_ARGUMENT, "device descriptor does not match the host tensor");
+    if (h->num_elements == 0) return DF11_OK;
+    cudaStream_t s = (cudaStream_t)stream_v;
+    struct { void *dst; const void *src; uint64_t n; } cp[] = {
+        {(void *)d->encoded_exponent, h->encoded_exponent, h->encoded_exponent_bytes},
+        {(void *)d->packed_sign_mantissa, h->packed_sign_mantissa, h->packed_sign_mantissa_bytes},
+        {(void *)d->gaps, h->gaps, h->gaps_bytes},
+        {(void *)d->luts, h->luts, h->luts_bytes},
+        {(void *)d->code_lengths, h->code_lengths, 256},
+        {(void *)d->block_output_pos, h->block_output_pos, 4ull * (h->B + 1)},
+    };
+    for (auto &c : cp) {
+        if (!c.dst) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL device staging pointer");
+        cudaError_t e = cudaMemcpyAsync(c.dst, c.src, c.n, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    }
+    df11_status st = df11_decompress(d, stream_v);
+    if (st != DF11_OK) return st;
+    cudaError_t e = cudaMemcpyAsync(host_out, d->out, 2ull * h->num_elements, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    return DF11_OK;
+}
+
+extern "C" const char *df11_status_string(df11_status s) {
+    switch (s) {
+        case DF11_OK: return "DF11_OK";
+        case DF11_E_INVALID_ARGUMENT: return "DF11_E_INVALID_ARGUMENT";
+        case DF11_E_RESERVED_EXPONENT: return "DF11_E_RESERVED_EXPONENT";
+        case DF11_E_LUT_OVERFLOW: return "DF11_E_LUT_OVERFLOW";
+        case DF11_E_TOO_LARGE: return "DF11_E_TOO_LARGE";
+        case DF11_E_CORRUPT: return "DF11_E_CORRUPT";
+        case DF11_E_CUDA: return "DF11_E_CUDA";
+        case DF11_E_ALLOC: return "DF11_E_ALLOC";
+        case DF11_E_UNSUPPORTED: return "DF11_E_UNSUPPORTED";
+    }
+    return "DF11_E_UNKNOWN";
+}
+
+extern "C" int df11_last_cuda_error(void) { return g_cuda_err; }
+extern "C" const char *df11_last_error_message(void) { return g_msg; }
+extern "C" const char *df11_version(void) { return "df11-b200 0.1 (sm_100a)"; }
+extern "C" uint64_t df11_launch_count(int reset) {
+    uint64_t v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}

@@ -1,0 +1,491 @@
+// encode.cpp — host DF11 encoder: df11_encode / df11_encode_group.
+//
+// Produces the bit-exact format of DESIGN.md §2 from the paper's description:
+//   split -> exponent histogram -> Huffman code lengths with the 32-bit
+//   cap (R3 tie rule, R4 package-merge) -> canonical codes -> hierarchical 256-entry LUTs
+//   (App. I.2; R6 breadth-first children, R8 wide fallback) -> MSB-first bit packing of
+//   EncodedExponent (R1) -> Gaps (R12/R13) and BlockOutputPos (R14).
+//
+// Built for speed, not for reading against the paper (that is oracle/'s job): every O(N) pass is
+// split over host threads; the bit packer gives every thread a bit range computed by a prefix sum of
+// per-segment code-length totals and ORs the two bytes it shares with its neighbours atomically.
+// This file shares no code with oracle/; byte-for-byte agreement is checked by tests/test_encoder_parity.py.
+#include "df11.h"
+#include "df11_internal.h"
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <new>
+#include <thread>
+#include <vector>
+
+namespace {
+
+constexpr int kMaxCodeLen = 32;
+
+// ------------------------------------------------------------------------------------ threading
+struct Pool {
+    unsigned nthreads;
+    explicit Pool(unsigned requested, uint64_t work) {
+        unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        nthreads = requested ? requested : hw;
+        // below ~256K elements per thread the spawn cost dominates
+        uint64_t cap = std::max<uint64_t>(1, work / (1u << 18));
+        if (nthreads > cap) nthreads = (unsigned)cap;
+        if (nthreads < 1) nthreads = 1;
+    }
+    // run f(tid, begin, end) over [0, n) split into nthreads contiguous ranges
+    void run(uint64_t n, const std::function<void(unsigned, uint64_t, uint64_t)> &f) const {
+        if (nthreads == 1) { f(0, 0, n); return; }
+        std::vector<std::thread> ts;
+        ts.reserve(nthreads);
+        for (unsigned t = 0; t < nthreads; t++) {
+            uint64_t b = n * t / nthreads, e = n * (t + 1) / nthreads;
+            ts.emplace_back([&f, t, b, e] { f(t, b, e); });
+        }
+        for (auto &th : ts) th.join();
+    }
+};
+
+inline uint64_t roundup(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
+// ------------------------------------------------------------------------------------ histogram
+void histogram(const uint16_t *w, uint64_t n, const Pool &pool, uint64_t hist[256]) {
+    std::vector<uint64_t> part((size_t)pool.nthreads * 256, 0);
+    pool.run(n, [&](unsigned t, uint64_t b, uint64_t e) {
+        uint64_t local[4][256] = {};
+        uint64_t i = b;
+        for (; i + 4 <= e; i += 4) {                      // 4 sub-histograms hide store-to-load stalls
+            local[0][(w[i] >> 7) & 0xFF]++;
+            local[1][(w[i + 1] >> 7) & 0xFF]++;
+            local[2][(w[i + 2] >> 7) & 0xFF]++;
+            local[3][(w[i + 3] >> 7) & 0xFF]++;
+        }
+        for (; i < e; i++) local[0][(w[i] >> 7) & 0xFF]++;
+        for (int s = 0; s < 256; s++) part[(size_t)t * 256 + s] = local[0][s] + local[1][s] + local[2][s] + local[3][s];
+    });
+    for (int s = 0; s < 256; s++) {
+        uint64_t acc = 0;
+        for (unsigned t = 0; t < pool.nthreads; t++) acc += part[(size_t)t * 256 + s];
+        hist[s] = acc;
+    }
+}
+
+// ------------------------------------------------------------------------------------ code lengths
+// Leaves in (count asc, symbol asc) order.
+std::vector<int> ranked_symbols(const uint64_t hist[256]) {
+    std::vector<int> syms;
+    for (int s = 0; s < 256; s++) if (hist[s]) syms.push_back(s);
+    std::stable_sort(syms.begin(), syms.end(), [&](int a, int b) { return hist[a] < hist[b]; });
+    return syms;   // stable sort over ascending symbols => ties broken by symbol
+}
+
+// Two-queue Huffman (R3).  With leaves sorted by (count, symbol) the queue of internal nodes is sorted
+// by creation, so comparing the two queue fronts on (weight, key) reproduces a min-heap keyed by
+// (weight, key) where leaves have keys 0..|S|-1 and internal nodes |S|+creation index: on equal
+// weight the leaf wins.
+void huffman_lengths(const uint64_t hist[256], const std::vector<int> &ranked, uint8_t len[256]) {
+    const int m = (int)ranked.size();
+    std::memset(len, 0, 256);
+    if (m == 0) return;
+    if (m == 1) { len[ranked[0]] = 1; return; }
+    // nodes 0..m-1 = leaves (rank order), m.. = internal nodes in creation order
+    std::vector<uint64_t> weight(2 * m - 1);
+    std::vector<int> parent(2 * m - 1, -1);
+    for (int i = 0; i < m; i++) weight[i] = hist[ranked[i]];
+    int leaf = 0, inner = m, next = m;
+    auto pop = [&]() {
+        bool take_leaf = leaf < m && (inner >= next || weight[leaf] <= weight[inner]);
+        return take_leaf ? leaf++ : inner++;
+    };
+    while (next < 2 * m - 1) {
+        int a = pop();
+        int b = pop();
+        weight[next] = weight[a] + weight[b];
+        parent[a] = parent[b] = next;
+        next++;
+    }
+    std::vector<uint8_t> depth(2 * m - 1, 0);
+    for (int v = 2 * m - 3; v >= 0; v--) depth[v] = (uint8_t)std::min(255, depth[parent[v]] + 1);
+    for (int i = 0; i < m; i++) len[ranked[i]] = depth[i];
+}
+
+// Package-merge with cap L (R4): level lists built bottom-up; an item is a leaf (rank r) or a package
+// of two consecutive items of the list below.  Selection of the first 2(|S|-1) items of the top list
+// is pushed down level by level.
+void package_merge_lengths(const uint64_t hist[256], const std::vector<int> &ranked, int cap, uint8_t len[256]) {
+    const int m = (int)ranked.size();
+    std::memset(len, 0, 256);
+    if (m == 0) return;
+    if (m == 1) { len[ranked[0]] = 1; return; }
+    struct Item { uint64_t w; int leaf; int child; };   // leaf >= 0: leaf rank; else package of list[child], list[child+1]
+    std::vector<std::vector<Item>> lists(cap);
+    lists[0].reserve(m);
+    for (int r = 0; r < m; r++) lists[0].push_back({hist[ranked[r]], r, -1});
+    for (int lvl = 1; lvl < cap; lvl++) {
+        const std::vector<Item> &below = lists[lvl - 1];
+        std::vector<Item> &cur = lists[lvl];
+        cur.reserve(m + below.size() / 2);
+        size_t npk = below.size() / 2;
+        size_t li = 0, pi = 0;
+        while (li < (size_t)m || pi < npk) {
+            uint64_t pw = pi < npk ? below[2 * pi].w + below[2 * pi + 1].w : 0;
+            if (pi >= npk || (li < (size_t)m && hist[ranked[li]] <= pw)) {
+                cur.push_back({hist[ranked[li]], (int)li, -1});
+                li++;
+            } else {
+                cur.push_back({pw, -1, (int)(2 * pi)});
+                pi++;
+            }
+        }
+    }
+    // selection mask, top level first
+    std::vector<char> sel(lists[cap - 1].size(), 0);
+    size_t take = std::min<size_t>(2 * (size_t)(m - 1), sel.size());
+    std::fill(sel.begin(), sel.begin() + take, 1);
+    std::vector<int> count(m, 0);
+    for (int lvl = cap - 1; lvl >= 0; lvl--) {
+        const std::vector<Item> &cur = lists[lvl];
+        std::vector<char> below_sel(lvl > 0 ? lists[lvl - 1].size() : 0, 0);
+        for (size_t i = 0; i < cur.size(); i++) {
+            if (!sel[i]) continue;
+            if (cur[i].leaf >= 0) count[cur[i].leaf]++;
+            else { below_sel[cur[i].child] = 1; below_sel[cur[i].child + 1] = 1; }
+        }
+        sel.swap(below_sel);
+    }
+    for (int r = 0; r < m; r++) len[ranked[r]] = (uint8_t)count[r];
+}
+
+// ------------------------------------------------------------------------------------ canonical codes
+void canonical_codes(const uint8_t len[256], uint32_t code[256]) {
+    std::memset(code, 0, 256 * sizeof(uint32_t));
+    uint32_t bl_count[kMaxCodeLen + 1] = {};
+    for (int s = 0; s < 256; s++) if (len[s]) bl_count[len[s]]++;
+    // first code of each length (DEFLATE-style recurrence; equals the (length, symbol) sort rule)
+    uint32_t next_code[kMaxCodeLen + 2] = {};
+    uint64_t c = 0;
+    for (int l = 1; l <= kMaxCodeLen; l++) {
+        c = (c + bl_count[l - 1]) << 1;
+        next_code[l] = (uint32_t)c;
+    }
+    for (int s = 0; s < 256; s++) if (len[s]) code[s] = next_code[len[s]]++;
+}
+
+// ------------------------------------------------------------------------------------ LUTs
+// Explicit code tree, then every table enumerates the 256 8-bit paths from its subtree root.
+struct Tree {
+    std::vector<int> child0, child1, symbol;   // symbol >= 0 at leaves
+    int add() { child0.push_back(-1); child1.push_back(-1); symbol.push_back(-1); return (int)symbol.size() - 1; }
+};
+
+df11_status build_luts(const uint8_t len[256], const uint32_t code[256], int lut_mode,
+                       std::vector<uint8_t> &out, uint32_t &k, uint32_t &entry_bytes) {
+    out.clear();
+    k = 0;
+    entry_bytes = 1;
+    int nsym = 0, only = -1;
+    bool reserved = false;
+    for (int s = 0; s < 256; s++) if (len[s]) { nsym++; only = s; if (s >= 240) reserved = true; }
+    if (nsym == 0) return DF11_OK;
+    Tree tree;
+    int root = tree.add();
+    for (int s = 0; s < 256; s++) {
+        if (!len[s]) continue;
+        int v = root;
+        for (int i = len[s] - 1; i >= 0; i--) {
+            int bit = (code[s] >> i) & 1;
+            int nxt = bit ? tree.child1[v] : tree.child0[v];
+            if (nxt < 0) {
+                nxt = tree.add();                                  // may reallocate: index afresh
+                (bit ? tree.child1 : tree.child0)[v] = nxt;
+            }
+            v = nxt;
+        }
+        tree.symbol[v] = s;
+    }
+    // tables: BFS queue of subtree roots; entry value: >= 0 symbol, < 0 => -(child table index)
+    std::vector<int> table_root{root};
+    std::vector<int> entries;
+    for (size_t t = 0; t < table_root.size(); t++) {
+        for (int idx = 0; idx < 256; idx++) {
+            int v = table_root[t];
+            int val = INT32_MIN;
+            for (int bit = 7; bit >= 0 && val == INT32_MIN; bit--) {
+                int b = (idx >> bit) & 1;
+                int nv = b ? tree.child1[v] : tree.child0[v];
+                if (nv < 0) { val = only; break; }           // unreachable: only when |S| = 1 (R7)
+                v = nv;
+                if (tree.symbol[v] >= 0) val = tree.symbol[v];
+            }
+            if (val == INT32_MIN) {                          // still inside the tree after 8 bits
+                int j = -1;
+                for (size_t q = t + 1; q < table_root.size(); q++) if (table_root[q] == v) { j = (int)q; break; }
+                if (j < 0) { table_root.push_back(v); j = (int)table_root.size() - 1; }
+                val = -j;
+            }
+            entries.push_back(val);
+        }
+    }
+    k = (uint32_t)table_root.size();
+    bool narrow_ok = !reserved && k - 1 <= 16;
+    bool wide;
+    if (lut_mode == DF11_LUT_NARROW) {
+        if (reserved) return DF11_E_RESERVED_EXPONENT;
+        if (k - 1 > 16) return DF11_E_LUT_OVERFLOW;
+        wide = false;
+    } else if (lut_mode == DF11_LUT_WIDE) {
+        wide = true;
+    } else {
+        wide = !narrow_ok;
+    }
+    entry_bytes = wide ? 2 : 1;
+    out.resize((size_t)k * 256 * entry_bytes);
+    for (size_t i = 0; i < entries.size(); i++) {
+        int e = entries[i];
+        uint32_t v = e >= 0 ? (uint32_t)e : (wide ? 256u + (uint32_t)(-e) : 256u - (uint32_t)(-e));
+        if (wide) { out[2 * i] = (uint8_t)(v & 0xFF); out[2 * i + 1] = (uint8_t)(v >> 8); }
+        else out[i] = (uint8_t)v;
+    }
+    return DF11_OK;
+}
+
+// ------------------------------------------------------------------------------------ codebook
+struct Codebook {
+    uint8_t len[256];
+    uint32_t code[256];
+    uint32_t max_len;
+    std::vector<uint8_t> luts;
+    uint32_t k, entry_bytes;
+};
+
+df11_status make_codebook(const uint64_t hist[256], int lut_mode, Codebook &cb) {
+    std::vector<int> ranked = ranked_symbols(hist);
+    huffman_lengths(hist, ranked, cb.len);
+    cb.max_len = 0;
+    for (int s = 0; s < 256; s++) cb.max_len = std::max<uint32_t>(cb.max_len, cb.len[s]);
+    if (cb.max_len > kMaxCodeLen) {
+        package_merge_lengths(hist, ranked, kMaxCodeLen, cb.len);
+        cb.max_len = 0;
+        for (int s = 0; s < 256; s++) cb.max_len = std::max<uint32_t>(cb.max_len, cb.len[s]);
+    }
+    canonical_codes(cb.len, cb.code);
+    return build_luts(cb.len, cb.code, lut_mode, cb.luts, cb.k, cb.entry_bytes);
+}
+
+// ------------------------------------------------------------------------------------ packing
+inline void or_byte(uint8_t *p, uint8_t v) { __atomic_fetch_or(p, v, __ATOMIC_RELAXED); }
+
+df11_status encode_with_codebook(const uint16_t *w, uint64_t n, uint32_t T, uint32_t nb, const Codebook &cb,
+                                 const Pool &pool, df11_host_tensor *out) {
+    df11_host_tensor r;
+    std::memset(&r, 0, sizeof(r));
+    r.num_elements = n;
+    r.T = T;
+    r.n = nb;
+    std::memcpy(r.code_lengths, cb.len, 256);
+    r.k = cb.k;
+    r.lut_entry_bytes = cb.entry_bytes;
+    r.max_code_len = cb.max_len;
+
+    // per-thread bit totals -> exclusive prefix (bit offset of each segment)
+    const unsigned P = pool.nthreads;
+    std::vector<uint64_t> seg_bits(P + 1, 0);
+    pool.run(n, [&](unsigned t, uint64_t b, uint64_t e) {
+        uint64_t acc = 0;
+        for (uint64_t i = b; i < e; i++) acc += cb.len[(w[i] >> 7) & 0xFF];
+        seg_bits[t + 1] = acc;
+    });
+    for (unsigned t = 0; t < P; t++) seg_bits[t + 1] += seg_bits[t];
+    const uint64_t total_bits = seg_bits[P];
+    const uint64_t chunk_bits = 8ull * nb, block_bits = chunk_bits * T;
+    const uint64_t B64 = (total_bits + block_bits - 1) / block_bits;
+    if (B64 > 0xFFFFFFFFull) return DF11_E_TOO_LARGE;
+    const uint32_t B = (uint32_t)B64;
+    r.B = B;
+    r.encoded_bits = total_bits;
+
+    r.luts_bytes = cb.luts.size();
+    r.encoded_exponent_bytes = (uint64_t)B * T * nb + 16;
+    r.packed_sign_mantissa_bytes = roundup(n, 16) + 16;
+    r.gaps_bytes = roundup((5ull * B * T + 7) / 8, 16) + 16;
+    r.luts = (uint8_t *)std::calloc(std::max<uint64_t>(r.luts_bytes, 1), 1);
+    r.encoded_exponent = (uint8_t *)std::calloc(r.encoded_exponent_bytes, 1);
+    r.packed_sign_mantissa = (uint8_t *)std::calloc(r.packed_sign_mantissa_bytes, 1);
+    r.gaps = (uint8_t *)std::calloc(r.gaps_bytes, 1);
+    r.block_output_pos = (uint32_t *)std::calloc((size_t)B + 1, sizeof(uint32_t));
+    std::vector<uint8_t> gap_vals((size_t)B * T, 0);
+    if (!r.luts || !r.encoded_exponent || !r.packed_sign_mantissa || !r.gaps || !r.block_output_pos) {
+        df11_host_tensor_free(&r);
+        return DF11_E_ALLOC;
+    }
+    if (r.luts_bytes) std::memcpy(r.luts, cb.luts.data(), r.luts_bytes);
+
+    uint8_t *stream = r.encoded_exponent;
+    uint8_t *psm = r.packed_sign_mantissa;
+    uint32_t *bop = r.block_output_pos;
+    const uint64_t nthreads_fmt = (uint64_t)B * T;
+    pool.run(n, [&](unsigned t, uint64_t b, uint64_t e) {
+        if (b >= e) return;
+        uint64_t bit = seg_bits[t];
+        // bit packer: acc holds `nacc` pending bits left-aligned in the low 64; emit whole bytes
+        uint64_t byte_pos = bit >> 3;
+        uint64_t acc = 0;
+        int nacc = (int)(bit & 7);             // leading bits belong to the previous segment (zeros here)
+        bool first_byte = true;
+        // gaps/BOP: chunks whose first codeword start lies in this segment
+        uint64_t prev_start = (b == 0) ? 0 : bit - cb.len[(w[b - 1] >> 7) & 0xFF];
+        uint64_t next_chunk = (b == 0) ? 0 : prev_start / chunk_bits + 1;
+        uint64_t next_block = (b == 0) ? 0 : prev_start / block_bits + 1;
+        for (uint64_t i = b; i < e; i++) {
+            const uint16_t word = w[i];
+            const uint8_t ex = (uint8_t)((word >> 7) & 0xFF);
+            psm[i] = (uint8_t)(((word >> 8) & 0x80) | (word & 0x7F));
+            // first codeword start at or after chunk / block boundaries
+            while (next_chunk < nthreads_fmt && next_chunk * chunk_bits <= bit) {
+                uint64_t gap = bit - next_chunk * chunk_bits;
+                gap_vals[next_chunk] = gap < chunk_bits ? (uint8_t)gap : 0;
+                next_chunk++;
+            }
+            while (next_block < B && next_block * block_bits <= bit) bop[next_block++] = (uint32_t)i;
+            const int l = cb.len[ex];
+            acc = (acc << l) | cb.code[ex];
+            nacc += l;
+            bit += l;
+            while (nacc >= 8) {
+                uint8_t v = (uint8_t)(acc >> (nacc - 8));
+                if (first_byte) { or_byte(stream + byte_pos, v); first_byte = false; }
+                else stream[byte_pos] = v;
+                byte_pos++;
+                nacc -= 8;
+            }
+            acc &= (nacc ? ((1ull << nacc) - 1) : 0);
+        }
+        if (nacc > 0) or_byte(stream + byte_pos, (uint8_t)(acc << (8 - nacc)));
+    });
+    // chunks / blocks past the last codeword start
+    {
+        // last start = total_bits - len(last)
+        uint64_t last_start = n ? total_bits - cb.len[(w[n - 1] >> 7) & 0xFF] : 0;
+        (void)last_start;
+        for (uint32_t b = 0; b < B; b++) if (b > 0 && bop[b] == 0 && (uint64_t)b * block_bits > last_start) bop[b] = (uint32_t)n;
+        bop[B] = (uint32_t)n;
+    }
+    // pack gaps: 8 fields = 40 bits = 5 bytes, MSB-first
+    Pool gpool(pool.nthreads, nthreads_fmt);
+    uint64_t groups = (nthreads_fmt + 7) / 8;
+    gpool.run(groups, [&](unsigned, uint64_t gb, uint64_t ge) {
+        for (uint64_t q = gb; q < ge; q++) {
+            uint64_t v = 0;
+            for (int j = 0; j < 8; j++) {
+                uint64_t g = q * 8 + j;
+                v = (v << 5) | (g < nthreads_fmt ? (gap_vals[g] & 31u) : 0u);
+            }
+            for (int j = 0; j < 5; j++) {
+                uint64_t at = q * 5 + j;
+                if (at < r.gaps_bytes) r.gaps[at] = (uint8_t)(v >> (32 - 8 * j));
+            }
+        }
+    });
+    *out = r;
+    return DF11_OK;
+}
+
+df11_status check_opts(const df11_encode_opts *opts, df11_encode_opts &o) {
+    o.threads_per_block = 256;
+    o.bytes_per_thread = 8;
+    o.lut_mode = DF11_LUT_AUTO;
+    o.num_threads = 0;
+    if (opts) o = *opts;
+    if (o.threads_per_block < 32 || o.threads_per_block > 1024 || o.threads_per_block % 32)
+        return df11_fail(DF11_E_INVALID_ARGUMENT, "threads_per_block must be a multiple of 32 in [32, 1024]");
+    if (o.bytes_per_thread < 4 || o.bytes_per_thread > 32)
+        return df11_fail(DF11_E_INVALID_ARGUMENT, "bytes_per_thread must be in [4, 32]");
+    if (o.lut_mode > DF11_LUT_WIDE) return df11_fail(DF11_E_INVALID_ARGUMENT, "bad lut_mode");
+    return DF11_OK;
+}
+
+}  // namespace
+
+extern "C" df11_status df11_encode(const uint16_t *bf16, uint64_t n_elems, const df11_encode_opts *opts,
+                                   df11_host_tensor *out) {
+    if (!out) return df11_fail(DF11_E_INVALID_ARGUMENT, "out is NULL");
+    std::memset(out, 0, sizeof(*out));
+    if (!bf16 && n_elems) return df11_fail(DF11_E_INVALID_ARGUMENT, "bf16 is NULL");
+    df11_encode_opts o;
+    df11_status st = check_opts(opts, o);
+    if (st != DF11_OK) return st;
+    if (n_elems >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "N >= 2^32 (BlockOutputPos is uint32)");
+    try {
+        Pool pool(o.num_threads, n_elems);
+        uint64_t hist[256];
+        histogram(bf16, n_elems, pool, hist);
+        Codebook cb;
+        st = make_codebook(hist, (int)o.lut_mode, cb);
+        if (st != DF11_OK) return df11_fail(st, st == DF11_E_RESERVED_EXPONENT ? "exponent >= 240 with NARROW LUTs"
+                                                                          : "more than 16 child LUTs with NARROW LUTs");
+        return encode_with_codebook(bf16, n_elems, o.threads_per_block, o.bytes_per_thread, cb, pool, out);
+    } catch (const std::bad_alloc &) {
+        return df11_fail(DF11_E_ALLOC, "host allocation failed");
+    }
+}
+
+extern "C" df11_status df11_encode_group(const uint16_t *const *tensors, const uint64_t *n_elems, uint32_t count,
+                                         const df11_encode_opts *opts, int shared_codebook, df11_host_tensor *outs) {
+    if (!outs || (count && (!tensors || !n_elems))) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL argument");
+    for (uint32_t i = 0; i < count; i++) std::memset(&outs[i], 0, sizeof(outs[i]));
+    if (!shared_codebook) {
+        for (uint32_t i = 0; i < count; i++) {
+            df11_status st = df11_encode(tensors[i], n_elems[i], opts, &outs[i]);
+            if (st != DF11_OK) {
+                for (uint32_t j = 0; j < i; j++) df11_host_tensor_free(&outs[j]);
+                return st;
+            }
+        }
+        return DF11_OK;
+    }
+    df11_encode_opts o;
+    df11_status st = check_opts(opts, o);
+    if (st != DF11_OK) return st;
+    try {
+        uint64_t hist[256] = {};
+        uint64_t total = 0;
+        for (uint32_t i = 0; i < count; i++) {
+            if (!tensors[i] && n_elems[i]) return df11_fail(DF11_E_INVALID_ARGUMENT, "tensor pointer is NULL");
+            if (n_elems[i] >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "N >= 2^32");
+            Pool pool(o.num_threads, n_elems[i]);
+            uint64_t h[256];
+            histogram(tensors[i], n_elems[i], pool, h);
+            for (int s = 0; s < 256; s++) hist[s] += h[s];
+            total += n_elems[i];
+        }
+        Codebook cb;
+        st = make_codebook(hist, (int)o.lut_mode, cb);
+        if (st != DF11_OK) return df11_fail(st, "shared codebook not representable with NARROW LUTs");
+        for (uint32_t i = 0; i < count; i++) {
+            Pool pool(o.num_threads, n_elems[i]);
+            st = encode_with_codebook(tensors[i], n_elems[i], o.threads_per_block, o.bytes_per_thread, cb, pool, &outs[i]);
+            if (st != DF11_OK) {
+                for (uint32_t j = 0; j < i; j++) df11_host_tensor_free(&outs[j]);
+                return df11_fail(st, "group encode failed");
+            }
+        }
+        (void)total;
+        return DF11_OK;
+    } catch (const std::bad_alloc &) {
+        return df11_fail(DF11_E_ALLOC, "host allocation failed");
+    }
+}
+
+extern "C" void df11_host_tensor_free(df11_host_tensor *t) {
+    if (!t) return;
+    std::free(t->luts);
+    std::free(t->encoded_exponent);
+    std::free(t->packed_sign_mantissa);
+    std::free(t->gaps);
+    std::free(t->block_output_pos);
+    std::memset(t, 0, sizeof(*t));
+}

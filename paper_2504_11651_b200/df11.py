@@ -1,0 +1,343 @@
+"""Thin Python binding of the C ABI in include/df11.h (argument marshalling only).
+
+Every step of encode and decode runs in libdf11.so (host encoder in C++, decode in sm_100a CUDA
+kernels).  PyTorch only provides device memory and the current CUDA stream.  There is no fallback:
+if the library is missing the import fails loudly.
+
+Names follow the C ABI: encode / encode_group / decompress / decompress_block / decompress_host.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdf11.so")
+
+DF11_OK = 0
+STATUS = {0: "DF11_OK", 1: "DF11_E_INVALID_ARGUMENT", 2: "DF11_E_RESERVED_EXPONENT", 3: "DF11_E_LUT_OVERFLOW",
+          4: "DF11_E_TOO_LARGE", 5: "DF11_E_CORRUPT", 6: "DF11_E_CUDA", 7: "DF11_E_ALLOC", 8: "DF11_E_UNSUPPORTED"}
+LUT_MODES = {"auto": 0, "narrow": 1, "wide": 2}
+KERNELS = {"auto": 0, "alg1": 1, "fast": 2}
+MAX_BATCH = 64
+
+EXPORTED_SYMBOLS = ("df11_encode", "df11_encode_group", "df11_host_tensor_free", "df11_decompress",
+                    "df11_decompress_block", "df11_decompress_block_ex", "df11_decompress_host",
+                    "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
+                    "df11_launch_count")
+
+
+class Df11Error(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.kind = STATUS.get(status, str(status))
+
+
+class EncodeOpts(ctypes.Structure):
+    _fields_ = [("threads_per_block", ctypes.c_uint32), ("bytes_per_thread", ctypes.c_uint32),
+                ("lut_mode", ctypes.c_uint32), ("num_threads", ctypes.c_uint32)]
+
+
+class HostTensorC(ctypes.Structure):
+    _fields_ = [("num_elements", ctypes.c_uint64), ("encoded_bits", ctypes.c_uint64),
+                ("T", ctypes.c_uint32), ("n", ctypes.c_uint32), ("B", ctypes.c_uint32), ("k", ctypes.c_uint32),
+                ("lut_entry_bytes", ctypes.c_uint32), ("max_code_len", ctypes.c_uint32),
+                ("code_lengths", ctypes.c_uint8 * 256),
+                ("luts", ctypes.POINTER(ctypes.c_uint8)), ("luts_bytes", ctypes.c_uint64),
+                ("encoded_exponent", ctypes.POINTER(ctypes.c_uint8)), ("encoded_exponent_bytes", ctypes.c_uint64),
+                ("packed_sign_mantissa", ctypes.POINTER(ctypes.c_uint8)),
+                ("packed_sign_mantissa_bytes", ctypes.c_uint64),
+                ("gaps", ctypes.POINTER(ctypes.c_uint8)), ("gaps_bytes", ctypes.c_uint64),
+                ("block_output_pos", ctypes.POINTER(ctypes.c_uint32))]
+
+
+class DeviceTensorC(ctypes.Structure):
+    _fields_ = [("encoded_exponent", ctypes.c_void_p), ("packed_sign_mantissa", ctypes.c_void_p),
+                ("gaps", ctypes.c_void_p), ("luts", ctypes.c_void_p), ("code_lengths", ctypes.c_void_p),
+                ("block_output_pos", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("num_elements", ctypes.c_uint64), ("T", ctypes.c_uint32), ("n", ctypes.c_uint32),
+                ("B", ctypes.c_uint32), ("k", ctypes.c_uint32), ("lut_entry_bytes", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(_LIB_PATH)
+        P, U32, U64 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64
+        L.df11_encode.argtypes = [P, U64, ctypes.POINTER(EncodeOpts), ctypes.POINTER(HostTensorC)]
+        L.df11_encode_group.argtypes = [ctypes.POINTER(P), ctypes.POINTER(U64), U32, ctypes.POINTER(EncodeOpts),
+                                        ctypes.c_int, ctypes.POINTER(HostTensorC)]
+        L.df11_host_tensor_free.argtypes = [ctypes.POINTER(HostTensorC)]
+        L.df11_decompress.argtypes = [ctypes.POINTER(DeviceTensorC), P]
+        L.df11_decompress_block.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P]
+        L.df11_decompress_block_ex.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P, ctypes.c_int]
+        L.df11_decompress_host.argtypes = [ctypes.POINTER(HostTensorC), ctypes.POINTER(DeviceTensorC), P, P]
+        for f in ("df11_encode", "df11_encode_group", "df11_decompress", "df11_decompress_block",
+                  "df11_decompress_block_ex", "df11_decompress_host"):
+            getattr(L, f).restype = ctypes.c_int
+        L.df11_status_string.argtypes = [ctypes.c_int]
+        L.df11_status_string.restype = ctypes.c_char_p
+        L.df11_last_error_message.restype = ctypes.c_char_p
+        L.df11_version.restype = ctypes.c_char_p
+        L.df11_launch_count.argtypes = [ctypes.c_int]
+        L.df11_launch_count.restype = ctypes.c_uint64
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != DF11_OK:
+        raise Df11Error(status, lib().df11_last_error_message().decode())
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().df11_launch_count(1 if reset else 0))
+
+
+# --------------------------------------------------------------------------- host side
+class HostTensor:
+    """A DF11 tensor in host memory (library-owned arrays exposed as numpy views)."""
+
+    def __init__(self, c: HostTensorC, shape):
+        self._c = c
+        self.shape = tuple(shape)
+
+    def __del__(self):
+        try:
+            lib().df11_host_tensor_free(ctypes.byref(self._c))
+        except Exception:
+            pass
+
+    def _arr(self, name, count, dtype=np.uint8):
+        p = getattr(self._c, name)
+        if count == 0 or not p:
+            return np.zeros(0, dtype)
+        return np.ctypeslib.as_array(p, shape=(count,)).view(dtype) if dtype is np.uint8 else \
+            np.ctypeslib.as_array(p, shape=(count,))
+
+    num_elements = property(lambda s: int(s._c.num_elements))
+    encoded_bits = property(lambda s: int(s._c.encoded_bits))
+    T = property(lambda s: int(s._c.T))
+    n = property(lambda s: int(s._c.n))
+    B = property(lambda s: int(s._c.B))
+    k = property(lambda s: int(s._c.k))
+    lut_entry_bytes = property(lambda s: int(s._c.lut_entry_bytes))
+    max_code_len = property(lambda s: int(s._c.max_code_len))
+
+    @property
+    def code_lengths(self):
+        return np.frombuffer(bytes(self._c.code_lengths), np.uint8).copy()
+
+    @property
+    def luts(self):
+        return self._arr("luts", int(self._c.luts_bytes))
+
+    @property
+    def encoded_exponent(self):
+        return self._arr("encoded_exponent", int(self._c.encoded_exponent_bytes))
+
+    @property
+    def packed_sign_mantissa(self):
+        return self._arr("packed_sign_mantissa", int(self._c.packed_sign_mantissa_bytes))
+
+    @property
+    def gaps(self):
+        return self._arr("gaps", int(self._c.gaps_bytes))
+
+    @property
+    def block_output_pos(self):
+        return self._arr("block_output_pos", self.B + 1, np.uint32)
+
+    def compressed_bytes(self) -> int:
+        """Bytes the method must read to rebuild the tensor (stream + sign/mantissa + 5-bit gaps +
+        BlockOutputPos + LUTs + CodeLengths), excluding alignment padding."""
+        return ((self.encoded_bits + 7) // 8 + self.num_elements + (5 * self.B * self.T + 7) // 8
+                + 4 * (self.B + 1) + self.k * 256 * self.lut_entry_bytes + 256)
+
+    def arrays(self) -> dict:
+        return dict(code_lengths=self.code_lengths, luts=self.luts, encoded_exponent=self.encoded_exponent,
+                    packed_sign_mantissa=self.packed_sign_mantissa, gaps=self.gaps,
+                    block_output_pos=self.block_output_pos)
+
+
+def _as_u16(w) -> np.ndarray:
+    try:
+        import torch
+        if isinstance(w, torch.Tensor):
+            if w.is_cuda:
+                raise ValueError("df11.encode takes a host tensor")
+            w = w.contiguous()
+            if w.dtype == torch.bfloat16:
+                w = w.view(torch.int16)
+            return w.numpy().view(np.uint16)
+    except ImportError:
+        pass
+    return np.ascontiguousarray(w).view(np.uint16)
+
+
+def _opts(T, n, lut_mode, num_threads):
+    return EncodeOpts(T, n, LUT_MODES[lut_mode], num_threads)
+
+
+def encode(w, T: int = 256, n: int = 8, lut_mode: str = "auto", num_threads: int = 0) -> HostTensor:
+    """df11_encode: BF16 host tensor (torch.bfloat16 or uint16 bit patterns) -> HostTensor."""
+    a = _as_u16(w)
+    shape = a.shape
+    a = a.reshape(-1)
+    c = HostTensorC()
+    o = _opts(T, n, lut_mode, num_threads)
+    _check(lib().df11_encode(ctypes.c_void_p(a.ctypes.data if a.size else 0), a.size, ctypes.byref(o),
+                             ctypes.byref(c)))
+    return HostTensor(c, shape)
+
+
+def encode_group(ws, T: int = 256, n: int = 8, lut_mode: str = "auto", shared_codebook: bool = False,
+                 num_threads: int = 0):
+    arrs = [_as_u16(w) for w in ws]
+    shapes = [a.shape for a in arrs]
+    flat = [a.reshape(-1) for a in arrs]
+    cnt = len(flat)
+    ptrs = (ctypes.c_void_p * cnt)(*[a.ctypes.data if a.size else None for a in flat])
+    ns = (ctypes.c_uint64 * cnt)(*[a.size for a in flat])
+    outs = (HostTensorC * cnt)()
+    o = _opts(T, n, lut_mode, num_threads)
+    _check(lib().df11_encode_group(ptrs, ns, cnt, ctypes.byref(o), 1 if shared_codebook else 0, outs))
+    res = []
+    for i in range(cnt):
+        c = HostTensorC()
+        ctypes.memmove(ctypes.byref(c), ctypes.byref(outs[i]), ctypes.sizeof(HostTensorC))
+        res.append(HostTensor(c, shapes[i]))
+    return res
+
+
+# --------------------------------------------------------------------------- device side
+class DeviceTensor:
+    """Device-resident DF11 tensor: torch uint8/int32 buffers + the C descriptor pointing at them."""
+
+    def __init__(self, h: HostTensor, device="cuda", out=None):
+        m = dict(num_elements=h.num_elements, T=h.T, n=h.n, B=h.B, k=h.k, lut_entry_bytes=h.lut_entry_bytes,
+                 encoded_bits=h.encoded_bits, max_code_len=h.max_code_len)
+        self._init(m, h.arrays(), h.shape, device, out)
+
+    @classmethod
+    def from_arrays(cls, meta: dict, arrays: dict, shape=None, device="cuda", out=None) -> "DeviceTensor":
+        """Upload DF11 arrays given as numpy (e.g. read from disk): keys code_lengths, luts,
+        encoded_exponent, packed_sign_mantissa, gaps, block_output_pos; meta: num_elements, T, n, B, k,
+        lut_entry_bytes, encoded_bits, max_code_len."""
+        self = cls.__new__(cls)
+        self._init(meta, arrays, shape if shape is not None else (int(meta["num_elements"]),), device, out)
+        return self
+
+    def _init(self, meta, a, shape, device, out):
+        import torch
+        dev = torch.device(device)
+        self.shape = tuple(shape)
+        self.num_elements = int(meta["num_elements"])
+        self.meta = {k: int(meta[k]) for k in ("T", "n", "B", "k", "lut_entry_bytes", "encoded_bits",
+                                               "max_code_len")}
+        B, T = self.meta["B"], self.meta["T"]
+        self.compressed_bytes = ((self.meta["encoded_bits"] + 7) // 8 + self.num_elements + (5 * B * T + 7) // 8
+                                 + 4 * (B + 1) + int(np.asarray(a["luts"]).size) + 256)
+
+        def up(x):
+            t = torch.from_numpy(np.ascontiguousarray(x).view(np.uint8).copy())
+            return t.to(dev, non_blocking=False)
+
+        luts = np.asarray(a["luts"])
+        self.encoded_exponent = up(a["encoded_exponent"])
+        self.packed_sign_mantissa = up(a["packed_sign_mantissa"])
+        self.gaps = up(a["gaps"])
+        self.luts = up(luts if luts.size else np.zeros(16, np.uint8))
+        self.code_lengths = up(a["code_lengths"])
+        self.block_output_pos = up(np.asarray(a["block_output_pos"], np.uint32).view(np.uint8))
+        self.out = out if out is not None else torch.empty(max(self.num_elements, 1), dtype=torch.bfloat16,
+                                                           device=dev)
+
+    def descriptor(self, out=None) -> DeviceTensorC:
+        o = self.out if out is None else out
+        if o.numel() < self.num_elements or o.dtype not in _u16_dtypes():
+            raise ValueError("output buffer too small or not 16-bit")
+        m = self.meta
+        return DeviceTensorC(self.encoded_exponent.data_ptr(), self.packed_sign_mantissa.data_ptr(),
+                             self.gaps.data_ptr(), self.luts.data_ptr(), self.code_lengths.data_ptr(),
+                             self.block_output_pos.data_ptr(), o.data_ptr(), self.num_elements,
+                             m["T"], m["n"], m["B"], m["k"], m["lut_entry_bytes"], 0)
+
+    def staging_bytes(self) -> int:
+        return sum(int(t.numel()) for t in (self.encoded_exponent, self.packed_sign_mantissa, self.gaps,
+                                            self.luts, self.code_lengths, self.block_output_pos))
+
+
+def _u16_dtypes():
+    import torch
+    return (torch.bfloat16, torch.int16, torch.uint16)
+
+
+def to_device(h: HostTensor, device="cuda", out=None) -> DeviceTensor:
+    return DeviceTensor(h, device, out)
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def decompress(dt: DeviceTensor, out=None, stream=None, kernel: str = "auto"):
+    """df11_decompress on the current (or given) stream; returns the BF16 tensor (shape restored)."""
+    d = dt.descriptor(out)
+    _check(lib().df11_decompress_block_ex(ctypes.byref(d), 1, _stream_ptr(stream), KERNELS[kernel]))
+    o = dt.out if out is None else out
+    return o[: dt.num_elements].view(dt.shape) if dt.num_elements else o[:0]
+
+
+class BlockPlan:
+    """Pre-marshalled descriptor array for repeated df11_decompress_block calls (no per-call Python
+    work beyond one ctypes call)."""
+
+    def __init__(self, dts, outs=None):
+        if len(dts) > MAX_BATCH:
+            raise ValueError("at most 64 tensors per block")
+        self.dts = list(dts)
+        self.outs = outs
+        self.arr = (DeviceTensorC * max(len(dts), 1))()
+        for i, dt in enumerate(self.dts):
+            self.arr[i] = dt.descriptor(None if outs is None else outs[i])
+        self.count = len(dts)
+
+    def run(self, stream=None, kernel: str = "auto"):
+        _check(lib().df11_decompress_block_ex(self.arr, self.count, _stream_ptr(stream), KERNELS[kernel]))
+
+    def outputs(self):
+        res = []
+        for i, dt in enumerate(self.dts):
+            o = dt.out if self.outs is None else self.outs[i]
+            res.append(o[: dt.num_elements].view(dt.shape))
+        return res
+
+
+def decompress_block(dts, outs=None, stream=None, kernel: str = "auto"):
+    """df11_decompress_block: every tensor of a transformer block in one launch."""
+    plan = BlockPlan(dts, outs)
+    plan.run(stream, kernel)
+    return plan.outputs()
+
+
+def decompress_host(h: HostTensor, dt: DeviceTensor, host_out, stream=None):
+    """df11_decompress_host: H2D of h's arrays into dt's buffers, decode, D2H into host_out."""
+    c_d = dt.descriptor()
+    _check(lib().df11_decompress_host(ctypes.byref(h._c), ctypes.byref(c_d),
+                                      ctypes.c_void_p(host_out.data_ptr()), _stream_ptr(stream)))
+    return host_out

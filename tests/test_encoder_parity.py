@@ -1,0 +1,134 @@
+"""Host encoder (libdf11.so df11_encode) vs the oracle, byte for byte (CPU only).
+
+The library encoder and oracle/ share no code; both implement DESIGN.md §2.  Every array of the DF11
+format must be identical, including the zero padding.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import workloads
+from paper_2504_11651_b200 import df11
+
+
+def _cmp(fmt, h):
+    assert h.num_elements == fmt["num_elements"]
+    assert h.encoded_bits == fmt["encoded_bits"]
+    assert (h.T, h.n, h.B, h.k) == (fmt["T"], fmt["n"], fmt["B"], fmt["k"])
+    assert h.lut_entry_bytes == fmt["lut_entry_bytes"] and h.max_code_len == fmt["max_code_len"]
+    a = h.arrays()
+    for key in ("code_lengths", "luts", "encoded_exponent", "packed_sign_mantissa", "gaps", "block_output_pos"):
+        assert np.array_equal(a[key], fmt[key]), key
+
+
+def test_library_exports_every_header_symbol():
+    """The C-ABI library loads and exports every function include/df11.h declares."""
+    import re
+    import os
+    hdr = open(os.path.join(os.path.dirname(df11.library_path()), "..", "..", "include", "df11.h")).read()
+    declared = set(re.findall(r"^(?:df11_status|void|int|uint64_t|const char)\s+\*?\s*(df11_\w+)\s*\(",
+                              hdr, flags=re.M))
+    L = ctypes.CDLL(df11.library_path())
+    for name in declared:
+        assert hasattr(L, name), name
+    assert declared == set(df11.EXPORTED_SYMBOLS)
+    assert df11.lib().df11_version().decode().startswith("df11-b200")
+
+
+@pytest.mark.parametrize("case", ["gauss_small", "gauss_ragged", "constant", "two_symbol", "all_patterns",
+                                  "overflow_wide", "fibonacci", "one", "empty"])
+def test_encoder_bytes_equal_oracle(oracle_mod, case):
+    rng = np.random.default_rng(3)
+    T, n = 256, 8
+    if case == "gauss_small":
+        w = workloads.gaussian_bf16((1 << 20,), seed=1)
+    elif case == "gauss_ragged":
+        w = workloads.gaussian_bf16((1234567,), seed=2, sigma=0.01)
+        T, n = 128, 16
+    elif case == "constant":
+        w = workloads.constant(200003)
+    elif case == "two_symbol":
+        w = workloads.from_exponent_histogram({100: 7000, 101: 3}, seed=1)
+    elif case == "all_patterns":
+        w = workloads.all_bf16_patterns()
+    elif case == "overflow_wide":
+        counts = {120: 1 << 18}
+        counts.update({e: 1 + e % 3 for e in range(1, 120)})
+        w = workloads.from_exponent_histogram(counts, seed=5)
+    elif case == "fibonacci":
+        w = workloads.from_exponent_histogram(workloads.fibonacci_histogram(34, 80), seed=1)
+        T, n = 64, 4
+    elif case == "one":
+        w = np.array([0xBF80], np.uint16)
+    else:
+        w = np.zeros(0, np.uint16)
+    fmt = oracle_mod.encode(w, T=T, n=n)
+    for threads in (1, 0):
+        h = df11.encode(w, T=T, n=n, num_threads=threads)
+        _cmp(fmt, h)
+
+
+def test_encoder_fuzz_vs_oracle(oracle_mod):
+    rng = np.random.default_rng(9)
+    geoms = [(32, 4), (64, 8), (256, 8), (512, 8), (96, 5), (1024, 16), (32, 32)]
+    for i in range(150):
+        N = int(rng.integers(1, 200000))
+        kind = i % 4
+        if kind == 0:
+            w = workloads.gaussian_bf16((N,), seed=100 + i, sigma=float(rng.choice([0.003, 0.02, 0.2])))
+        elif kind == 1:
+            w = rng.integers(0, 1 << 16, size=N, dtype=np.uint32).astype(np.uint16)
+        elif kind == 2:
+            nsym = int(rng.integers(1, 50))
+            counts = {int(e): int(c) for e, c in zip(rng.choice(256, nsym, replace=False),
+                                                    rng.geometric(0.05, nsym))}
+            w = workloads.from_exponent_histogram(counts, seed=i)
+        else:
+            w = workloads.constant(N, int(rng.integers(0, 1 << 16)))
+        T, n = geoms[i % len(geoms)]
+        fmt = oracle_mod.encode(w, T=T, n=n)
+        h = df11.encode(w, T=T, n=n, num_threads=int(rng.choice([0, 1, 3])))
+        _cmp(fmt, h)
+
+
+def test_encoder_errors(oracle_mod):
+    with pytest.raises(df11.Df11Error) as e:
+        df11.encode(workloads.all_bf16_patterns(), lut_mode="narrow")
+    assert e.value.kind == "DF11_E_RESERVED_EXPONENT"
+    counts = {120: 1 << 18}
+    counts.update({e: 1 + e % 3 for e in range(1, 120)})
+    with pytest.raises(df11.Df11Error) as e:
+        df11.encode(workloads.from_exponent_histogram(counts, seed=5), lut_mode="narrow")
+    assert e.value.kind == "DF11_E_LUT_OVERFLOW"
+    for T, n in ((33, 8), (2048, 8), (256, 3), (256, 33)):
+        with pytest.raises(df11.Df11Error) as e:
+            df11.encode(workloads.constant(10), T=T, n=n)
+        assert e.value.kind == "DF11_E_INVALID_ARGUMENT"
+    h = df11.encode(workloads.all_bf16_patterns(), lut_mode="wide")
+    assert h.lut_entry_bytes == 2
+
+
+def test_encode_group_shared_codebook(oracle_mod):
+    ts = workloads.config_tensors("flux_single_block")
+    small = [w.reshape(-1)[: 50000 + 7 * i] for i, (_, w) in enumerate(ts)]
+    hs = df11.encode_group(small, shared_codebook=True)
+    assert len({bytes(h.code_lengths) for h in hs}) == 1
+    # the shared codebook is the one the oracle builds from the concatenation
+    fmt = oracle_mod.encode(np.concatenate(small))
+    assert np.array_equal(hs[0].code_lengths, fmt["code_lengths"])
+    assert np.array_equal(hs[0].luts, fmt["luts"])
+    per = df11.encode_group(small, shared_codebook=False)
+    for w, h in zip(small, per):
+        _cmp(oracle_mod.encode(w), h)
+
+
+def test_encoder_speed_8b_block():
+    """The host encoder must keep setup practical: > 50 M elements/s."""
+    import time
+    w = workloads.gaussian_bf16((14336, 4096), seed=7)
+    t = time.perf_counter()
+    h = df11.encode(w)
+    dt = time.perf_counter() - t
+    assert h.num_elements == w.size
+    assert w.size / dt > 50e6, w.size / dt
