@@ -2,28 +2,26 @@
 //
 // Same result as Algorithm 1 — every thread decodes the codewords that start in its
 // 8-byte chunk, a block-level exclusive scan turns per-thread counts into output positions
-// (P:148-150), phase 2 re-decodes into an SRAM buffer and the block writes BF16 with coalesced stores
-// — re-designed for B200:
+// (P:148-150), phase 2 re-decodes into an SRAM buffer and BF16 leaves with coalesced stores —
+// re-designed for B200:
 //
 //  * Persistent CTAs, one per SM, 4 groups of 256 threads; group g of CTA c walks the format blocks
-//    ("tiles") of a contiguous range.  Each group owns a 16 KB exponent buffer and uses its own
-//    named barrier, so groups drift apart and hide each other's memory latency.
+//    ("tiles") of a contiguous range.  Each group owns a 16 KB exponent buffer and its own named
+//    barrier (one per tile), so groups drift apart and hide each other's latency.
 //  * Derived decode tables are built in SMEM once per (CTA, tensor) from the format's hierarchical
-//    LUTs: for every R-bit prefix (R = 9),
-//      T1 = {count of complete codes, their start mask, bits consumed}      (phase 1: counting)
-//      T2 = {up to 3 decoded exponents, their count, bits consumed}         (phase 2: decoding)
-//    Both are replicated 32x with lane-private banks (word = prefix*32 + lane): every LDS is
-//    conflict-free.  Codes longer than R bits (≈0.1 % on LLM-like weights) take the paper's LUT walk
-//    over the format tables (global, L1-resident) at a warp-uniform check every 4 steps.
-//  * The thread's 8-byte chunk + 4 spill bytes live in 3 registers (big-endian); the 32-bit decode
-//    window is a funnel shift — EncodedExponent is read from HBM exactly once (the paper re-reads it
-//    from SRAM in phase 2).
-//  * The next tile's chunk, gap and BlockOutputPos are prefetched into registers while the current
-//    tile decodes; the sign/mantissa bytes of the tile are prefetched with 128-bit loads before
-//    phase 1 and consumed by the merge.
-//  * Merge: 16 elements per thread per step: LDS.128 exponents + LDG.128 sign/mantissa -> 8 words of
-//    BF16 via byte permutes -> two 128-bit stores.  Head/tail groups shared with the neighbouring
-//    tiles are written element-wise (disjoint ownership, no races).
+//    LUTs.  For every R-bit prefix (R = 9):
+//      T1 = consumed | count << 16      (phase 1; every complete code in the R bits)
+//      T2 = s0 | s1 << 8 | s2 << 16 | count << 24 | consumed << 28   (phase 2; up to 3 exponents)
+//      SM = start mask of the T1 codes  (one lookup per thread per tile, for the chunk-end fixup)
+//    T1/T2 are replicated 32x with lane-private banks (word = prefix*32 + lane): conflict-free LDS.
+//    Codes longer than R bits (~0.1 % on LLM-like weights) leave the entry 0; the thread stalls on it
+//    and a warp-uniform check every 4 steps resolves it with the paper's LUT walk.
+//  * Phase 1 keeps (bit offset | count << 16) in ONE register and adds the T1 entry to it.
+//  * The thread's 8-byte chunk + 4 spill bytes live in 3 registers; the decode window is a funnel
+//    shift, so EncodedExponent is read from HBM exactly once.
+//  * One barrier per tile: the scan.  Each warp then merges its own contiguous output range (its 32
+//    threads' outputs are adjacent): 16 elements per lane-step, LDS.128 exponents + LDG.128
+//    sign/mantissa (prefetched before phase 2) -> PRMT sign-replicate compose -> 2x 128-bit stores.
 #include "decode_common.cuh"
 
 namespace df11 {
@@ -34,30 +32,52 @@ constexpr int kN = 8;                      // bytes per thread
 constexpr int kGroups = 4;
 constexpr int kCta = kT * kGroups;         // 1024 threads
 constexpr int kR = 9;                      // root bits of the derived tables
-constexpr int kTabWords = (1 << kR) * 32;  // 32 lane replicas
-constexpr int kExpBuf = 8 * kN * kT + 64;  // worst case 1-bit codes + head offset + spill
-constexpr size_t kSmemBytes = 2 * (size_t)kTabWords * 4 + (size_t)kGroups * kExpBuf + kGroups * 8 * 4;
+constexpr uint32_t kRows = 1u << kR;
+constexpr uint32_t kTabWords = kRows * 32; // 32 lane replicas
+constexpr uint32_t kExpBuf = 8 * kN * kT + 64;
 
-struct Smem {
-    uint32_t t1[kTabWords];
-    uint32_t t2[kTabWords];
-    uint8_t expbuf[kGroups][kExpBuf];
-    uint32_t wsum[kGroups][8];
-};
-static_assert(sizeof(Smem) == kSmemBytes, "smem layout");
+// SMEM layout (bytes)
+constexpr uint32_t kOffT1 = 0;
+constexpr uint32_t kOffT2 = kOffT1 + kTabWords * 4;
+constexpr uint32_t kOffSM = kOffT2 + kTabWords * 4;           // uint16[kRows]
+constexpr uint32_t kLutSmem = 8192;                           // format LUTs copied when they fit
+constexpr uint32_t kOffLut = kOffSM + kRows * 2;              // uint8/uint16 [k][256]
+constexpr uint32_t kOffLen = kOffLut + kLutSmem;              // CodeLengths[256]
+constexpr uint32_t kOffWsum = kOffLen + 256;                  // [groups][2 parities][8] uint32
+constexpr uint32_t kOffExp = kOffWsum + kGroups * 2 * 8 * 4;  // [groups][kExpBuf]
+constexpr uint32_t kChunkBytes = kT * kN + 16;                // a tile's EncodedExponent + spill
+constexpr uint32_t kGapBytes = kT * 5 / 8 + 16;               // a tile's 5-bit gaps (+ 1 byte read past)
+constexpr uint32_t kStageBytes = kChunkBytes + kGapBytes;     // one TMA stage
+constexpr uint32_t kOffStage = kOffExp + kGroups * kExpBuf;   // [groups][2][kStageBytes]
+constexpr uint32_t kOffMbar = kOffStage + kGroups * 2 * kStageBytes;   // [groups][2] uint64
+constexpr uint32_t kSmemBytes = kOffMbar + kGroups * 2 * 8;
+static_assert(kStageBytes % 16 == 0 && kOffStage % 16 == 0 && kOffMbar % 8 == 0, "TMA alignment");
+static_assert(kSmemBytes <= 232448, "SMEM budget");
+static_assert(kOffExp % 16 == 0 && kExpBuf % 16 == 0, "alignment");
+
+extern __shared__ __align__(16) uint32_t smem_w[];
+
+__device__ __forceinline__ uint8_t *smem_b() { return reinterpret_cast<uint8_t *>(smem_w); }
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
 // Paper's hierarchical LUT walk over the format tables in global memory; returns the
 // exponent and its code length.  Bounded: <= 4 levels, child < k, zero length -> 32.
-__device__ __forceinline__ uint32_t lut_walk(uint32_t w, const df11_device_tensor &ts, uint32_t &len) {
+__device__ __noinline__ uint32_t lut_walk(uint32_t w, const df11_device_tensor &ts, uint32_t &len) {
     const uint8_t *__restrict__ luts = ts.luts;
     const uint32_t eb = ts.lut_entry_bytes, thr = eb == 1 ? 240u : 256u;
     uint32_t table = 0, e = 0;
 #pragma unroll 1
     for (int i = 0; i < 4; i++) {
-        uint32_t off = table * 256u + ((w >> (24 - 8 * i)) & 0xFFu);
-        e = eb == 1 ? (uint32_t)__ldg(luts + off) : ((uint32_t)__ldg(luts + 2 * off) | ((uint32_t)__ldg(luts + 2 * off + 1) << 8));
+        const uint32_t off = table * 256u + ((w >> (24 - 8 * i)) & 0xFFu);
+        e = eb == 1 ? (uint32_t)__ldg(luts + off)
+                    : ((uint32_t)__ldg(luts + 2 * off) | ((uint32_t)__ldg(luts + 2 * off + 1) << 8));
         if (e < thr) break;
         table = eb == 1 ? 256u - e : e - 256u;
         if (table >= ts.k || i == 3) { e = 0; break; }
@@ -68,56 +88,114 @@ __device__ __forceinline__ uint32_t lut_walk(uint32_t w, const df11_device_tenso
     return e;
 }
 
+// Same walk over the SMEM copy of the format tables (used when k*256*entry_bytes <= kLutSmem).
+__device__ __forceinline__ uint32_t lut_walk_smem(uint32_t w, const uint8_t *lut, const uint8_t *clen,
+                                                  uint32_t eb, uint32_t k, uint32_t &len) {
+    const uint32_t thr = eb == 1 ? 240u : 256u;
+    uint32_t e = eb == 1 ? lut[w >> 24] : reinterpret_cast<const uint16_t *>(lut)[w >> 24];
+#pragma unroll 1
+    for (int sh = 16; e >= thr; sh -= 8) {
+        const uint32_t table = eb == 1 ? 256u - e : e - 256u;
+        if (table >= k || sh < 0) { e = 0; break; }
+        const uint32_t idx = table * 256u + ((w >> sh) & 0xFFu);
+        e = eb == 1 ? lut[idx] : reinterpret_cast<const uint16_t *>(lut)[idx];
+    }
+    e &= 0xFFu;
+    len = clen[e];
+    if (len == 0) len = 32;
+    return e;
+}
+
 __device__ __forceinline__ void group_bar(int g) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kT) : "memory");
 }
 
-// 32-bit MSB-first window at bit `off` (0 <= off < 64) of the 96-bit chunk (w0:w1:w2).
+// 32-bit MSB-first window at bit `off` (0 <= off < 64) of the 96-bit chunk (w0:w1:w2).  Only bits
+// 0..5 of `off` are used, so callers may pass a packed counter.
 __device__ __forceinline__ uint32_t window(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t off) {
-    const bool lo = off < 32;
-    const uint32_t hi_w = lo ? w0 : w1, lo_w = lo ? w1 : w2;
-    return __funnelshift_l(lo_w, hi_w, off);
+    const bool lo = (off & 32u) == 0;
+    return __funnelshift_l(lo ? w1 : w2, lo ? w0 : w1, off);
 }
 
-// Two packed BF16 from x = (E1<<24 | S1<<16 | E0<<8 | S0): (sign<<15) | (E<<7) | mantissa per half.
-__device__ __forceinline__ uint32_t compose2(uint32_t x) {
-    return (x & 0x007F007Fu) | ((x >> 1) & 0x7F807F80u) | ((x << 8) & 0x80008000u);
+// Two BF16 from 2 exponents (bytes 0,1 of E) and 2 sign/mantissa bytes (bytes 0,1 of S) — or bytes
+// 2,3 with hi = true: W = [S0, sign(S0)x8, S1, sign(S1)x8] (PRMT sign replicate), X = [E0,0,E1,0];
+// result = (W & 0x807F807F) + (X << 7)  =  (sign << 15) | (E << 7) | mantissa per half.
+template <bool hi>
+__device__ __forceinline__ uint32_t compose2(uint32_t E, uint32_t S) {
+    const uint32_t W = prmt(S, 0u, hi ? 0xB3A2u : 0x9180u);
+    const uint32_t X = prmt(E, 0u, hi ? 0x4342u : 0x4140u);
+    return (W & 0x807F807Fu) + (X << 7);
 }
 
-struct TileIn {              // per-thread registers describing one tile
-    uint32_t w0, w1, w2;     // chunk bytes (big-endian words)
-    uint32_t gap;
-    uint32_t lo, hi;         // clipped BlockOutputPos[b], BlockOutputPos[b+1]
-};
+// Row `w >> (32-R)` of a lane-private replicated table: address = lane_base + row * 128.
+__device__ __forceinline__ uint32_t lds_row(uint32_t lane_base, uint32_t w) {
+    uint32_t v;
+    asm volatile("{\n\t.reg .u32 t;\n\tshr.u32 t, %1, %3;\n\tmad.lo.u32 t, t, 128, %2;\n\tld.shared.u32 %0, [t];\n\t}"
+                 : "=r"(v) : "r"(w), "r"(lane_base), "n"(32 - kR));
+    return v;
+}
 
-__device__ __forceinline__ void load_tile(const df11_device_tensor &ts, uint32_t b, uint32_t t, TileIn &ti) {
-    const uint8_t *enc = ts.encoded_exponent + (size_t)b * (kT * kN) + (size_t)t * kN;
-    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(enc));
-    const uint32_t spill = __ldg(reinterpret_cast<const uint32_t *>(enc + 8));
-    ti.w0 = v.x;                              // byte-swapped at use (keeps the loads in flight)
-    ti.w1 = v.y;
-    ti.w2 = spill;
-    const uint64_t bit = 5ull * ((uint64_t)b * kT + t);
-    const uint32_t hb = __ldg(ts.gaps + (bit >> 3)), lb = __ldg(ts.gaps + (bit >> 3) + 1);
-    ti.gap = ((hb << 8) | lb) >> (11 - (uint32_t)(bit & 7));   // masked at use
-    ti.lo = __ldg(ts.block_output_pos + b);
-    ti.hi = __ldg(ts.block_output_pos + b + 1);
+// st.shared.u8 [addr + k] = v, predicated on pos < lim (no branch).
+template <int k>
+__device__ __forceinline__ void sts8_if(uint32_t addr, uint32_t v, uint32_t pos, uint32_t lim) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p st.shared.u8 [%0+%4], %1;\n\t}"
+                 ::"r"(addr), "r"(v), "r"(pos), "r"(lim), "n"(k) : "memory");
+}
+
+// ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n\tLAB_WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+// Stage format block b of tensor ts (its EncodedExponent chunk + spill, and its gaps) into `stage`.
+__device__ __forceinline__ void issue_tile(const df11_device_tensor &ts, uint32_t b, uint32_t stage, uint32_t bar) {
+    mbar_expect_tx(bar, kChunkBytes + kGapBytes);
+    tma_g2s(stage, ts.encoded_exponent + (size_t)b * (kT * kN), kChunkBytes, bar);
+    tma_g2s(stage + kChunkBytes, ts.gaps + (size_t)b * (kT * 5 / 8), kGapBytes, bar);
 }
 
 __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ Batch bt) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const uint32_t tid = threadIdx.x;
     const int g = (int)(tid / kT);
     const uint32_t t = tid % kT;
     const uint32_t lane = tid & 31, wig = t >> 5;
     const uint32_t FULL = 0xFFFFFFFFu;
+    uint8_t *sb = smem_b();
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
+    // lane-private table addresses: row r of table X is at X + r*128 + lane*4
+    const uint32_t t1_lane = sbase + kOffT1 + lane * 4u;
+    const uint32_t t2_lane = sbase + kOffT2 + lane * 4u;
+    const uint32_t ebuf_off = kOffExp + (uint32_t)g * kExpBuf;             // byte offset into smem
+    uint32_t *wsum = smem_w + kOffWsum / 4 + (uint32_t)g * 16;            // [2][8]
+    const uint16_t *smask = reinterpret_cast<const uint16_t *>(sb + kOffSM);
 
     const uint32_t total = bt.total_tiles;
     const uint32_t c_begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
     const uint32_t c_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
     if (c_begin >= c_end) return;
 
+    const uint32_t stage0 = sbase + kOffStage + (uint32_t)g * 2 * kStageBytes;
+    const uint32_t mbar0 = sbase + kOffMbar + (uint32_t)g * 16;
+    if (t == 0) {
+        mbar_init(mbar0, 1);
+        mbar_init(mbar0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t q = 0;                    // tiles consumed by this group so far (stage = q & 1)
+
+    uint32_t parity = 0;
     int ti_idx = tensor_of_tile(bt, c_begin);
     for (uint32_t seg_begin = c_begin; seg_begin < c_end; ti_idx++) {
         const df11_device_tensor &ts = bt.t[ti_idx];
@@ -127,7 +205,12 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
 
         // ---- derived tables for this tensor (CTA-wide)
         __syncthreads();
-        for (uint32_t idx = tid; idx < (1u << kR); idx += kCta) {
+        const uint32_t lut_bytes = ts.k * 256u * ts.lut_entry_bytes;
+        const bool lut_in_smem = lut_bytes <= kLutSmem;
+        if (lut_in_smem)
+            for (uint32_t i = tid; i < lut_bytes; i += kCta) sb[kOffLut + i] = __ldg(ts.luts + i);
+        for (uint32_t i = tid; i < 256u; i += kCta) sb[kOffLen + i] = __ldg(ts.code_lengths + i);
+        for (uint32_t idx = tid; idx < kRows; idx += kCta) {
             const uint32_t W = idx << (32 - kR);
             uint32_t s = 0, cnt = 0, mask = 0, cons = 0, syms = 0, c2 = 0, cons2 = 0;
             while (s < (uint32_t)kR) {
@@ -140,156 +223,202 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 cons = s;
                 if (c2 < 3) { syms |= sym << (8 * c2); c2++; cons2 = s; }
             }
-            const uint32_t e1 = cnt ? (cnt | (mask << 8) | (cons << 28)) : 0u;
+            const uint32_t e1 = cnt ? (cons | (cnt << 16)) : 0u;
             const uint32_t e2 = c2 ? (syms | (c2 << 24) | (cons2 << 28)) : 0u;
-            uint4 *d1 = reinterpret_cast<uint4 *>(S.t1 + idx * 32);
-            uint4 *d2 = reinterpret_cast<uint4 *>(S.t2 + idx * 32);
+            uint4 *d1 = reinterpret_cast<uint4 *>(smem_w + kOffT1 / 4 + idx * 32);
+            uint4 *d2 = reinterpret_cast<uint4 *>(smem_w + kOffT2 / 4 + idx * 32);
 #pragma unroll
             for (int q = 0; q < 8; q++) {
                 d1[q] = make_uint4(e1, e1, e1, e1);
                 d2[q] = make_uint4(e2, e2, e2, e2);
             }
+            reinterpret_cast<uint16_t *>(sb + kOffSM)[idx] = (uint16_t)mask;
         }
         __syncthreads();
 
+        const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
+        // escape path: the paper's LUT walk for a code longer than R bits
+        const bool narrow_smem = lut_in_smem && eb_bytes == 1;
+        auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
+            if (narrow_smem) {                                  // root, then child tables via 256 - v
+                const uint32_t lb = sbase + kOffLut;
+                uint32_t e, sh = 24, table = 0;
+#pragma unroll 1
+                for (int i = 0; i < 4; i++, sh -= 8) {
+                    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(e) : "r"(lb + table * 256u + ((w >> sh) & 0xFFu)));
+                    if (e < 240u) break;
+                    table = 256u - e;
+                    if (table >= kk || i == 3) { e = 0; break; }
+                }
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(len) : "r"(sbase + kOffLen + e));
+                if (len == 0) len = 32;
+                return e;
+            }
+            if (lut_in_smem) return lut_walk_smem(w, sb + kOffLut, sb + kOffLen, eb_bytes, kk, len);
+            return lut_walk(w, ts, len);
+        };
         const uint32_t N = (uint32_t)ts.num_elements;
         const bool vec_out = ((reinterpret_cast<uintptr_t>(ts.out) & 15) == 0);
-        const uint32_t *t1 = S.t1 + lane;
-        const uint32_t *t2 = S.t2 + lane;
-        uint8_t *ebuf = S.expbuf[g];
+        const uint4 *__restrict__ psm4 = reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa);
+        uint16_t *__restrict__ out = ts.out;
 
         uint32_t tile = seg_begin + g;
-        TileIn cur;
-        if (tile < seg_end) load_tile(ts, tile - base_tile, t, cur);
-        for (; tile < seg_end; tile += kGroups) {
+        if (t == 0) {                                                          // producer: first two tiles
+            if (tile < seg_end) issue_tile(ts, tile - base_tile, stage0 + (q & 1) * kStageBytes, mbar0 + (q & 1) * 8);
+            if (tile + kGroups < seg_end)
+                issue_tile(ts, tile + kGroups - base_tile, stage0 + ((q + 1) & 1) * kStageBytes, mbar0 + ((q + 1) & 1) * 8);
+        }
+        uint32_t nlo = 0, nhi = 0;
+        if (tile < seg_end) {
+            nlo = __ldg(ts.block_output_pos + tile - base_tile);
+            nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
+        }
+        for (; tile < seg_end; tile += kGroups, q++) {
             const uint32_t b = tile - base_tile;
-            // prefetch the next tile of this group
-            TileIn nxt;
+            const uint32_t clo = nlo, chi = nhi;
             const bool has_next = tile + kGroups < seg_end;
-            if (has_next) load_tile(ts, b + kGroups, t, nxt);
+            if (has_next) {                                                    // prefetch next BlockOutputPos
+                nlo = __ldg(ts.block_output_pos + b + kGroups);
+                nhi = __ldg(ts.block_output_pos + b + kGroups + 1);
+            }
+            const uint32_t st = stage0 + (q & 1) * kStageBytes;
+            mbar_wait(mbar0 + (q & 1) * 8, (q >> 1) & 1u);
+            uint32_t w0, w1, w2, gap;
+            {
+                uint32_t a, c, d, h0, h1;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(c) : "r"(st + t * kN));
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(st + t * kN + 8));
+                const uint32_t gb0 = st + kChunkBytes + ((t * 5) >> 3);
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h0) : "r"(gb0));
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h1) : "r"(gb0 + 1));
+                w0 = bswap32(a);
+                w1 = bswap32(c);
+                w2 = bswap32(d);
+                gap = (((h0 << 8) | h1) >> (11u - ((t * 5) & 7u))) & 31u;
+            }
+            const uint32_t lo = min(clo, N);
+            const uint32_t hi = min(max(min(chi, N), lo), lo + (uint32_t)(8 * kN * kT));
+            const uint32_t f = lo & ~15u;                                      // 16-element frame
 
-            const uint32_t w0 = bswap32(cur.w0), w1 = bswap32(cur.w1), w2 = bswap32(cur.w2);
-            const uint32_t gap = cur.gap & 31u;
-            const uint32_t lo = min(cur.lo, N);
-            const uint32_t hi = min(max(min(cur.hi, N), lo), lo + (uint32_t)(8 * kN * kT));
-            const uint32_t f = lo & ~15u;                      // 16-element aligned frame origin
-            const uint32_t g_first = f >> 4, g_last = (hi + 15) >> 4;
-
-            // sign/mantissa prefetch for this thread's first two merge groups
-            uint4 smA = make_uint4(0, 0, 0, 0), smB = make_uint4(0, 0, 0, 0);
-            const uint32_t gA = g_first + t, gB = g_first + t + kT;
-            if (gA < g_last) smA = __ldg(reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa) + gA);
-            if (gB < g_last) smB = __ldg(reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa) + gB);
-
-            // ---- phase 1: count codewords starting in [0, 64) (T1, several codes per lookup)
-            uint32_t off = gap, cnt = 0, e1 = 1;
+            // ---- phase 1: acc = bit offset | count << 16; every T1 lookup counts all complete codes
+            uint32_t acc = gap, e1 = 1;
             for (;;) {
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    if (off < 64) {
-                        const uint32_t w = window(w0, w1, w2, off);
-                        e1 = t1[(w >> (32 - kR)) << 5];
-                        cnt += e1 & 15u;
-                        off += e1 >> 28;
+                    const uint32_t e = lds_row(t1_lane, window(w0, w1, w2, acc));
+                    if ((acc & 0xFFC0u) == 0) {                                // offset < 64: still ours
+                        acc += e;
+                        e1 = e;
                     }
                 }
-                if (!__any_sync(FULL, off < 64)) break;
-                const bool esc = off < 64 && e1 == 0;
-                if (__any_sync(FULL, esc)) {
-                    if (esc) {                                 // code longer than R bits
+                const bool live = (acc & 0xFFC0u) == 0, esc = live && e1 == 0;
+                const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
+                if (!(flags & 1u)) break;
+                if (flags & 2u) {
+                    if (esc) {                                                 // code longer than R bits
                         uint32_t len;
-                        lut_walk(window(w0, w1, w2, off), ts, len);
-                        cnt++;
-                        off += len;
+                        walk(window(w0, w1, w2, acc), len);
+                        acc += len + (1u << 16);
                     }
                 }
             }
-            {   // the last group may hold complete codes that start at or after bit 64: not ours
-                const uint32_t last = off - (e1 >> 28);
-                const uint32_t keep = __funnelshift_lc(0u, 1u, 64u - min(last, 64u)) - 1u;  // starts s < 64-last
-                cnt -= __popc((e1 >> 8) & 0x1FFu & ~keep);
+            uint32_t cnt = acc >> 16;
+            if (e1 != 0) {     // last T1 group may contain complete codes starting at bit >= 64: not ours
+                const uint32_t last = (acc & 0xFFFFu) - (e1 & 0xFFFFu);        // < 64
+                const uint32_t m = smask[window(w0, w1, w2, last) >> (32 - kR)];
+                cnt -= __popc(m >> min(64u - last, 31u));
             }
 
-            // ---- block exclusive scan over the 256 counts (warp shuffles + 8 warp totals)
+            // ---- block exclusive scan of the counts: warp shuffles + 8 warp totals (1 barrier)
             uint32_t incl = cnt;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const uint32_t v = __shfl_up_sync(FULL, incl, d);
                 if (lane >= (uint32_t)d) incl += v;
             }
-            if (lane == 31) S.wsum[g][wig] = incl;
-            group_bar(g);
+            uint32_t *ws = wsum + parity * 8;
+            if (lane == 31) ws[wig] = incl;
+            group_bar(g);                          // every thread has read this tile's stage
+            parity ^= 1u;
+            if (t == 0 && tile + 2 * kGroups < seg_end)
+                issue_tile(ts, b + 2 * kGroups, st, mbar0 + (q & 1) * 8);
             uint32_t wpre = 0;
+            {
+                const uint4 a = *reinterpret_cast<const uint4 *>(ws);
+                const uint4 c = *reinterpret_cast<const uint4 *>(ws + 4);
+                const uint32_t v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
 #pragma unroll
-            for (uint32_t q = 0; q < 8; q++) {
-                const uint32_t s = S.wsum[g][q];
-                wpre += q < wig ? s : 0u;
+                for (uint32_t q = 0; q < 7; q++) wpre += q < wig ? v[q] : 0u;
             }
-            uint8_t *wp = ebuf + (lo - f) + wpre + incl - cnt;
+            const uint32_t wtot = __shfl_sync(FULL, incl, 31);
+            // this warp's output range [ra, rb) (absolute elements), clipped to the tile
+            const uint32_t ra = min(lo + wpre, hi), rb = min(lo + wpre + wtot, hi);
+            // full 16-element groups [ga, gb) take the vector path; the <= 15 + 15 edge elements
+            // [ra, ha) and [tb, rb) are shared with the neighbouring warps and go one per lane
+            const uint32_t ga = vec_out ? (ra + 15) >> 4 : 0, gb = vec_out ? max(rb >> 4, ga) : 0;
+            const uint32_t ha = vec_out ? min(ga << 4, rb) : rb, tb = vec_out ? max(gb << 4, ha) : rb;
+            uint4 smA = make_uint4(0, 0, 0, 0), smB = make_uint4(0, 0, 0, 0);
+            if (ga + lane < gb) smA = __ldg(psm4 + ga + lane);                 // prefetch for the merge
+            if (ga + lane + 32 < gb) smB = __ldg(psm4 + ga + lane + 32);
+            const uint32_t es = lane < 16 ? ra + lane : tb + (lane - 16);      // this lane's edge element
+            const bool edge = vec_out && (lane < 16 ? es < ha : es < rb);
+            uint32_t sm1 = 0;
+            if (edge) sm1 = __ldg(ts.packed_sign_mantissa + es);
 
-            // ---- phase 2: re-decode (T2, up to 3 exponents per lookup) into the SMEM buffer
-            off = gap;
-            uint32_t j = 0, e2 = 1;
+            // ---- phase 2: re-decode with T2 (<= 3 exponents per lookup) into the SMEM buffer
+            const uint32_t wp0 = sbase + ebuf_off + (lo - f) + wpre + incl - cnt;
+            const uint32_t wend = wp0 + cnt;
+            const uint32_t wend1 = wend - 1, wend2 = wend - 2;
+            uint32_t wp = wp0, off = gap, e2 = 1;
             for (;;) {
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    if (j < cnt) {
-                        const uint32_t w = window(w0, w1, w2, off);
-                        e2 = t2[(w >> (32 - kR)) << 5];
-                        wp[j] = (uint8_t)e2;
-                        if (j + 1 < cnt) wp[j + 1] = (uint8_t)(e2 >> 8);
-                        if (j + 2 < cnt) wp[j + 2] = (uint8_t)(e2 >> 16);
-                        j += (e2 >> 24) & 3u;
-                        off += e2 >> 28;
-                    }
+                    // finished lanes keep advancing harmlessly: every store is predicated on wp
+                    e2 = lds_row(t2_lane, window(w0, w1, w2, off));
+                    sts8_if<0>(wp, e2, wp, wend);
+                    sts8_if<1>(wp, e2 >> 8, wp, wend1);
+                    sts8_if<2>(wp, e2 >> 16, wp, wend2);
+                    wp += (e2 >> 24) & 3u;
+                    off += e2 >> 28;
                 }
-                if (!__any_sync(FULL, j < cnt)) break;
-                const bool esc = j < cnt && e2 == 0;
-                if (__any_sync(FULL, esc)) {
+                const bool live = wp < wend, esc = live && e2 == 0;
+                const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
+                if (!(flags & 1u)) break;
+                if (flags & 2u) {
                     if (esc) {
                         uint32_t len;
-                        wp[j] = (uint8_t)lut_walk(window(w0, w1, w2, off), ts, len);
-                        j++;
+                        const uint32_t sym = walk(window(w0, w1, w2, off), len);
+                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(wp), "r"(sym) : "memory");
+                        wp++;
                         off += len;
                     }
                 }
             }
-            group_bar(g);
+            __syncwarp();
 
-            // ---- merge: compose BF16 and store, 16 elements per thread per step
-            uint16_t *__restrict__ out = ts.out;
-            for (uint32_t gi = gA, it = 0; gi < g_last; gi += kT, it++) {
+            // ---- per-warp merge of [ra, rb): compose BF16 and store
+            const uint8_t *ebf = sb + ebuf_off;                                // ebf[e - f] = exponent of element e
+            if (edge) out[es] = compose(ebf[es - f], sm1);
+            for (uint32_t gi = ga + lane, it = 0; gi < gb; gi += 32, it++) {
                 const uint32_t e0 = gi << 4;
-                const uint4 ex = *reinterpret_cast<const uint4 *>(ebuf + (e0 - f));
-                uint4 sm;
-                if (it == 0) sm = smA;
-                else if (it == 1) sm = smB;
-                else sm = __ldg(reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa) + gi);
-                if (vec_out && e0 >= lo && e0 + 16 <= hi) {
-                    uint4 o0, o1;
-                    o0.x = compose2(__byte_perm(sm.x, ex.x, 0x5140));
-                    o0.y = compose2(__byte_perm(sm.x, ex.x, 0x7362));
-                    o0.z = compose2(__byte_perm(sm.y, ex.y, 0x5140));
-                    o0.w = compose2(__byte_perm(sm.y, ex.y, 0x7362));
-                    o1.x = compose2(__byte_perm(sm.z, ex.z, 0x5140));
-                    o1.y = compose2(__byte_perm(sm.z, ex.z, 0x7362));
-                    o1.z = compose2(__byte_perm(sm.w, ex.w, 0x5140));
-                    o1.w = compose2(__byte_perm(sm.w, ex.w, 0x7362));
-                    uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
-                    dst[0] = o0;
-                    dst[1] = o1;
-                } else {
-                    const uint32_t exw[4] = {ex.x, ex.y, ex.z, ex.w};
-                    const uint32_t smw[4] = {sm.x, sm.y, sm.z, sm.w};
-#pragma unroll
-                    for (uint32_t q = 0; q < 16; q++) {
-                        const uint32_t e = e0 + q;
-                        if (e >= lo && e < hi)
-                            out[e] = compose((exw[q >> 2] >> (8 * (q & 3))) & 0xFFu, (smw[q >> 2] >> (8 * (q & 3))) & 0xFFu);
-                    }
-                }
+                const uint4 sm = it == 0 ? smA : (it == 1 ? smB : __ldg(psm4 + gi));
+                const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - f));
+                uint4 o0, o1;
+                o0.x = compose2<false>(ex.x, sm.x);
+                o0.y = compose2<true>(ex.x, sm.x);
+                o0.z = compose2<false>(ex.y, sm.y);
+                o0.w = compose2<true>(ex.y, sm.y);
+                o1.x = compose2<false>(ex.z, sm.z);
+                o1.y = compose2<true>(ex.z, sm.z);
+                o1.z = compose2<false>(ex.w, sm.w);
+                o1.w = compose2<true>(ex.w, sm.w);
+                uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
+                dst[0] = o0;
+                dst[1] = o1;
             }
-            if (has_next) cur = nxt;
+            if (!vec_out)                                                      // unaligned output: scalar
+                for (uint32_t e = ra + lane; e < rb; e += 32)
+                    out[e] = compose(ebf[e - f], __ldg(ts.packed_sign_mantissa + e));
         }
         seg_begin = seg_end;
     }
@@ -301,7 +430,8 @@ int g_attr_set[64];
 
 bool fast_supports(const df11_device_tensor &t) {
     return t.T == (uint32_t)kT && t.n == (uint32_t)kN &&
-           (reinterpret_cast<uintptr_t>(t.encoded_exponent) & 7) == 0 &&
+           (reinterpret_cast<uintptr_t>(t.encoded_exponent) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(t.gaps) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.packed_sign_mantissa) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.out) & 1) == 0;
 }
