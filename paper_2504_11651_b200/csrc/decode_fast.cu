@@ -10,13 +10,16 @@
 //    barrier (one per tile), so groups drift apart and hide each other's latency.
 //  * Derived decode tables are built in SMEM once per (CTA, tensor) from the format's hierarchical
 //    LUTs.  For every R-bit prefix (R = 9):
-//      T1 = consumed | count << 16      (phase 1; every complete code in the R bits)
-//      T2 = s0 | s1 << 8 | s2 << 16 | count << 24 | consumed << 28   (phase 2; up to 3 exponents)
-//      SM = start mask of the T1 codes  (one lookup per thread per tile, for the chunk-end fixup)
+//      T1 = consumed | count << 8 | startmask << 23        (phase 1; every complete code in R bits)
+//      T2 = s0 | s1 << 8 | s2 << 16 | consumed << 24 | count << 29   (phase 2; up to 3 exponents)
 //    T1/T2 are replicated 32x with lane-private banks (word = prefix*32 + lane): conflict-free LDS.
-//    Codes longer than R bits (~0.1 % on LLM-like weights) leave the entry 0; the thread stalls on it
-//    and a warp-uniform check every 4 steps resolves it with the paper's LUT walk.
-//  * Phase 1 keeps (bit offset | count << 16) in ONE register and adds the T1 entry to it.
+//    A prefix whose first code is longer than R bits (~0.1 % of codes on LLM-like weights) is an
+//    "escape" row: its entry advances nothing, the thread stalls on it and a warp-uniform check every
+//    4 steps resolves it through a second-level table (next 9 bits -> symbol, length) built for up to
+//    8 escape rows, or, for longer codes, through the paper's LUT walk.
+//  * Phase 1 keeps (bit offset | count << 8) in ONE register and adds the T1 entry to it.
+//  * The decode window is the top word of a 96-bit bit buffer shifted by the consumed bits; field
+//    extraction uses IMAD.HI so the ALU and FMA pipes are equally loaded.
 //  * The thread's 8-byte chunk + 4 spill bytes live in 3 registers; the decode window is a funnel
 //    shift, so EncodedExponent is read from HBM exactly once.
 //  * One barrier per tile: the scan.  Each warp then merges its own contiguous output range (its 32
@@ -39,9 +42,11 @@ constexpr uint32_t kExpBuf = 8 * kN * kT + 64;
 // SMEM layout (bytes)
 constexpr uint32_t kOffT1 = 0;
 constexpr uint32_t kOffT2 = kOffT1 + kTabWords * 4;
-constexpr uint32_t kOffSM = kOffT2 + kTabWords * 4;           // uint16[kRows]
+constexpr uint32_t kEscRows = 8;                              // escape rows with a second-level table
+constexpr uint32_t kR2 = 9;                                   // bits resolved by the second level
+constexpr uint32_t kOffL2 = kOffT2 + kTabWords * 4;           // uint16 [kEscRows][1 << kR2]: sym | len << 8
 constexpr uint32_t kLutSmem = 8192;                           // format LUTs copied when they fit
-constexpr uint32_t kOffLut = kOffSM + kRows * 2;              // uint8/uint16 [k][256]
+constexpr uint32_t kOffLut = kOffL2 + kEscRows * (1u << kR2) * 2;   // uint8/uint16 [k][256]
 constexpr uint32_t kOffLen = kOffLut + kLutSmem;              // CodeLengths[256]
 constexpr uint32_t kOffWsum = kOffLen + 256;                  // [groups][2 parities][8] uint32
 constexpr uint32_t kOffExp = kOffWsum + kGroups * 2 * 8 * 4;  // [groups][kExpBuf]
@@ -127,6 +132,36 @@ __device__ __forceinline__ uint32_t compose2(uint32_t E, uint32_t S) {
     return (W & 0x807F807Fu) + (X << 7);
 }
 
+// FMA-pipe integer helpers.  The B200 ALU pipe (SHF/LOP3/PRMT/SEL/ISETP) issues a warp instruction
+// every 2 cycles per SMSP, as does the FMA pipe (IMAD*): bit-field extraction is moved onto the FMA
+// pipe with multiplies by powers of two that the compiler cannot strength-reduce (runtime operands).
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {     // (a * b) >> 32
+    uint32_t d;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {   // ((a*b) >> 32) + c
+    uint32_t d;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {   // a*b + c
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+// 96-bit MSB-first bit buffer (a:b:c) shifted left by `s` (0..31; only the low 5 bits are used).
+__device__ __forceinline__ void shift96(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
+    a = __funnelshift_l(b, a, s);
+    b = __funnelshift_l(c, b, s);
+    c = __funnelshift_l(0u, c, s);
+}
+
 // Row `w >> (32-R)` of a lane-private replicated table: address = lane_base + row * 128.
 __device__ __forceinline__ uint32_t lds_row(uint32_t lane_base, uint32_t w) {
     uint32_t v;
@@ -171,6 +206,9 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
     const uint32_t t = tid % kT;
     const uint32_t lane = tid & 31, wig = t >> 5;
     const uint32_t FULL = 0xFFFFFFFFu;
+    const uint32_t one = blockDim.x >> 10;                       // == 1, opaque to the compiler
+    const uint32_t K_ROW = one << kR, K_128 = one << 7, K_S24 = one << 8, K_S8 = one << 24,
+                   K_S16 = one << 16, K_S29 = one << 3;
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
     // lane-private table addresses: row r of table X is at X + r*128 + lane*4
@@ -178,7 +216,6 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
     const uint32_t t2_lane = sbase + kOffT2 + lane * 4u;
     const uint32_t ebuf_off = kOffExp + (uint32_t)g * kExpBuf;             // byte offset into smem
     uint32_t *wsum = smem_w + kOffWsum / 4 + (uint32_t)g * 16;            // [2][8]
-    const uint16_t *smask = reinterpret_cast<const uint16_t *>(sb + kOffSM);
 
     const uint32_t total = bt.total_tiles;
     const uint32_t c_begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
@@ -210,35 +247,13 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
         if (lut_in_smem)
             for (uint32_t i = tid; i < lut_bytes; i += kCta) sb[kOffLut + i] = __ldg(ts.luts + i);
         for (uint32_t i = tid; i < 256u; i += kCta) sb[kOffLen + i] = __ldg(ts.code_lengths + i);
-        for (uint32_t idx = tid; idx < kRows; idx += kCta) {
-            const uint32_t W = idx << (32 - kR);
-            uint32_t s = 0, cnt = 0, mask = 0, cons = 0, syms = 0, c2 = 0, cons2 = 0;
-            while (s < (uint32_t)kR) {
-                uint32_t len;
-                const uint32_t sym = lut_walk(W << s, ts, len);
-                if (len > (uint32_t)kR - s) break;
-                mask |= 1u << s;
-                cnt++;
-                s += len;
-                cons = s;
-                if (c2 < 3) { syms |= sym << (8 * c2); c2++; cons2 = s; }
-            }
-            const uint32_t e1 = cnt ? (cons | (cnt << 16)) : 0u;
-            const uint32_t e2 = c2 ? (syms | (c2 << 24) | (cons2 << 28)) : 0u;
-            uint4 *d1 = reinterpret_cast<uint4 *>(smem_w + kOffT1 / 4 + idx * 32);
-            uint4 *d2 = reinterpret_cast<uint4 *>(smem_w + kOffT2 / 4 + idx * 32);
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                d1[q] = make_uint4(e1, e1, e1, e1);
-                d2[q] = make_uint4(e2, e2, e2, e2);
-            }
-            reinterpret_cast<uint16_t *>(sb + kOffSM)[idx] = (uint16_t)mask;
-        }
+        uint32_t *esc_mask = smem_w + kOffExp / 4;                 // scratch: the exponent buffers are idle
+        uint32_t *esc_row = esc_mask + kRows / 32;
+        if (tid < kRows / 32) esc_mask[tid] = 0;
         __syncthreads();
-
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
-        // escape path: the paper's LUT walk for a code longer than R bits
         const bool narrow_smem = lut_in_smem && eb_bytes == 1;
+        // the paper's LUT walk for one code at the top of window w
         auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
             if (narrow_smem) {                                  // root, then child tables via 256 - v
                 const uint32_t lb = sbase + kOffLut;
@@ -256,6 +271,69 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             }
             if (lut_in_smem) return lut_walk_smem(w, sb + kOffLut, sb + kOffLen, eb_bytes, kk, len);
             return lut_walk(w, ts, len);
+        };
+        uint32_t row_e1 = 0, row_e2 = 0;
+        bool row_esc = false;
+        if (tid < kRows) {
+            const uint32_t idx = tid, W = idx << (32 - kR);
+            uint32_t s = 0, cnt = 0, mask = 0, cons = 0, syms = 0, c2 = 0, cons2 = 0;
+            while (s < (uint32_t)kR) {
+                uint32_t len;
+                const uint32_t sym = walk(W << s, len);
+                if (len > (uint32_t)kR - s) break;
+                mask |= 1u << s;
+                cnt++;
+                s += len;
+                cons = s;
+                if (c2 < 3) { syms |= sym << (8 * c2); c2++; cons2 = s; }
+            }
+            row_esc = cnt == 0;
+            row_e1 = cons | (cnt << 8) | (mask << 23);
+            row_e2 = syms | (cons2 << 24) | (c2 << 29);
+            if (row_esc) atomicOr(esc_mask + idx / 32, 1u << (idx % 32));
+        }
+        __syncthreads();
+        if (row_esc) {                                             // id = 1 + rank among escape rows
+            uint32_t id = 1 + __popc(esc_mask[tid / 32] & ((1u << (tid % 32)) - 1u));
+            for (uint32_t q2 = 0; q2 < tid / 32; q2++) id += __popc(esc_mask[q2]);
+            if (id > kEscRows) id = 0;                             // no second-level table: walk
+            else esc_row[id - 1] = tid;
+            row_e1 = id << 23;                                     // advances nothing: the thread stalls
+            row_e2 = id;
+        }
+        if (tid < kRows) {
+            uint4 *d1 = reinterpret_cast<uint4 *>(smem_w + kOffT1 / 4 + tid * 32);
+            uint4 *d2 = reinterpret_cast<uint4 *>(smem_w + kOffT2 / 4 + tid * 32);
+#pragma unroll
+            for (int q2 = 0; q2 < 8; q2++) {
+                d1[q2] = make_uint4(row_e1, row_e1, row_e1, row_e1);
+                d2[q2] = make_uint4(row_e2, row_e2, row_e2, row_e2);
+            }
+        }
+        __syncthreads();
+        {   // second-level tables: row id-1, next kR2 bits -> sym | len << 8 (0 if longer than kR + kR2)
+            uint32_t n_esc = 0;
+            for (uint32_t q2 = 0; q2 < kRows / 32; q2++) n_esc += __popc(esc_mask[q2]);
+            n_esc = min(n_esc, kEscRows);
+            uint16_t *l2 = reinterpret_cast<uint16_t *>(sb + kOffL2);
+            for (uint32_t i = tid; i < n_esc << kR2; i += kCta) {
+                const uint32_t row = esc_row[i >> kR2], j = i & ((1u << kR2) - 1u);
+                uint32_t len;
+                const uint32_t sym = walk((row << (32 - kR)) | (j << (32 - kR - kR2)), len);
+                l2[i] = len <= (uint32_t)(kR + kR2) ? (uint16_t)(sym | (len << 8)) : (uint16_t)0;
+            }
+        }
+        __syncthreads();
+
+        // resolve one code longer than R bits at the top of `a` (escape row id from the table entry)
+        auto escape = [&](uint32_t a_, uint32_t id, uint32_t &len) -> uint32_t {
+            if (id != 0) {
+                uint32_t v;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v)
+                             : "r"(sbase + kOffL2 + (((id - 1) << kR2) + ((a_ >> (32 - kR - kR2)) & ((1u << kR2) - 1u))) * 2));
+                if (v >> 8) { len = v >> 8; return v & 0xFFu; }
+            }
+            return walk(a_, len);
         };
         const uint32_t N = (uint32_t)ts.num_elements;
         const bool vec_out = ((reinterpret_cast<uintptr_t>(ts.out) & 15) == 0);
@@ -283,50 +361,52 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             }
             const uint32_t st = stage0 + (q & 1) * kStageBytes;
             mbar_wait(mbar0 + (q & 1) * 8, (q >> 1) & 1u);
-            uint32_t w0, w1, w2, gap;
+            uint32_t gap, raw0, raw1, raw2;
             {
-                uint32_t a, c, d, h0, h1;
-                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(c) : "r"(st + t * kN));
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(st + t * kN + 8));
+                uint32_t h0, h1;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(raw0), "=r"(raw1) : "r"(st + t * kN));
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw2) : "r"(st + t * kN + 8));
                 const uint32_t gb0 = st + kChunkBytes + ((t * 5) >> 3);
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h0) : "r"(gb0));
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h1) : "r"(gb0 + 1));
-                w0 = bswap32(a);
-                w1 = bswap32(c);
-                w2 = bswap32(d);
                 gap = (((h0 << 8) | h1) >> (11u - ((t * 5) & 7u))) & 31u;
             }
             const uint32_t lo = min(clo, N);
             const uint32_t hi = min(max(min(chi, N), lo), lo + (uint32_t)(8 * kN * kT));
             const uint32_t f = lo & ~15u;                                      // 16-element frame
 
-            // ---- phase 1: acc = bit offset | count << 16; every T1 lookup counts all complete codes
+            // ---- phase 1: bit buffer (a:b:c) starts at the gap; acc = offset | count << 8 (+ junk >= bit 23)
+            uint32_t a = bswap32(raw0), bb = bswap32(raw1), c = bswap32(raw2);
+            shift96(a, bb, c, gap);
             uint32_t acc = gap, e1 = 1;
             for (;;) {
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    const uint32_t e = lds_row(t1_lane, window(w0, w1, w2, acc));
-                    if ((acc & 0xFFC0u) == 0) {                                // offset < 64: still ours
+                    const uint32_t e = lds32(madlo(mulhi(a, K_ROW), K_128, t1_lane));
+                    if ((acc & 0xC0u) == 0) {                                  // offset < 64: still ours
                         acc += e;
                         e1 = e;
                     }
+                    shift96(a, bb, c, e);                                      // e & 31 = consumed bits
                 }
-                const bool live = (acc & 0xFFC0u) == 0, esc = live && e1 == 0;
+                const bool live = (acc & 0xC0u) == 0, esc = live && (e1 & 0x7FFFFFu) == 0;
                 const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
                 if (!(flags & 1u)) break;
                 if (flags & 2u) {
                     if (esc) {                                                 // code longer than R bits
                         uint32_t len;
-                        walk(window(w0, w1, w2, acc), len);
-                        acc += len + (1u << 16);
+                        escape(a, e1 >> 23, len);
+                        e1 = 0;                                                // exactly one code: no fixup
+                        acc += len + (1u << 8);
+                        shift96(a, bb, c, len & 31u);
+                        if (len == 32) { a = bb; bb = c; c = 0; }
                     }
                 }
             }
-            uint32_t cnt = acc >> 16;
-            if (e1 != 0) {     // last T1 group may contain complete codes starting at bit >= 64: not ours
-                const uint32_t last = (acc & 0xFFFFu) - (e1 & 0xFFFFu);        // < 64
-                const uint32_t m = smask[window(w0, w1, w2, last) >> (32 - kR)];
-                cnt -= __popc(m >> min(64u - last, 31u));
+            uint32_t cnt = (acc >> 8) & 0x7Fu;
+            if ((e1 & 0x7FFFFFu) != 0) {   // last T1 group may hold complete codes starting at bit >= 64
+                const uint32_t last = (acc & 0xFFu) - (e1 & 0xFu);             // < 64
+                cnt -= __popc((e1 >> 23) >> min(64u - last, 31u));
             }
 
             // ---- block exclusive scan of the counts: warp shuffles + 8 warp totals (1 barrier)
@@ -369,28 +449,31 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             const uint32_t wp0 = sbase + ebuf_off + (lo - f) + wpre + incl - cnt;
             const uint32_t wend = wp0 + cnt;
             const uint32_t wend1 = wend - 1, wend2 = wend - 2;
-            uint32_t wp = wp0, off = gap, e2 = 1;
+            uint32_t wp = wp0, e2 = 1;
+            a = bswap32(raw0); bb = bswap32(raw1); c = bswap32(raw2);
+            shift96(a, bb, c, gap);
             for (;;) {
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     // finished lanes keep advancing harmlessly: every store is predicated on wp
-                    e2 = lds_row(t2_lane, window(w0, w1, w2, off));
+                    e2 = lds32(madlo(mulhi(a, K_ROW), K_128, t2_lane));
                     sts8_if<0>(wp, e2, wp, wend);
-                    sts8_if<1>(wp, e2 >> 8, wp, wend1);
-                    sts8_if<2>(wp, e2 >> 16, wp, wend2);
-                    wp += (e2 >> 24) & 3u;
-                    off += e2 >> 28;
+                    sts8_if<1>(wp, mulhi(e2, K_S8), wp, wend1);
+                    sts8_if<2>(wp, mulhi(e2, K_S16), wp, wend2);
+                    wp = madhi(e2, K_S29, wp);                                 // wp += count
+                    shift96(a, bb, c, mulhi(e2, K_S24));                       // (e2 >> 24) & 31 = consumed
                 }
-                const bool live = wp < wend, esc = live && e2 == 0;
+                const bool live = wp < wend, esc = live && e2 < (1u << 24);
                 const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
                 if (!(flags & 1u)) break;
                 if (flags & 2u) {
                     if (esc) {
                         uint32_t len;
-                        const uint32_t sym = walk(window(w0, w1, w2, off), len);
+                        const uint32_t sym = escape(a, e2 & 0xFFu, len);
                         asm volatile("st.shared.u8 [%0], %1;" ::"r"(wp), "r"(sym) : "memory");
                         wp++;
-                        off += len;
+                        shift96(a, bb, c, len & 31u);
+                        if (len == 32) { a = bb; bb = c; c = 0; }
                     }
                 }
             }
