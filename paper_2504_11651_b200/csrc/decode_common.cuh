@@ -15,6 +15,9 @@ struct Batch {
     uint32_t tile_start[DF11_MAX_BATCH + 1];   // exclusive prefix of format blocks B over the batch
     uint32_t count;
     uint32_t total_tiles;
+    // powers of two used as IMAD multipliers (field extraction on the FMA pipe); read from the
+    // constant bank so the compiler cannot strength-reduce them into ALU shifts (set by the launcher)
+    uint32_t kpow[8];
 };
 
 // Tensor owning global tile `g` (binary search over tile_start).

@@ -1,13 +1,14 @@
 // decode_fast.cu — persistent sm_100a DF11 decode kernel (format T = 256, n = 8; narrow or wide LUTs).
 //
-// Same result as Algorithm 1 — every thread decodes the codewords that start in its
-// 8-byte chunk, a block-level exclusive scan turns per-thread counts into output positions
-// (P:148-150), phase 2 re-decodes into an SRAM buffer and BF16 leaves with coalesced stores —
-// re-designed for B200:
+// Same result as Algorithm 1: the codewords that start in each 8-byte chunk are
+// counted (phase 1), a block-level exclusive scan turns counts into output positions, the
+// chunks are re-decoded into an SRAM exponent buffer (phase 2) and BF16 leaves with coalesced stores
+// (P:150).  Re-designed for B200:
 //
-//  * Persistent CTAs, one per SM, 4 groups of 256 threads; group g of CTA c walks the format blocks
-//    ("tiles") of a contiguous range.  Each group owns a 16 KB exponent buffer and its own named
-//    barrier (one per tile), so groups drift apart and hide each other's latency.
+//  * Persistent CTAs (one per SM, 1024 threads) = 8 groups of 128 threads; group g of CTA c walks the
+//    format blocks ("tiles") of a contiguous range.  A thread decodes TWO adjacent chunks of its tile
+//    as one 128-bit stream starting at the first chunk's gap (the second gap is implied), which
+//    halves per-thread bookkeeping and evens out the per-lane work (warp lockstep).
 //  * Derived decode tables are built in SMEM once per (CTA, tensor) from the format's hierarchical
 //    LUTs.  For every R-bit prefix (R = 9):
 //      T1 = consumed | count << 8 | startmask << 23        (phase 1; every complete code in R bits)
@@ -17,53 +18,58 @@
 //    "escape" row: its entry advances nothing, the thread stalls on it and a warp-uniform check every
 //    4 steps resolves it through a second-level table (next 9 bits -> symbol, length) built for up to
 //    8 escape rows, or, for longer codes, through the paper's LUT walk.
-//  * Phase 1 keeps (bit offset | count << 8) in ONE register and adds the T1 entry to it.
-//  * The decode window is the top word of a 96-bit bit buffer shifted by the consumed bits; field
-//    extraction uses IMAD.HI so the ALU and FMA pipes are equally loaded.
-//  * The thread's 8-byte chunk + 4 spill bytes live in 3 registers; the decode window is a funnel
-//    shift, so EncodedExponent is read from HBM exactly once.
-//  * One barrier per tile: the scan.  Each warp then merges its own contiguous output range (its 32
-//    threads' outputs are adjacent): 16 elements per lane-step, LDS.128 exponents + LDG.128
-//    sign/mantissa (prefetched before phase 2) -> PRMT sign-replicate compose -> 2x 128-bit stores.
+//  * The decode window is the top word of a 96-bit bit buffer shifted by the consumed bits and
+//    refilled at the warp checks; field extraction uses IMAD.HI so the ALU and FMA pipes share the
+//    work.  Phase 1 keeps (bit offset | count << 8) in one register and adds the T1 entry to it.
+//  * EncodedExponent chunks and gaps of the next tile are staged by TMA (cp.async.bulk + mbarrier)
+//    while the current tile decodes; EncodedExponent is read from HBM exactly once.
+//  * One named barrier per tile (the scan).  Each warp then merges its own contiguous output range:
+//    16 elements per lane-step, LDS.128 exponents + LDG.128 sign/mantissa (prefetched before phase
+//    2) -> PRMT sign-replicate compose -> 2x 128-bit stores.  Tiles whose outputs exceed the SMEM
+//    buffer (extremely compressible tensors) are written directly to HBM instead.
 #include "decode_common.cuh"
 
 namespace df11 {
 namespace {
 
-constexpr int kT = 256;                    // format threads per block == group size
-constexpr int kN = 8;                      // bytes per thread
-constexpr int kGroups = 4;
-constexpr int kCta = kT * kGroups;         // 1024 threads
-constexpr int kR = 9;                      // root bits of the derived tables
+constexpr uint32_t kT = 256;               // format threads per block
+constexpr uint32_t kN = 8;                 // bytes per format thread
+constexpr uint32_t kCpl = 2;               // chunks per lane
+constexpr uint32_t kLanes = kT / kCpl;     // 128 threads per group (one tile)
+constexpr uint32_t kGroups = 8;
+constexpr uint32_t kCta = kLanes * kGroups;  // 1024 threads
+constexpr uint32_t kWarps = kLanes / 32;   // 4 warps per group
+constexpr uint32_t kBits = 8 * kN * kCpl;  // 128 bits decoded per lane
+constexpr uint32_t kR = 9;                 // root bits of the derived tables
 constexpr uint32_t kRows = 1u << kR;
 constexpr uint32_t kTabWords = kRows * 32; // 32 lane replicas
-constexpr uint32_t kExpBuf = 8 * kN * kT + 64;
+constexpr uint32_t kEscRows = 8;           // escape rows with a second-level table
+constexpr uint32_t kR2 = 9;                // bits resolved by the second level
+constexpr uint32_t kLutSmem = 8192;        // format LUTs copied when they fit
+constexpr uint32_t kExpBuf = 8304;         // per-group exponent buffer (bytes)
+constexpr uint32_t kCap = kExpBuf - 32;    // max outputs per tile through SMEM (else direct mode)
+constexpr uint32_t kChunkBytes = kT * kN + 16;   // a tile's EncodedExponent + spill
+constexpr uint32_t kGapBytes = kT * 5 / 8 + 16;  // a tile's 5-bit gaps (+ 1 byte read past)
+constexpr uint32_t kStageBytes = kChunkBytes + kGapBytes;
 
 // SMEM layout (bytes)
 constexpr uint32_t kOffT1 = 0;
 constexpr uint32_t kOffT2 = kOffT1 + kTabWords * 4;
-constexpr uint32_t kEscRows = 8;                              // escape rows with a second-level table
-constexpr uint32_t kR2 = 9;                                   // bits resolved by the second level
-constexpr uint32_t kOffL2 = kOffT2 + kTabWords * 4;           // uint16 [kEscRows][1 << kR2]: sym | len << 8
-constexpr uint32_t kLutSmem = 8192;                           // format LUTs copied when they fit
-constexpr uint32_t kOffLut = kOffL2 + kEscRows * (1u << kR2) * 2;   // uint8/uint16 [k][256]
-constexpr uint32_t kOffLen = kOffLut + kLutSmem;              // CodeLengths[256]
-constexpr uint32_t kOffWsum = kOffLen + 256;                  // [groups][2 parities][8] uint32
-constexpr uint32_t kOffExp = kOffWsum + kGroups * 2 * 8 * 4;  // [groups][kExpBuf]
-constexpr uint32_t kChunkBytes = kT * kN + 16;                // a tile's EncodedExponent + spill
-constexpr uint32_t kGapBytes = kT * 5 / 8 + 16;               // a tile's 5-bit gaps (+ 1 byte read past)
-constexpr uint32_t kStageBytes = kChunkBytes + kGapBytes;     // one TMA stage
-constexpr uint32_t kOffStage = kOffExp + kGroups * kExpBuf;   // [groups][2][kStageBytes]
-constexpr uint32_t kOffMbar = kOffStage + kGroups * 2 * kStageBytes;   // [groups][2] uint64
-constexpr uint32_t kSmemBytes = kOffMbar + kGroups * 2 * 8;
-static_assert(kStageBytes % 16 == 0 && kOffStage % 16 == 0 && kOffMbar % 8 == 0, "TMA alignment");
+constexpr uint32_t kOffL2 = kOffT2 + kTabWords * 4;                 // uint16 [kEscRows][1 << kR2]
+constexpr uint32_t kOffLut = kOffL2 + kEscRows * (1u << kR2) * 2;    // uint8/uint16 [k][256]
+constexpr uint32_t kOffLen = kOffLut + kLutSmem;                     // CodeLengths[256]
+constexpr uint32_t kOffWsum = kOffLen + 256;                         // [groups][2][kWarps] uint32
+constexpr uint32_t kOffExp = kOffWsum + kGroups * 2 * kWarps * 4;    // [groups][kExpBuf]
+constexpr uint32_t kOffStage = kOffExp + kGroups * kExpBuf;          // [groups][kStageBytes]
+constexpr uint32_t kOffMbar = kOffStage + kGroups * kStageBytes;     // [groups] uint64
+constexpr uint32_t kSmemBytes = kOffMbar + kGroups * 8;
+static_assert(kOffExp % 16 == 0 && kExpBuf % 16 == 0 && kStageBytes % 16 == 0 && kOffStage % 16 == 0 &&
+              kOffMbar % 8 == 0, "alignment");
 static_assert(kSmemBytes <= 232448, "SMEM budget");
-static_assert(kOffExp % 16 == 0 && kExpBuf % 16 == 0, "alignment");
 
 extern __shared__ __align__(16) uint32_t smem_w[];
 
 __device__ __forceinline__ uint8_t *smem_b() { return reinterpret_cast<uint8_t *>(smem_w); }
-
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -72,80 +78,20 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     return d;
 }
 
-// Paper's hierarchical LUT walk (P:405-411) over the format tables in global memory; returns the
-// exponent and its code length.  Bounded: <= 4 levels, child < k, zero length -> 32.
-__device__ __noinline__ uint32_t lut_walk(uint32_t w, const df11_device_tensor &ts, uint32_t &len) {
-    const uint8_t *__restrict__ luts = ts.luts;
-    const uint32_t eb = ts.lut_entry_bytes, thr = eb == 1 ? 240u : 256u;
-    uint32_t table = 0, e = 0;
-#pragma unroll 1
-    for (int i = 0; i < 4; i++) {
-        const uint32_t off = table * 256u + ((w >> (24 - 8 * i)) & 0xFFu);
-        e = eb == 1 ? (uint32_t)__ldg(luts + off)
-                    : ((uint32_t)__ldg(luts + 2 * off) | ((uint32_t)__ldg(luts + 2 * off + 1) << 8));
-        if (e < thr) break;
-        table = eb == 1 ? 256u - e : e - 256u;
-        if (table >= ts.k || i == 3) { e = 0; break; }
-    }
-    e &= 0xFFu;
-    len = __ldg(ts.code_lengths + e);
-    if (len == 0) len = 32;
-    return e;
-}
-
-// Same walk over the SMEM copy of the format tables (used when k*256*entry_bytes <= kLutSmem).
-__device__ __forceinline__ uint32_t lut_walk_smem(uint32_t w, const uint8_t *lut, const uint8_t *clen,
-                                                  uint32_t eb, uint32_t k, uint32_t &len) {
-    const uint32_t thr = eb == 1 ? 240u : 256u;
-    uint32_t e = eb == 1 ? lut[w >> 24] : reinterpret_cast<const uint16_t *>(lut)[w >> 24];
-#pragma unroll 1
-    for (int sh = 16; e >= thr; sh -= 8) {
-        const uint32_t table = eb == 1 ? 256u - e : e - 256u;
-        if (table >= k || sh < 0) { e = 0; break; }
-        const uint32_t idx = table * 256u + ((w >> sh) & 0xFFu);
-        e = eb == 1 ? lut[idx] : reinterpret_cast<const uint16_t *>(lut)[idx];
-    }
-    e &= 0xFFu;
-    len = clen[e];
-    if (len == 0) len = 32;
-    return e;
-}
-
-__device__ __forceinline__ void group_bar(int g) {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kT) : "memory");
-}
-
-// 32-bit MSB-first window at bit `off` (0 <= off < 64) of the 96-bit chunk (w0:w1:w2).  Only bits
-// 0..5 of `off` are used, so callers may pass a packed counter.
-__device__ __forceinline__ uint32_t window(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t off) {
-    const bool lo = (off & 32u) == 0;
-    return __funnelshift_l(lo ? w1 : w2, lo ? w0 : w1, off);
-}
-
-// Two BF16 from 2 exponents (bytes 0,1 of E) and 2 sign/mantissa bytes (bytes 0,1 of S) — or bytes
-// 2,3 with hi = true: W = [S0, sign(S0)x8, S1, sign(S1)x8] (PRMT sign replicate), X = [E0,0,E1,0];
-// result = (W & 0x807F807F) + (X << 7)  =  (sign << 15) | (E << 7) | mantissa per half (P:429-434).
-template <bool hi>
-__device__ __forceinline__ uint32_t compose2(uint32_t E, uint32_t S) {
-    const uint32_t W = prmt(S, 0u, hi ? 0xB3A2u : 0x9180u);
-    const uint32_t X = prmt(E, 0u, hi ? 0x4342u : 0x4140u);
-    return (W & 0x807F807Fu) + (X << 7);
-}
-
 // FMA-pipe integer helpers.  The B200 ALU pipe (SHF/LOP3/PRMT/SEL/ISETP) issues a warp instruction
 // every 2 cycles per SMSP, as does the FMA pipe (IMAD*): bit-field extraction is moved onto the FMA
 // pipe with multiplies by powers of two that the compiler cannot strength-reduce (runtime operands).
-__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {     // (a * b) >> 32
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {
     uint32_t d;
     asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
     return d;
 }
-__device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {   // ((a*b) >> 32) + c
+__device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
     asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
 }
-__device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {   // a*b + c
+__device__ __forceinline__ uint32_t madlo(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
@@ -155,26 +101,41 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
-// 96-bit MSB-first bit buffer (a:b:c) shifted left by `s` (0..31; only the low 5 bits are used).
-__device__ __forceinline__ void shift96(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
-    a = __funnelshift_l(b, a, s);
-    b = __funnelshift_l(c, b, s);
-    c = __funnelshift_l(0u, c, s);
-}
-
-// Row `w >> (32-R)` of a lane-private replicated table: address = lane_base + row * 128.
-__device__ __forceinline__ uint32_t lds_row(uint32_t lane_base, uint32_t w) {
-    uint32_t v;
-    asm volatile("{\n\t.reg .u32 t;\n\tshr.u32 t, %1, %3;\n\tmad.lo.u32 t, t, 128, %2;\n\tld.shared.u32 %0, [t];\n\t}"
-                 : "=r"(v) : "r"(w), "r"(lane_base), "n"(32 - kR));
-    return v;
-}
-
 // st.shared.u8 [addr + k] = v, predicated on pos < lim (no branch).
 template <int k>
 __device__ __forceinline__ void sts8_if(uint32_t addr, uint32_t v, uint32_t pos, uint32_t lim) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p st.shared.u8 [%0+%4], %1;\n\t}"
                  ::"r"(addr), "r"(v), "r"(pos), "r"(lim), "n"(k) : "memory");
+}
+
+// 96-bit MSB-first bit buffer (a:b:c) shifted left by `s` (only the low 5 bits of s are used).
+__device__ __forceinline__ void shift96(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
+    a = __funnelshift_l(b, a, s);
+    b = __funnelshift_l(c, b, s);
+    c = __funnelshift_l(0u, c, s);
+}
+// Shift by 0..63 bits (escape path).
+__device__ __forceinline__ void shift96_long(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
+    if (s >= 32) { a = b; b = c; c = 0; s -= 32; }
+    shift96(a, b, c, s);
+}
+// PTX shifts clamp the shift amount: any amount >= 32 (incl. "negative" unsigned) yields 0.
+__device__ __forceinline__ uint32_t shl_c(uint32_t x, uint32_t n) {
+    uint32_t d;
+    asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(n));
+    return d;
+}
+__device__ __forceinline__ uint32_t shr_c(uint32_t x, uint32_t n) {
+    uint32_t d;
+    asm("shr.b32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(n));
+    return d;
+}
+// OR word w into the buffer at bit position v (0 = top, v < 96); bits below the valid region are
+// zero.  Branch-free: every out-of-range term shifts by >= 32 and vanishes.
+__device__ __forceinline__ void insert96(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t v, uint32_t w) {
+    a |= shr_c(w, v);
+    b |= shl_c(w, 32u - v) | shr_c(w, v - 32u);
+    c |= shl_c(w, 64u - v) | shr_c(w, v - 64u);
 }
 
 // ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier
@@ -193,46 +154,101 @@ __device__ __forceinline__ void tma_g2s(uint32_t dst, const void *src, uint32_t 
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
-// Stage format block b of tensor ts (its EncodedExponent chunk + spill, and its gaps) into `stage`.
+// Stage format block b of tensor ts (EncodedExponent chunk + spill, and its gaps) into `stage`.
 __device__ __forceinline__ void issue_tile(const df11_device_tensor &ts, uint32_t b, uint32_t stage, uint32_t bar) {
     mbar_expect_tx(bar, kChunkBytes + kGapBytes);
     tma_g2s(stage, ts.encoded_exponent + (size_t)b * (kT * kN), kChunkBytes, bar);
     tma_g2s(stage + kChunkBytes, ts.gaps + (size_t)b * (kT * 5 / 8), kGapBytes, bar);
 }
 
+// Paper's hierarchical LUT walk (P:405-411) over the format tables in global memory; returns the
+// exponent and its code length.  Bounded: <= 4 levels, child < k, zero length -> 32.
+__device__ __noinline__ uint32_t lut_walk_global(uint32_t w, const df11_device_tensor &ts, uint32_t &len) {
+    const uint8_t *__restrict__ luts = ts.luts;
+    const uint32_t eb = ts.lut_entry_bytes, thr = eb == 1 ? 240u : 256u;
+    uint32_t table = 0, e = 0;
+#pragma unroll 1
+    for (int i = 0; i < 4; i++) {
+        const uint32_t off = table * 256u + ((w >> (24 - 8 * i)) & 0xFFu);
+        e = eb == 1 ? (uint32_t)__ldg(luts + off)
+                    : ((uint32_t)__ldg(luts + 2 * off) | ((uint32_t)__ldg(luts + 2 * off + 1) << 8));
+        if (e < thr) break;
+        table = eb == 1 ? 256u - e : e - 256u;
+        if (table >= ts.k || i == 3) { e = 0; break; }
+    }
+    e &= 0xFFu;
+    len = __ldg(ts.code_lengths + e);
+    if (len == 0) len = 32;
+    return e;
+}
+
+// The same walk over the SMEM copy of the format tables (narrow or wide).
+__device__ __forceinline__ uint32_t lut_walk_smem(uint32_t w, uint32_t lut, uint32_t clen, uint32_t eb,
+                                                  uint32_t k, uint32_t &len) {
+    const uint32_t thr = eb == 1 ? 240u : 256u;
+    uint32_t e = 0, table = 0;
+#pragma unroll 1
+    for (int i = 0, sh = 24; i < 4; i++, sh -= 8) {
+        const uint32_t idx = table * 256u + ((w >> sh) & 0xFFu);
+        if (eb == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(e) : "r"(lut + idx));
+        else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(lut + 2 * idx));
+        if (e < thr) break;
+        table = eb == 1 ? 256u - e : e - 256u;
+        if (table >= k || i == 3) { e = 0; break; }
+    }
+    e &= 0xFFu;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(len) : "r"(clen + e));
+    if (len == 0) len = 32;
+    return e;
+}
+
+__device__ __forceinline__ void group_bar(uint32_t g) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kLanes) : "memory");
+}
+
+// Two BF16 from 2 exponents (bytes 0,1 of E) and 2 sign/mantissa bytes (bytes 0,1 of S) — or bytes
+// 2,3 with hi = true: W = [S0, sign(S0)x8, S1, sign(S1)x8] (PRMT sign replicate), X = [E0,0,E1,0];
+// result = (W & 0x807F807F) + (X << 7)  =  (sign << 15) | (E << 7) | mantissa per half (P:429-434).
+template <bool hi>
+__device__ __forceinline__ uint32_t compose2(uint32_t E, uint32_t S) {
+    const uint32_t W = prmt(S, 0u, hi ? 0xB3A2u : 0x9180u);
+    const uint32_t X = prmt(E, 0u, hi ? 0x4342u : 0x4140u);
+    return (W & 0x807F807Fu) + (X << 7);
+}
+
 __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ Batch bt) {
     const uint32_t tid = threadIdx.x;
-    const int g = (int)(tid / kT);
-    const uint32_t t = tid % kT;
+    const uint32_t g = tid / kLanes;
+    const uint32_t t = tid % kLanes;
     const uint32_t lane = tid & 31, wig = t >> 5;
     const uint32_t FULL = 0xFFFFFFFFu;
-    const uint32_t one = blockDim.x >> 10;                       // == 1, opaque to the compiler
-    const uint32_t K_ROW = one << kR, K_128 = one << 7, K_S24 = one << 8, K_S8 = one << 24,
-                   K_S16 = one << 16, K_S29 = one << 3;
+    // IMAD multipliers from the constant bank (see Batch::kpow)
+#define K_ROW bt.kpow[0]
+#define K_128 bt.kpow[1]
+#define K_S24 bt.kpow[2]
+#define K_S8 bt.kpow[3]
+#define K_S16 bt.kpow[4]
+#define K_S29 bt.kpow[5]
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
-    // lane-private table addresses: row r of table X is at X + r*128 + lane*4
-    const uint32_t t1_lane = sbase + kOffT1 + lane * 4u;
+    const uint32_t t1_lane = sbase + kOffT1 + lane * 4u;         // row r at + r*128
     const uint32_t t2_lane = sbase + kOffT2 + lane * 4u;
-    const uint32_t ebuf_off = kOffExp + (uint32_t)g * kExpBuf;             // byte offset into smem
-    uint32_t *wsum = smem_w + kOffWsum / 4 + (uint32_t)g * 16;            // [2][8]
+    const uint32_t ebuf_off = kOffExp + g * kExpBuf;
+    uint32_t *wsum = smem_w + kOffWsum / 4 + g * 2 * kWarps;
+    const uint32_t stage = sbase + kOffStage + g * kStageBytes;
+    const uint32_t mbar = sbase + kOffMbar + g * 8;
 
     const uint32_t total = bt.total_tiles;
     const uint32_t c_begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
     const uint32_t c_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
     if (c_begin >= c_end) return;
-
-    const uint32_t stage0 = sbase + kOffStage + (uint32_t)g * 2 * kStageBytes;
-    const uint32_t mbar0 = sbase + kOffMbar + (uint32_t)g * 16;
     if (t == 0) {
-        mbar_init(mbar0, 1);
-        mbar_init(mbar0 + 8, 1);
+        mbar_init(mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
-    uint32_t q = 0;                    // tiles consumed by this group so far (stage = q & 1)
+    uint32_t q = 0;                    // tiles consumed by this group (mbarrier phase = q & 1)
+    uint32_t parity = 0;               // wsum double buffer
 
-    uint32_t parity = 0;
     int ti_idx = tensor_of_tile(bt, c_begin);
     for (uint32_t seg_begin = c_begin; seg_begin < c_end; ti_idx++) {
         const df11_device_tensor &ts = bt.t[ti_idx];
@@ -240,47 +256,31 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
         const uint32_t base_tile = bt.tile_start[ti_idx];
         if (seg_end <= seg_begin) continue;
 
-        // ---- derived tables for this tensor (CTA-wide)
+        // =============================== derived tables for this tensor (CTA-wide)
         __syncthreads();
-        const uint32_t lut_bytes = ts.k * 256u * ts.lut_entry_bytes;
+        const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
+        const uint32_t lut_bytes = kk * 256u * eb_bytes;
         const bool lut_in_smem = lut_bytes <= kLutSmem;
         if (lut_in_smem)
             for (uint32_t i = tid; i < lut_bytes; i += kCta) sb[kOffLut + i] = __ldg(ts.luts + i);
         for (uint32_t i = tid; i < 256u; i += kCta) sb[kOffLen + i] = __ldg(ts.code_lengths + i);
-        uint32_t *esc_mask = smem_w + kOffExp / 4;                 // scratch: the exponent buffers are idle
+        uint32_t *esc_mask = smem_w + kOffExp / 4;                 // scratch: exponent buffers are idle
         uint32_t *esc_row = esc_mask + kRows / 32;
         if (tid < kRows / 32) esc_mask[tid] = 0;
         __syncthreads();
-        const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
-        const bool narrow_smem = lut_in_smem && eb_bytes == 1;
-        // the paper's LUT walk for one code at the top of window w
         auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
-            if (narrow_smem) {                                  // root, then child tables via 256 - v
-                const uint32_t lb = sbase + kOffLut;
-                uint32_t e, sh = 24, table = 0;
-#pragma unroll 1
-                for (int i = 0; i < 4; i++, sh -= 8) {
-                    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(e) : "r"(lb + table * 256u + ((w >> sh) & 0xFFu)));
-                    if (e < 240u) break;
-                    table = 256u - e;
-                    if (table >= kk || i == 3) { e = 0; break; }
-                }
-                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(len) : "r"(sbase + kOffLen + e));
-                if (len == 0) len = 32;
-                return e;
-            }
-            if (lut_in_smem) return lut_walk_smem(w, sb + kOffLut, sb + kOffLen, eb_bytes, kk, len);
-            return lut_walk(w, ts, len);
+            if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, len);
+            return lut_walk_global(w, ts, len);
         };
         uint32_t row_e1 = 0, row_e2 = 0;
         bool row_esc = false;
         if (tid < kRows) {
-            const uint32_t idx = tid, W = idx << (32 - kR);
+            const uint32_t W = tid << (32 - kR);
             uint32_t s = 0, cnt = 0, mask = 0, cons = 0, syms = 0, c2 = 0, cons2 = 0;
-            while (s < (uint32_t)kR) {
+            while (s < kR) {
                 uint32_t len;
                 const uint32_t sym = walk(W << s, len);
-                if (len > (uint32_t)kR - s) break;
+                if (len > kR - s) break;
                 mask |= 1u << s;
                 cnt++;
                 s += len;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             row_esc = cnt == 0;
             row_e1 = cons | (cnt << 8) | (mask << 23);
             row_e2 = syms | (cons2 << 24) | (c2 << 29);
-            if (row_esc) atomicOr(esc_mask + idx / 32, 1u << (idx % 32));
+            if (row_esc) atomicOr(esc_mask + tid / 32, 1u << (tid % 32));
         }
         __syncthreads();
         if (row_esc) {                                             // id = 1 + rank among escape rows
@@ -316,16 +316,16 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             for (uint32_t q2 = 0; q2 < kRows / 32; q2++) n_esc += __popc(esc_mask[q2]);
             n_esc = min(n_esc, kEscRows);
             uint16_t *l2 = reinterpret_cast<uint16_t *>(sb + kOffL2);
-            for (uint32_t i = tid; i < n_esc << kR2; i += kCta) {
+            for (uint32_t i = tid; i < (n_esc << kR2); i += kCta) {
                 const uint32_t row = esc_row[i >> kR2], j = i & ((1u << kR2) - 1u);
                 uint32_t len;
                 const uint32_t sym = walk((row << (32 - kR)) | (j << (32 - kR - kR2)), len);
-                l2[i] = len <= (uint32_t)(kR + kR2) ? (uint16_t)(sym | (len << 8)) : (uint16_t)0;
+                l2[i] = len <= kR + kR2 ? (uint16_t)(sym | (len << 8)) : (uint16_t)0;
             }
         }
         __syncthreads();
 
-        // resolve one code longer than R bits at the top of `a` (escape row id from the table entry)
+        // resolve one code longer than R bits at the top of window a_ (escape row id from the entry)
         auto escape = [&](uint32_t a_, uint32_t id, uint32_t &len) -> uint32_t {
             if (id != 0) {
                 uint32_t v;
@@ -340,12 +340,9 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
         const uint4 *__restrict__ psm4 = reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa);
         uint16_t *__restrict__ out = ts.out;
 
+        // =============================== tiles of this group
         uint32_t tile = seg_begin + g;
-        if (t == 0) {                                                          // producer: first two tiles
-            if (tile < seg_end) issue_tile(ts, tile - base_tile, stage0 + (q & 1) * kStageBytes, mbar0 + (q & 1) * 8);
-            if (tile + kGroups < seg_end)
-                issue_tile(ts, tile + kGroups - base_tile, stage0 + ((q + 1) & 1) * kStageBytes, mbar0 + ((q + 1) & 1) * 8);
-        }
+        if (t == 0 && tile < seg_end) issue_tile(ts, tile - base_tile, stage, mbar);
         uint32_t nlo = 0, nhi = 0;
         if (tile < seg_end) {
             nlo = __ldg(ts.block_output_pos + tile - base_tile);
@@ -359,122 +356,159 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 nlo = __ldg(ts.block_output_pos + b + kGroups);
                 nhi = __ldg(ts.block_output_pos + b + kGroups + 1);
             }
-            const uint32_t st = stage0 + (q & 1) * kStageBytes;
-            mbar_wait(mbar0 + (q & 1) * 8, (q >> 1) & 1u);
-            uint32_t gap, raw0, raw1, raw2;
+            mbar_wait(mbar, q & 1u);
+            // this lane's 20 stream bytes (chunks 2t, 2t+1 + spill) and the first chunk's gap
+            uint32_t r0, r1, r2, r3, r4, gap;
             {
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(stage + t * 16));
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r4) : "r"(stage + t * 16 + 16));
                 uint32_t h0, h1;
-                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(raw0), "=r"(raw1) : "r"(st + t * kN));
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw2) : "r"(st + t * kN + 8));
-                const uint32_t gb0 = st + kChunkBytes + ((t * 5) >> 3);
+                const uint32_t gb0 = stage + kChunkBytes + ((t * 10) >> 3);  // gap field of chunk 2t
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h0) : "r"(gb0));
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h1) : "r"(gb0 + 1));
-                gap = (((h0 << 8) | h1) >> (11u - ((t * 5) & 7u))) & 31u;
+                gap = (((h0 << 8) | h1) >> (11u - ((t * 10) & 7u))) & 31u;
             }
             const uint32_t lo = min(clo, N);
-            const uint32_t hi = min(max(min(chi, N), lo), lo + (uint32_t)(8 * kN * kT));
+            const uint32_t hi = min(max(min(chi, N), lo), lo + 8 * kN * kT);
             const uint32_t f = lo & ~15u;                                      // 16-element frame
+            const bool direct = hi - lo > kCap;                                // group-uniform
 
-            // ---- phase 1: bit buffer (a:b:c) starts at the gap; acc = offset | count << 8 (+ junk >= bit 23)
-            uint32_t a = bswap32(raw0), bb = bswap32(raw1), c = bswap32(raw2);
+            // ---- phase 1: count the codes that start in [gap, 128)
+            uint32_t a = bswap32(r0), bb = bswap32(r1), c = bswap32(r2);
+            const uint32_t w3 = bswap32(r3), w4 = bswap32(r4);
             shift96(a, bb, c, gap);
-            uint32_t acc = gap, e1 = 1;
+            uint32_t acc = gap, e1 = 1, fill = 96;                             // acc = offset | count << 8
+            // keep >= 64 valid bits in the buffer (or the whole 160-bit stream) at every warp check
+            auto refill = [&](uint32_t off_) {
+                if (fill < 160 && fill - off_ < 64) {
+                    insert96(a, bb, c, fill - off_, fill == 96 ? w3 : w4);
+                    fill += 32;
+                }
+            };
             for (;;) {
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     const uint32_t e = lds32(madlo(mulhi(a, K_ROW), K_128, t1_lane));
-                    if ((acc & 0xC0u) == 0) {                                  // offset < 64: still ours
+                    if ((acc & 0x80u) == 0) {                                  // offset < 128: still ours
                         acc += e;
                         e1 = e;
                     }
                     shift96(a, bb, c, e);                                      // e & 31 = consumed bits
                 }
-                const bool live = (acc & 0xC0u) == 0, esc = live && (e1 & 0x7FFFFFu) == 0;
+                const bool live = (acc & 0x80u) == 0, esc = live && (e1 & 0x7FFFFFu) == 0;
                 const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
                 if (!(flags & 1u)) break;
+                refill(acc & 0xFFu);
                 if (flags & 2u) {
                     if (esc) {                                                 // code longer than R bits
                         uint32_t len;
                         escape(a, e1 >> 23, len);
                         e1 = 0;                                                // exactly one code: no fixup
                         acc += len + (1u << 8);
-                        shift96(a, bb, c, len & 31u);
-                        if (len == 32) { a = bb; bb = c; c = 0; }
+                        shift96_long(a, bb, c, len);
+                        refill(acc & 0xFFu);
+                        refill(acc & 0xFFu);
                     }
                 }
             }
-            uint32_t cnt = (acc >> 8) & 0x7Fu;
-            if ((e1 & 0x7FFFFFu) != 0) {   // last T1 group may hold complete codes starting at bit >= 64
-                const uint32_t last = (acc & 0xFFu) - (e1 & 0xFu);             // < 64
-                cnt -= __popc((e1 >> 23) >> min(64u - last, 31u));
+            uint32_t cnt = (acc >> 8) & 0xFFu;
+            if ((e1 & 0x7FFFFFu) != 0) {   // the last T1 group may hold complete codes starting at >= 128
+                const uint32_t last = (acc & 0xFFu) - (e1 & 0xFu);
+                cnt -= __popc((e1 >> 23) >> min(kBits - last, 31u));
             }
 
-            // ---- block exclusive scan of the counts: warp shuffles + 8 warp totals (1 barrier)
+            // ---- exclusive scan of the counts over the tile: warp shuffles + 4 warp totals
             uint32_t incl = cnt;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const uint32_t v = __shfl_up_sync(FULL, incl, d);
                 if (lane >= (uint32_t)d) incl += v;
             }
-            uint32_t *ws = wsum + parity * 8;
+            uint32_t *ws = wsum + parity * kWarps;
             if (lane == 31) ws[wig] = incl;
-            group_bar(g);                          // every thread has read this tile's stage
+            group_bar(g);                          // also: every thread has read this tile's stage
             parity ^= 1u;
-            if (t == 0 && tile + 2 * kGroups < seg_end)
-                issue_tile(ts, b + 2 * kGroups, st, mbar0 + (q & 1) * 8);
+            if (t == 0 && has_next) issue_tile(ts, b + kGroups, stage, mbar);
             uint32_t wpre = 0;
             {
-                const uint4 a = *reinterpret_cast<const uint4 *>(ws);
-                const uint4 c = *reinterpret_cast<const uint4 *>(ws + 4);
-                const uint32_t v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-#pragma unroll
-                for (uint32_t q = 0; q < 7; q++) wpre += q < wig ? v[q] : 0u;
+                const uint4 v = *reinterpret_cast<const uint4 *>(ws);
+                wpre = (wig > 0 ? v.x : 0u) + (wig > 1 ? v.y : 0u) + (wig > 2 ? v.z : 0u);
             }
             const uint32_t wtot = __shfl_sync(FULL, incl, 31);
+            const uint32_t pos0 = wpre + incl - cnt;                           // this lane's first output
             // this warp's output range [ra, rb) (absolute elements), clipped to the tile
             const uint32_t ra = min(lo + wpre, hi), rb = min(lo + wpre + wtot, hi);
             // full 16-element groups [ga, gb) take the vector path; the <= 15 + 15 edge elements
             // [ra, ha) and [tb, rb) are shared with the neighbouring warps and go one per lane
-            const uint32_t ga = vec_out ? (ra + 15) >> 4 : 0, gb = vec_out ? max(rb >> 4, ga) : 0;
-            const uint32_t ha = vec_out ? min(ga << 4, rb) : rb, tb = vec_out ? max(gb << 4, ha) : rb;
+            const bool vec = vec_out && !direct;
+            const uint32_t ga = vec ? (ra + 15) >> 4 : 0, gb = vec ? max(rb >> 4, ga) : 0;
+            const uint32_t ha = vec ? min(ga << 4, rb) : rb, tb = vec ? max(gb << 4, ha) : rb;
             uint4 smA = make_uint4(0, 0, 0, 0), smB = make_uint4(0, 0, 0, 0);
             if (ga + lane < gb) smA = __ldg(psm4 + ga + lane);                 // prefetch for the merge
             if (ga + lane + 32 < gb) smB = __ldg(psm4 + ga + lane + 32);
             const uint32_t es = lane < 16 ? ra + lane : tb + (lane - 16);      // this lane's edge element
-            const bool edge = vec_out && (lane < 16 ? es < ha : es < rb);
+            const bool edge = vec && (lane < 16 ? es < ha : es < rb);
             uint32_t sm1 = 0;
             if (edge) sm1 = __ldg(ts.packed_sign_mantissa + es);
 
-            // ---- phase 2: re-decode with T2 (<= 3 exponents per lookup) into the SMEM buffer
-            const uint32_t wp0 = sbase + ebuf_off + (lo - f) + wpre + incl - cnt;
-            const uint32_t wend = wp0 + cnt;
-            const uint32_t wend1 = wend - 1, wend2 = wend - 2;
-            uint32_t wp = wp0, e2 = 1;
-            a = bswap32(raw0); bb = bswap32(raw1); c = bswap32(raw2);
+            // ---- phase 2: re-decode with T2 (<= 3 exponents per lookup)
+            a = bswap32(r0); bb = bswap32(r1); c = bswap32(r2);
             shift96(a, bb, c, gap);
-            for (;;) {
+            fill = 96;
+            uint32_t off = gap;
+            if (!direct) {
+                const uint32_t wp0 = sbase + ebuf_off + (lo - f) + pos0;
+                const uint32_t wend = wp0 + cnt, wend1 = wend - 1, wend2 = wend - 2;
+                uint32_t wp = wp0, e2 = 1, off2 = gap;                         // off2 = off + 32 * (wp - wp0)
+                for (;;) {
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    // finished lanes keep advancing harmlessly: every store is predicated on wp
-                    e2 = lds32(madlo(mulhi(a, K_ROW), K_128, t2_lane));
-                    sts8_if<0>(wp, e2, wp, wend);
-                    sts8_if<1>(wp, mulhi(e2, K_S8), wp, wend1);
-                    sts8_if<2>(wp, mulhi(e2, K_S16), wp, wend2);
-                    wp = madhi(e2, K_S29, wp);                                 // wp += count
-                    shift96(a, bb, c, mulhi(e2, K_S24));                       // (e2 >> 24) & 31 = consumed
-                }
-                const bool live = wp < wend, esc = live && e2 < (1u << 24);
-                const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
-                if (!(flags & 1u)) break;
-                if (flags & 2u) {
-                    if (esc) {
-                        uint32_t len;
-                        const uint32_t sym = escape(a, e2 & 0xFFu, len);
-                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(wp), "r"(sym) : "memory");
-                        wp++;
-                        shift96(a, bb, c, len & 31u);
-                        if (len == 32) { a = bb; bb = c; c = 0; }
+                    for (int u = 0; u < 4; u++) {
+                        // finished lanes keep advancing harmlessly: every store is predicated on wp
+                        e2 = lds32(madlo(mulhi(a, K_ROW), K_128, t2_lane));
+                        sts8_if<0>(wp, e2, wp, wend);
+                        sts8_if<1>(wp, mulhi(e2, K_S8), wp, wend1);
+                        sts8_if<2>(wp, mulhi(e2, K_S16), wp, wend2);
+                        const uint32_t s = mulhi(e2, K_S24);                   // consumed | count << 5
+                        off2 += s;
+                        wp = madhi(e2, K_S29, wp);                             // wp += count
+                        shift96(a, bb, c, s);                                  // s & 31 = consumed
                     }
+                    const bool live = wp < wend, esc = live && e2 < (1u << 24);
+                    const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
+                    if (!(flags & 1u)) break;
+                    off = off2 - 32u * (wp - wp0);
+                    refill(off);
+                    if (flags & 2u) {
+                        if (esc) {
+                            uint32_t len;
+                            const uint32_t sym = escape(a, e2 & 0xFFu, len);
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(wp), "r"(sym) : "memory");
+                            wp++;
+                            off += len;
+                            off2 += len + 32u;
+                            shift96_long(a, bb, c, len);
+                            refill(off);
+                            refill(off);
+                        }
+                    }
+                }
+            } else {
+                // direct mode (more than kCap outputs in this tile): compose and store to HBM per code
+                uint32_t p = lo + pos0;
+                const uint32_t pend = min(lo + pos0 + cnt, hi);
+                while (p < pend) {
+                    uint32_t len;
+                    const uint32_t e = lds32(madlo(mulhi(a, K_ROW), K_128, t2_lane));
+                    uint32_t syms, n, consumed;
+                    if (e >= (1u << 24)) { syms = e; n = e >> 29; consumed = (e >> 24) & 15u; }
+                    else { syms = escape(a, e & 0xFFu, len); n = 1; consumed = len; }
+                    for (uint32_t i = 0; i < n && p < pend; i++, p++)
+                        out[p] = compose((syms >> (8 * i)) & 0xFFu, __ldg(ts.packed_sign_mantissa + p));
+                    off += consumed;
+                    shift96_long(a, bb, c, consumed);
+                    refill(off);
+                    refill(off);
                 }
             }
             __syncwarp();
@@ -499,7 +533,7 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 dst[0] = o0;
                 dst[1] = o1;
             }
-            if (!vec_out)                                                      // unaligned output: scalar
+            if (!vec_out && !direct)                                          // unaligned output: scalar
                 for (uint32_t e = ra + lane; e < rb; e += 32)
                     out[e] = compose(ebf[e - f], __ldg(ts.packed_sign_mantissa + e));
         }
@@ -512,7 +546,7 @@ int g_attr_set[64];
 }  // namespace
 
 bool fast_supports(const df11_device_tensor &t) {
-    return t.T == (uint32_t)kT && t.n == (uint32_t)kN &&
+    return t.T == kT && t.n == kN &&
            (reinterpret_cast<uintptr_t>(t.encoded_exponent) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.gaps) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.packed_sign_mantissa) & 15) == 0 &&
