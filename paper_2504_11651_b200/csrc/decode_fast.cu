@@ -384,6 +384,10 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 if (fill < 160 && fill - off_ < 64) {
                     insert96(a, bb, c, fill - off_, fill == 96 ? w3 : w4);
                     fill += 32;
+                    if (fill < 160 && fill - off_ < 64) {                     // rare: after escapes
+                        insert96(a, bb, c, fill - off_, w4);
+                        fill += 32;
+                    }
                 }
             };
             for (;;) {
@@ -407,8 +411,7 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                         e1 = 0;                                                // exactly one code: no fixup
                         acc += len + (1u << 8);
                         shift96_long(a, bb, c, len);
-                        refill(acc & 0xFFu);
-                        refill(acc & 0xFFu);
+                        if (len > kR + kR2) refill(acc & 0xFFu);               // long walked code
                     }
                 }
             }
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                         sts8_if<2>(wp, mulhi(e2, K_S16), wp, wend2);
                         const uint32_t s = mulhi(e2, K_S24);                   // consumed | count << 5
                         off2 += s;
-                        wp = madhi(e2, K_S29, wp);                             // wp += count
+                        wp += e2 >> 29;                                        // count (LEA.HI)
                         shift96(a, bb, c, s);                                  // s & 31 = consumed
                     }
                     const bool live = wp < wend, esc = live && e2 < (1u << 24);
@@ -488,8 +491,7 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                             off += len;
                             off2 += len + 32u;
                             shift96_long(a, bb, c, len);
-                            refill(off);
-                            refill(off);
+                            if (len > kR + kR2) refill(off);                   // long walked code
                         }
                     }
                 }
@@ -507,7 +509,6 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                         out[p] = compose((syms >> (8 * i)) & 0xFFu, __ldg(ts.packed_sign_mantissa + p));
                     off += consumed;
                     shift96_long(a, bb, c, consumed);
-                    refill(off);
                     refill(off);
                 }
             }

@@ -53,7 +53,7 @@ def _check_oracle_format(df11, oracle_mod, w, kernel, **kw):
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("case", ["gauss_1m", "gauss_ragged", "constant_1bit", "two_symbol", "all_patterns_wide",
                                   "overflow_wide", "fibonacci_32bit", "one_element", "tiny_17", "sigma_large",
-                                  "random_bits"])
+                                  "random_bits", "escape_heavy", "escape_deep"])
 def test_parity_cases(df11, oracle_mod, kernel, case):
     if case == "gauss_1m":
         w = workloads.gaussian_bf16((1 << 20,), seed=1)
@@ -77,6 +77,17 @@ def test_parity_cases(df11, oracle_mod, kernel, case):
         w = workloads.gaussian_bf16((17,), seed=3)
     elif case == "sigma_large":
         w = workloads.gaussian_bf16((777777,), seed=4, sigma=3.0)
+    elif case == "escape_heavy":
+        # 16 frequent exponents (~4-bit codes) + 200 rare ones (~12-bit codes): many codes are
+        # longer than the 9-bit root (~9 %: (escape rows, second-level tables, bit-buffer refills)
+        counts = {100 + i: 24000 for i in range(16)}
+        counts.update({i: 200 for i in range(1, 100)})
+        counts.update({116 + i: 200 for i in range(101)})
+        w = workloads.from_exponent_histogram(counts, seed=7)
+    elif case == "escape_deep":
+        # geometric tail: codes up to ~26 bits, some beyond the second level (walk path)
+        counts = {e: max(1, int(400000 * 0.72 ** i)) for i, e in enumerate(range(60, 200))}
+        w = workloads.from_exponent_histogram(counts, seed=8)
     else:
         w = np.random.default_rng(5).integers(0, 1 << 16, size=400001, dtype=np.uint32).astype(np.uint16)
     _check_oracle_format(df11, oracle_mod, w, kernel)
