@@ -216,6 +216,15 @@ __device__ __forceinline__ uint32_t compose2(uint32_t E, uint32_t S) {
     return (W & 0x807F807Fu) + (X << 7);
 }
 
+// Four BF16 from 4 exponents E and 4 sign/mantissa bytes S, as byte planes: the high byte of each
+// BF16 is sign | E >> 1, the low byte (E & 1) << 7 | mantissa; PRMT interleaves them.
+__device__ __forceinline__ void compose4(uint32_t E, uint32_t S, uint32_t &lo2, uint32_t &hi2) {
+    const uint32_t H = (S & 0x80808080u) | ((E >> 1) & 0x7F7F7F7Fu);
+    const uint32_t L = ((E << 7) & 0x80808080u) | (S & 0x7F7F7F7Fu);
+    lo2 = prmt(L, H, 0x5140u);
+    hi2 = prmt(L, H, 0x7362u);
+}
+
 __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ Batch bt) {
     const uint32_t tid = threadIdx.x;
     const uint32_t g = tid / kLanes;
@@ -357,66 +366,74 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 nhi = __ldg(ts.block_output_pos + b + kGroups + 1);
             }
             mbar_wait(mbar, q & 1u);
-            // this lane's 20 stream bytes (chunks 2t, 2t+1 + spill) and the first chunk's gap
-            uint32_t r0, r1, r2, r3, r4, gap;
+            // this lane's 20 stream bytes (chunks 2t, 2t+1 + spill) and both chunks' gaps
+            uint32_t r0, r1, r2, r3, r4, gapA, gapB;
             {
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(stage + t * 16));
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r4) : "r"(stage + t * 16 + 16));
-                uint32_t h0, h1;
-                const uint32_t gb0 = stage + kChunkBytes + ((t * 10) >> 3);  // gap field of chunk 2t
+                // 10 gap bits of chunks 2t, 2t+1 start at bit 10t: read the aligned 16-bit window
+                uint32_t h0, h1, h2;
+                const uint32_t gb0 = stage + kChunkBytes + ((t * 10) >> 3);
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h0) : "r"(gb0));
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h1) : "r"(gb0 + 1));
-                gap = (((h0 << 8) | h1) >> (11u - ((t * 10) & 7u))) & 31u;
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(h2) : "r"(gb0 + 2));
+                const uint32_t g24 = (h0 << 16) | (h1 << 8) | h2;                // bit 10t at bit 23-(10t&7)
+                const uint32_t g10 = (g24 >> (14u - ((t * 10) & 7u))) & 1023u;
+                gapA = g10 >> 5;
+                gapB = g10 & 31u;
             }
             const uint32_t lo = min(clo, N);
             const uint32_t hi = min(max(min(chi, N), lo), lo + 8 * kN * kT);
             const uint32_t f = lo & ~15u;                                      // 16-element frame
             const bool direct = hi - lo > kCap;                                // group-uniform
+            const uint32_t W0 = bswap32(r0), W1 = bswap32(r1), W2 = bswap32(r2), W3 = bswap32(r3),
+                           W4 = bswap32(r4);
 
-            // ---- phase 1: count the codes that start in [gap, 128)
-            uint32_t a = bswap32(r0), bb = bswap32(r1), c = bswap32(r2);
-            const uint32_t w3 = bswap32(r3), w4 = bswap32(r4);
-            shift96(a, bb, c, gap);
-            uint32_t acc = gap, e1 = 1, fill = 96;                             // acc = offset | count << 8
-            // keep >= 64 valid bits in the buffer (or the whole 160-bit stream) at every warp check
-            auto refill = [&](uint32_t off_) {
-                if (fill < 160 && fill - off_ < 64) {
-                    insert96(a, bb, c, fill - off_, fill == 96 ? w3 : w4);
-                    fill += 32;
-                    if (fill < 160 && fill - off_ < 64) {                     // rare: after escapes
-                        insert96(a, bb, c, fill - off_, w4);
-                        fill += 32;
-                    }
-                }
-            };
+            // ---- phase 1: count the codes that start in chunk 2t ("A": bits [gapA, 64)), then in
+            // chunk 2t+1 ("B": bits [64+gapB, 128)).  Each sub-stream fits a 96-bit bit buffer; a lane
+            // switches from A to B at the first warp check after A is done.
+            uint32_t a = W0, bb = W1, c = W2;
+            shift96(a, bb, c, gapA);
+            uint32_t acc = gapA, e1 = 1, lim = 0xC0u, cntA = 0;                // acc = offset | count << 8
             for (;;) {
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     const uint32_t e = lds32(madlo(mulhi(a, K_ROW), K_128, t1_lane));
-                    if ((acc & 0x80u) == 0) {                                  // offset < 128: still ours
+                    if ((acc & lim) == 0) {                                    // offset below the sub-stream end
                         acc += e;
                         e1 = e;
                     }
                     shift96(a, bb, c, e);                                      // e & 31 = consumed bits
                 }
-                const bool live = (acc & 0x80u) == 0, esc = live && (e1 & 0x7FFFFFu) == 0;
-                const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
-                if (!(flags & 1u)) break;
-                refill(acc & 0xFFu);
-                if (flags & 2u) {
+                const bool act = (acc & lim) == 0;
+                const bool live = act || lim == 0xC0u;
+                if (!__any_sync(FULL, live)) break;
+                const bool esc = act && (e1 & 0x7FFFFFu) == 0;
+                if (__any_sync(FULL, esc)) {
                     if (esc) {                                                 // code longer than R bits
                         uint32_t len;
                         escape(a, e1 >> 23, len);
                         e1 = 0;                                                // exactly one code: no fixup
                         acc += len + (1u << 8);
                         shift96_long(a, bb, c, len);
-                        if (len > kR + kR2) refill(acc & 0xFFu);               // long walked code
                     }
+                }
+                if (!act && lim == 0xC0u) {                                    // A done: drop codes >= bit 64
+                    if ((e1 & 0x7FFFFFu) != 0) {
+                        const uint32_t last = (acc & 0xFFu) - (e1 & 0xFu);
+                        acc -= (uint32_t)__popc((e1 >> 23) >> min(64u - last, 31u)) << 8;
+                    }
+                    cntA = (acc >> 8) & 0xFFu;
+                    acc = (acc & ~0xFFu) | (64u + gapB);                       // ... and start B
+                    lim = 0x80u;
+                    a = W2; bb = W3; c = W4;
+                    shift96(a, bb, c, gapB);
+                    e1 = 1;
                 }
             }
             uint32_t cnt = (acc >> 8) & 0xFFu;
-            if ((e1 & 0x7FFFFFu) != 0) {   // the last T1 group may hold complete codes starting at >= 128
+            if ((e1 & 0x7FFFFFu) != 0) {   // B's last T1 group may hold complete codes starting at >= 128
                 const uint32_t last = (acc & 0xFFu) - (e1 & 0xFu);
                 cnt -= __popc((e1 >> 23) >> min(kBits - last, 31u));
             }
@@ -455,61 +472,73 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             uint32_t sm1 = 0;
             if (edge) sm1 = __ldg(ts.packed_sign_mantissa + es);
 
-            // ---- phase 2: re-decode with T2 (<= 3 exponents per lookup)
-            a = bswap32(r0); bb = bswap32(r1); c = bswap32(r2);
-            shift96(a, bb, c, gap);
-            fill = 96;
-            uint32_t off = gap;
+            // ---- phase 2: re-decode with T2 (<= 3 exponents per lookup), A then B
+            a = W0; bb = W1; c = W2;
+            shift96(a, bb, c, gapA);
             if (!direct) {
                 const uint32_t wp0 = sbase + ebuf_off + (lo - f) + pos0;
                 const uint32_t wend = wp0 + cnt, wend1 = wend - 1, wend2 = wend - 2;
-                uint32_t wp = wp0, e2 = 1, off2 = gap;                         // off2 = off + 32 * (wp - wp0)
+                // A writes [wp0, wpA); it may run past wpA until the next warp check (writing B's
+                // leading codes, then garbage, all inside [wp0, wend) and rewritten by B).
+                const uint32_t wpA = wp0 + min(cntA, cnt);
+                uint32_t wp = wp0, e2 = 1, wlim = wpA;
+                bool inA = true;
                 for (;;) {
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
-                        // finished lanes keep advancing harmlessly: every store is predicated on wp
                         e2 = lds32(madlo(mulhi(a, K_ROW), K_128, t2_lane));
                         sts8_if<0>(wp, e2, wp, wend);
                         sts8_if<1>(wp, mulhi(e2, K_S8), wp, wend1);
                         sts8_if<2>(wp, mulhi(e2, K_S16), wp, wend2);
-                        const uint32_t s = mulhi(e2, K_S24);                   // consumed | count << 5
-                        off2 += s;
                         wp += e2 >> 29;                                        // count (LEA.HI)
-                        shift96(a, bb, c, s);                                  // s & 31 = consumed
+                        shift96(a, bb, c, mulhi(e2, K_S24));                   // (e2 >> 24) & 31 = consumed
                     }
-                    const bool live = wp < wend, esc = live && e2 < (1u << 24);
-                    const uint32_t flags = __reduce_or_sync(FULL, (live ? 1u : 0u) | (esc ? 2u : 0u));
-                    if (!(flags & 1u)) break;
-                    off = off2 - 32u * (wp - wp0);
-                    refill(off);
-                    if (flags & 2u) {
+                    const bool act = wp < wlim;
+                    if (!__any_sync(FULL, act || inA)) break;
+                    const bool esc = act && e2 < (1u << 24);
+                    if (__any_sync(FULL, esc)) {
                         if (esc) {
                             uint32_t len;
                             const uint32_t sym = escape(a, e2 & 0xFFu, len);
                             asm volatile("st.shared.u8 [%0], %1;" ::"r"(wp), "r"(sym) : "memory");
                             wp++;
-                            off += len;
-                            off2 += len + 32u;
                             shift96_long(a, bb, c, len);
-                            if (len > kR + kR2) refill(off);                   // long walked code
                         }
+                    }
+                    if (inA && !act) {                                         // A done: start B
+                        wp = wpA;
+                        wlim = wend;
+                        inA = false;
+                        a = W2; bb = W3; c = W4;
+                        shift96(a, bb, c, gapB);
                     }
                 }
             } else {
                 // direct mode (more than kCap outputs in this tile): compose and store to HBM per code
                 uint32_t p = lo + pos0;
                 const uint32_t pend = min(lo + pos0 + cnt, hi);
-                while (p < pend) {
-                    uint32_t len;
-                    const uint32_t e = lds32(madlo(mulhi(a, K_ROW), K_128, t2_lane));
-                    uint32_t syms, n, consumed;
-                    if (e >= (1u << 24)) { syms = e; n = e >> 29; consumed = (e >> 24) & 15u; }
-                    else { syms = escape(a, e & 0xFFu, len); n = 1; consumed = len; }
-                    for (uint32_t i = 0; i < n && p < pend; i++, p++)
-                        out[p] = compose((syms >> (8 * i)) & 0xFFu, __ldg(ts.packed_sign_mantissa + p));
-                    off += consumed;
-                    shift96_long(a, bb, c, consumed);
-                    refill(off);
+#pragma unroll 1
+                for (int sub = 0; sub < 2; sub++) {
+                    uint32_t off = sub ? 64u + gapB : gapA;
+                    if (sub) { a = W2; bb = W3; c = W4; shift96(a, bb, c, gapB); }
+                    const uint32_t lim_off = sub ? 128u : 64u;
+                    while (p < pend && off < lim_off) {
+                        uint32_t len;
+                        const uint32_t e = lds32(madlo(mulhi(a, K_ROW), K_128, t2_lane));
+                        uint32_t syms, n, consumed;
+                        if (e >= (1u << 24)) { syms = e; n = e >> 29; consumed = (e >> 24) & 15u; }
+                        else { syms = escape(a, e & 0xFFu, len); n = 1; consumed = len; }
+                        // only the codes that start before the sub-stream end belong to it
+                        uint32_t start = off;
+                        for (uint32_t i = 0; i < n && p < pend && start < lim_off; i++, p++) {
+                            out[p] = compose((syms >> (8 * i)) & 0xFFu, __ldg(ts.packed_sign_mantissa + p));
+                            uint32_t l;
+                            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(l) : "r"(sbase + kOffLen + ((syms >> (8 * i)) & 0xFFu)));
+                            start += n == 1 ? consumed : l;
+                        }
+                        off += consumed;
+                        shift96_long(a, bb, c, consumed);
+                    }
                 }
             }
             __syncwarp();
@@ -522,14 +551,10 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 const uint4 sm = it == 0 ? smA : (it == 1 ? smB : __ldg(psm4 + gi));
                 const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - f));
                 uint4 o0, o1;
-                o0.x = compose2<false>(ex.x, sm.x);
-                o0.y = compose2<true>(ex.x, sm.x);
-                o0.z = compose2<false>(ex.y, sm.y);
-                o0.w = compose2<true>(ex.y, sm.y);
-                o1.x = compose2<false>(ex.z, sm.z);
-                o1.y = compose2<true>(ex.z, sm.z);
-                o1.z = compose2<false>(ex.w, sm.w);
-                o1.w = compose2<true>(ex.w, sm.w);
+                compose4(ex.x, sm.x, o0.x, o0.y);
+                compose4(ex.y, sm.y, o0.z, o0.w);
+                compose4(ex.z, sm.z, o1.x, o1.y);
+                compose4(ex.w, sm.w, o1.z, o1.w);
                 uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
                 dst[0] = o0;
                 dst[1] = o1;
