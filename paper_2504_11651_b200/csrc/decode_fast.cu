@@ -390,53 +390,54 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             const uint32_t W0 = bswap32(r0), W1 = bswap32(r1), W2 = bswap32(r2), W3 = bswap32(r3),
                            W4 = bswap32(r4);
 
-            // ---- phase 1: count the codes that start in chunk 2t ("A": bits [gapA, 64)), then in
-            // chunk 2t+1 ("B": bits [64+gapB, 128)).  Each sub-stream fits a 96-bit bit buffer; a lane
-            // switches from A to B at the first warp check after A is done.
-            uint32_t a = W0, bb = W1, c = W2;
-            shift96(a, bb, c, gapA);
-            uint32_t acc = gapA, e1 = 1, lim = 0xC0u, cntA = 0;                // acc = offset | count << 8
+            // ---- phase 1: count the codes that start in chunk 2t ("A": bits [gapA, 64)) and in chunk
+            // 2t+1 ("B": bits [64+gapB, 128)) as two independent chains interleaved step by step
+            // (2x instruction-level parallelism); each fits a 96-bit bit buffer.
+            uint32_t aA = W0, bA = W1, cA = W2, aB = W2, bB = W3, cB = W4;
+            shift96(aA, bA, cA, gapA);
+            shift96(aB, bB, cB, gapB);
+            uint32_t accA = gapA, accB = 64u + gapB, eA1 = 1, eB1 = 1;          // acc = offset | count << 8
             for (;;) {
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    const uint32_t e = lds32(madlo(mulhi(a, K_ROW), K_128, t1_lane));
-                    if ((acc & lim) == 0) {                                    // offset below the sub-stream end
-                        acc += e;
-                        e1 = e;
-                    }
-                    shift96(a, bb, c, e);                                      // e & 31 = consumed bits
+                    const uint32_t eA = lds32(madlo(mulhi(aA, K_ROW), K_128, t1_lane));
+                    const uint32_t eB = lds32(madlo(mulhi(aB, K_ROW), K_128, t1_lane));
+                    if ((accA & 0xC0u) == 0) { accA += eA; eA1 = eA; }         // offset < 64
+                    if ((accB & 0x80u) == 0) { accB += eB; eB1 = eB; }         // offset < 128
+                    shift96(aA, bA, cA, eA);                                   // e & 31 = consumed bits
+                    shift96(aB, bB, cB, eB);
                 }
-                const bool act = (acc & lim) == 0;
-                const bool live = act || lim == 0xC0u;
-                if (!__any_sync(FULL, live)) break;
-                const bool esc = act && (e1 & 0x7FFFFFu) == 0;
-                if (__any_sync(FULL, esc)) {
-                    if (esc) {                                                 // code longer than R bits
+                const bool actA = (accA & 0xC0u) == 0, actB = (accB & 0x80u) == 0;
+                if (!__any_sync(FULL, actA || actB)) break;
+                const bool escA = actA && (eA1 & 0x7FFFFFu) == 0, escB = actB && (eB1 & 0x7FFFFFu) == 0;
+                if (__any_sync(FULL, escA || escB)) {                          // codes longer than R bits
+                    if (escA) {
                         uint32_t len;
-                        escape(a, e1 >> 23, len);
-                        e1 = 0;                                                // exactly one code: no fixup
-                        acc += len + (1u << 8);
-                        shift96_long(a, bb, c, len);
+                        escape(aA, eA1 >> 23, len);
+                        eA1 = 0;                                               // exactly one code: no fixup
+                        accA += len + (1u << 8);
+                        shift96_long(aA, bA, cA, len);
+                    }
+                    if (escB) {
+                        uint32_t len;
+                        escape(aB, eB1 >> 23, len);
+                        eB1 = 0;
+                        accB += len + (1u << 8);
+                        shift96_long(aB, bB, cB, len);
                     }
                 }
-                if (!act && lim == 0xC0u) {                                    // A done: drop codes >= bit 64
-                    if ((e1 & 0x7FFFFFu) != 0) {
-                        const uint32_t last = (acc & 0xFFu) - (e1 & 0xFu);
-                        acc -= (uint32_t)__popc((e1 >> 23) >> min(64u - last, 31u)) << 8;
-                    }
-                    cntA = (acc >> 8) & 0xFFu;
-                    acc = (acc & ~0xFFu) | (64u + gapB);                       // ... and start B
-                    lim = 0x80u;
-                    a = W2; bb = W3; c = W4;
-                    shift96(a, bb, c, gapB);
-                    e1 = 1;
-                }
             }
-            uint32_t cnt = (acc >> 8) & 0xFFu;
-            if ((e1 & 0x7FFFFFu) != 0) {   // B's last T1 group may hold complete codes starting at >= 128
-                const uint32_t last = (acc & 0xFFu) - (e1 & 0xFu);
-                cnt -= __popc((e1 >> 23) >> min(kBits - last, 31u));
+            // each chain's last T1 group may hold complete codes starting past its end: not ours
+            uint32_t cntA = (accA >> 8) & 0xFFu, cntB = (accB >> 8) & 0xFFu;
+            if ((eA1 & 0x7FFFFFu) != 0) {
+                const uint32_t last = (accA & 0xFFu) - (eA1 & 0xFu);
+                cntA -= __popc((eA1 >> 23) >> min(64u - last, 31u));
             }
+            if ((eB1 & 0x7FFFFFu) != 0) {
+                const uint32_t last = (accB & 0xFFu) - (eB1 & 0xFu);
+                cntB -= __popc((eB1 >> 23) >> min(kBits - last, 31u));
+            }
+            const uint32_t cnt = cntA + cntB;
 
             // ---- exclusive scan of the counts over the tile: warp shuffles + 4 warp totals
             uint32_t incl = cnt;
@@ -472,49 +473,55 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             uint32_t sm1 = 0;
             if (edge) sm1 = __ldg(ts.packed_sign_mantissa + es);
 
-            // ---- phase 2: re-decode with T2 (<= 3 exponents per lookup), A then B
-            a = W0; bb = W1; c = W2;
-            shift96(a, bb, c, gapA);
+            // ---- phase 2: re-decode with T2 (<= 3 exponents per lookup), chains A and B interleaved
             if (!direct) {
                 const uint32_t wp0 = sbase + ebuf_off + (lo - f) + pos0;
-                const uint32_t wend = wp0 + cnt, wend1 = wend - 1, wend2 = wend - 2;
-                // A writes [wp0, wpA); it may run past wpA until the next warp check (writing B's
-                // leading codes, then garbage, all inside [wp0, wend) and rewritten by B).
-                const uint32_t wpA = wp0 + min(cntA, cnt);
-                uint32_t wp = wp0, e2 = 1, wlim = wpA;
-                bool inA = true;
+                // A writes [wp0, wpAe), B writes [wpAe, wend); stores are predicated on the chain's end
+                const uint32_t wpAe = wp0 + cntA, wend = wpAe + cntB;
+                aA = W0; bA = W1; cA = W2; aB = W2; bB = W3; cB = W4;
+                shift96(aA, bA, cA, gapA);
+                shift96(aB, bB, cB, gapB);
+                uint32_t wA = wp0, wB = wpAe, eA2 = 1, eB2 = 1;
                 for (;;) {
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
-                        e2 = lds32(madlo(mulhi(a, K_ROW), K_128, t2_lane));
-                        sts8_if<0>(wp, e2, wp, wend);
-                        sts8_if<1>(wp, mulhi(e2, K_S8), wp, wend1);
-                        sts8_if<2>(wp, mulhi(e2, K_S16), wp, wend2);
-                        wp += e2 >> 29;                                        // count (LEA.HI)
-                        shift96(a, bb, c, mulhi(e2, K_S24));                   // (e2 >> 24) & 31 = consumed
+                        eA2 = lds32(madlo(mulhi(aA, K_ROW), K_128, t2_lane));
+                        eB2 = lds32(madlo(mulhi(aB, K_ROW), K_128, t2_lane));
+                        sts8_if<0>(wA, eA2, wA, wpAe);
+                        sts8_if<1>(wA, mulhi(eA2, K_S8), wA, wpAe - 1);
+                        sts8_if<2>(wA, mulhi(eA2, K_S16), wA, wpAe - 2);
+                        sts8_if<0>(wB, eB2, wB, wend);
+                        sts8_if<1>(wB, mulhi(eB2, K_S8), wB, wend - 1);
+                        sts8_if<2>(wB, mulhi(eB2, K_S16), wB, wend - 2);
+                        wA += eA2 >> 29;                                       // count (LEA.HI)
+                        wB += eB2 >> 29;
+                        shift96(aA, bA, cA, mulhi(eA2, K_S24));                // (e >> 24) & 31 = consumed
+                        shift96(aB, bB, cB, mulhi(eB2, K_S24));
                     }
-                    const bool act = wp < wlim;
-                    if (!__any_sync(FULL, act || inA)) break;
-                    const bool esc = act && e2 < (1u << 24);
-                    if (__any_sync(FULL, esc)) {
-                        if (esc) {
+                    const bool actA = wA < wpAe, actB = wB < wend;
+                    if (!__any_sync(FULL, actA || actB)) break;
+                    const bool escA = actA && eA2 < (1u << 24), escB = actB && eB2 < (1u << 24);
+                    if (__any_sync(FULL, escA || escB)) {
+                        if (escA) {
                             uint32_t len;
-                            const uint32_t sym = escape(a, e2 & 0xFFu, len);
-                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(wp), "r"(sym) : "memory");
-                            wp++;
-                            shift96_long(a, bb, c, len);
+                            const uint32_t sym = escape(aA, eA2 & 0xFFu, len);
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(wA), "r"(sym) : "memory");
+                            wA++;
+                            shift96_long(aA, bA, cA, len);
                         }
-                    }
-                    if (inA && !act) {                                         // A done: start B
-                        wp = wpA;
-                        wlim = wend;
-                        inA = false;
-                        a = W2; bb = W3; c = W4;
-                        shift96(a, bb, c, gapB);
+                        if (escB) {
+                            uint32_t len;
+                            const uint32_t sym = escape(aB, eB2 & 0xFFu, len);
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(wB), "r"(sym) : "memory");
+                            wB++;
+                            shift96_long(aB, bB, cB, len);
+                        }
                     }
                 }
             } else {
                 // direct mode (more than kCap outputs in this tile): compose and store to HBM per code
+                uint32_t a = W0, bb = W1, c = W2;
+                shift96(a, bb, c, gapA);
                 uint32_t p = lo + pos0;
                 const uint32_t pend = min(lo + pos0 + cnt, hi);
 #pragma unroll 1
