@@ -41,6 +41,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-transfer", action="store_true", help="skip the CPU->GPU transfer baseline (NEXT-2)")
+    p.add_argument("--unique-blocks", type=int, default=2,
+                   help="model configs: distinct encoded blocks per rank (device copies fill the shard)")
     return p.parse_args()
 
 
@@ -195,6 +198,12 @@ def main():
         if world > 1:
             dist.barrier()
 
+    if args.config in workloads.MODELS:
+        run_model(args, df11, dev, rank, world, local, barrier)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
     # ---- this rank's shard: one transformer block (seeded by rank -> distinct weights per GPU)
     tensors = workloads.config_tensors(args.config, layer=rank)
     hs = [df11.encode(w) for _, w in tensors]
@@ -265,6 +274,11 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(df11, hs, dts, dev, args.e2e_steps, world, barrier, tensors)
 
+    # ---- NEXT-2: CPU->GPU transfer of the same BF16 bytes (the paper's comparator)
+    transfer = None
+    if not args.no_transfer:
+        transfer = run_transfer(tensors, dev, world, barrier, value)
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
@@ -287,6 +301,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "transfer_baseline": transfer,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "per_gpu_gbs": value / world,
@@ -294,6 +309,177 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_transfer(tensors, dev, world, barrier, decode_gbs):
+    """Pinned host -> device copy of the block's BF16 weights (what DF11 decode replaces when weights
+    are offloaded to CPU memory).  Returns GB/s of BF16 delivered and the decode/transfer ratio."""
+    import torch
+    import torch.distributed as dist
+    host = [torch.from_numpy(w.reshape(-1).view(np.int16)).pin_memory() for _, w in tensors]
+    dst = [torch.empty_like(h, device=dev) for h in host]
+    stream = torch.cuda.current_stream()
+    for h, d in zip(host, dst):
+        d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    a.record(stream)
+    for _ in range(reps):
+        for h, d in zip(host, dst):
+            d.copy_(h, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    nbytes = sum(h.numel() * 2 for h in host)
+    gbs = world * nbytes * reps / (float(ms[0]) / 1e3) / 1e9
+    return {"h2d_gbs": gbs, "unit": UNIT, "decode_over_transfer": decode_gbs / gbs,
+            "what": "pinned H2D of the block's BF16 weights vs DF11 decode of the same weights on the GPU"}
+
+
+def run_model(args, df11, dev, rank, world, local, barrier):
+    """Whole-model sweeps (BASELINE configs[2] and [4]): the model's transformer blocks (+ embedding,
+    LM head) are placed on ranks by plan_shards; a step decodes every block of this rank's shard, one
+    df11_decompress_block launch per block into a reused BF16 scratch.
+
+    llama70b_model: the full 80-block model split over the N ranks (strong scaling).
+    llama405b_model: the 8-GPU shard set; rank r decodes shard r of 8 whatever N is (weak scaling).
+    Weights: `--unique-blocks` distinct blocks per rank are generated (torch Philox on the GPU), host-
+    encoded and verified; the rest of the shard are device copies of them (same sizes and entropy)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_11651_b200.shard import plan_shards
+    m = workloads.MODELS[args.config]
+    block_cfg = m["block"]
+    shapes = workloads.CONFIGS[block_cfg]
+    block_elems = sum(int(np.prod(sh)) for _, sh in shapes)
+    head_elems = m["vocab"] * m["hidden"]
+    units = [head_elems] + [block_elems] * m["blocks"] + [head_elems]      # embed, blocks..., lm_head
+    if args.config == "llama405b_model":
+        shard_world, shard_id, scaling = 8, rank % 8, "weak"
+    else:
+        shard_world, shard_id, scaling = world, rank, "strong"
+    mine = list(plan_shards(units, shard_world)[shard_id])
+    t0 = time.perf_counter()
+    # unique encoded units of this rank: up to U blocks + the head/embedding if present
+    kinds = []
+    for u in mine:
+        kinds.append("embed" if u == 0 else ("head" if u == len(units) - 1 else "block"))
+    uniq_blocks = min(args.unique_blocks, kinds.count("block"))
+
+    def encode_unit(kind, idx):
+        if kind == "block":
+            ts = [(name, workloads.gaussian_bf16_torch(sh, workloads.seed_for(block_cfg, idx, name), dev))
+                  for name, sh in shapes]
+        else:
+            ts = [(kind, workloads.gaussian_bf16_torch((m["vocab"], m["hidden"]),
+                                                        workloads.seed_for(args.config, idx, kind), dev))]
+        hs = [df11.encode(w) for _, w in ts]
+        dts = [df11.to_device(h, dev) for h in hs]
+        return ts, hs, dts
+
+    protos = []           # (kind, [DeviceTensor]) verified prototypes
+    maxN = 0
+    verified = 0
+    for i in range(uniq_blocks):
+        ts, hs, dts = encode_unit("block", mine[kinds.index("block")] + i)
+        protos.append(("block", ts, dts))
+    for kind in ("embed", "head"):
+        if kind in kinds:
+            ts, hs, dts = encode_unit(kind, mine[kinds.index(kind)])
+            protos.append((kind, ts, dts))
+    for _, ts, dts in protos:
+        maxN = max(maxN, sum(dt.num_elements + 8 for dt in dts))
+    scratch = torch.empty(maxN + 64, dtype=torch.bfloat16, device=dev)
+
+    def views(dts):
+        outs, o = [], 0
+        for dt in dts:
+            outs.append(scratch[o:o + dt.num_elements])
+            o += (dt.num_elements + 7) // 8 * 8
+        return outs
+
+    # verify every prototype bit-exactly, then build the per-unit plans (device copies for the rest)
+    for kind, ts, dts in protos:
+        plan = df11.BlockPlan(dts, views(dts))
+        plan.run()
+        torch.cuda.synchronize()
+        for (name, w), out in zip(ts, plan.outputs()):
+            ref = torch.from_numpy(w.reshape(-1).view(np.int16)).to(dev)
+            if not torch.equal(out.reshape(-1).view(torch.int16), ref):
+                raise SystemExit(f"bit-exact check failed on {kind}/{name}")
+            verified += w.size
+    block_protos = [dts for kind, _, dts in protos if kind == "block"]
+    plans, keep = [], []
+    nb = 0
+    bf16_bytes = algo = 0
+    for kind in kinds:
+        if kind == "block":
+            src = block_protos[nb % len(block_protos)]
+            if nb < len(block_protos):
+                dts = src
+            else:                                   # device copy of a verified prototype
+                dts = []
+                for d in src:
+                    c = df11.DeviceTensor.__new__(df11.DeviceTensor)
+                    c.__dict__.update(d.__dict__)
+                    for key in ("encoded_exponent", "packed_sign_mantissa", "gaps", "luts", "code_lengths",
+                                "block_output_pos"):
+                        setattr(c, key, getattr(d, key).clone())
+                    dts.append(c)
+                keep.append(dts)
+            nb += 1
+        else:
+            dts = [d for k, _, dd in protos if k == kind for d in dd]
+        plans.append(df11.BlockPlan(dts, views(dts)))
+        bf16_bytes += sum(2 * d.num_elements for d in dts)
+        algo += sum(d.compressed_bytes + 2 * d.num_elements for d in dts)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for p in plans:
+            p.run(stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    df11.launch_count(reset=True)
+    with ClockSampler(local) as clocks:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            for p in plans:
+                p.run(stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+    launches = df11.launch_count()
+    barrier()
+    from paper_2504_11651_b200.shard import max_over_ranks, sum_over_ranks
+    ms = max_over_ranks([a.elapsed_time(b)], dev)[0]
+    tot_bf16, tot_algo = sum_over_ranks([bf16_bytes, algo], dev)
+    value = tot_bf16 * args.steps / (ms / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    achieved = algo * args.steps / (a.elapsed_time(b) / 1e3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": args.config, "units_this_rank": len(mine), "blocks_this_rank": kinds.count("block"),
+                       "unique_blocks_encoded": uniq_blocks, "bf16_bytes_all_ranks_per_step": tot_bf16,
+                       "df11_bytes_all_ranks_per_step": tot_algo - tot_bf16,
+                       "parallelism": f"{'shard8' if scaling == 'weak' else 'shard' + str(world)} "
+                                      "(contiguous blocks per GPU, no collective)",
+                       "setup_s": round(setup_s, 1), "verified_elements_rank0": verified,
+                       "l2": "inputs larger than L2 (GB per step)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "note": "rank-0 achieved = (DF11 read + BF16 written) / rank-0 step time; one launch per unit"},
+            "gpu_launches": launches, "clocks": clocks.summary(), "per_gpu_gbs": value / world,
+        }), flush=True)
 
 
 def run_e2e(df11, hs, dts, dev, steps, world, barrier, tensors):

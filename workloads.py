@@ -82,6 +82,22 @@ def gaussian_bf16(shape, seed: int, sigma: float = SIGMA) -> np.ndarray:
     return f32_to_bf16_bits(x).reshape(shape)
 
 
+def gaussian_bf16_torch(shape, seed: int, device, sigma: float = SIGMA):
+    """BF16(N(0, sigma^2)) generated on `device` with torch's Philox (fast, for the multi-GB model
+    configs); returned as a host uint16 array (the host encoder's input)."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(int(seed))
+    w = (torch.randn(tuple(shape), generator=g, device=device, dtype=torch.float32) * sigma).to(torch.bfloat16)
+    return w.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+# Whole-model sweeps: units = transformer blocks (+ embedding first, LM head last).
+MODELS = {
+    "llama70b_model": dict(block="llama70b_block", blocks=80, vocab=128256, hidden=8192),
+    "llama405b_model": dict(block="llama405b_block", blocks=126, vocab=128256, hidden=16384),
+}
+
+
 def config_tensors(config: str, layer: int = 0, base_seed: int = 0, sigma: float = SIGMA):
     """[(name, uint16 array)] for one unit of `config`."""
     return [(name, gaussian_bf16(shape, seed_for(config, layer, name, base_seed), sigma))
