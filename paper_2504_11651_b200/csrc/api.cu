@@ -5,6 +5,7 @@
 // format parameters the fast kernel does not specialise go through the literal Algorithm 1 kernel
 // (decode_alg1.cu), one launch per distinct T.
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -15,6 +16,7 @@ namespace df11 {
 cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_fast(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 bool fast_supports(const df11_device_tensor &t);
+uint32_t fast_grid(uint32_t total_tiles, int num_sms);
 }  // namespace df11
 
 namespace {
@@ -103,17 +105,46 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
     static thread_local df11::Batch bt;   // ~6 KB: keep it off the stack
     bool use_fast = all_fast && kernel != DF11_KERNEL_ALG1;
     if (use_fast) {
+        // Tile schedule (the block-batched launcher).  CTA c of the persistent kernel walks the
+        // contiguous global tile range [c*total/G, (c+1)*total/G) and rebuilds its SMEM decode tables at
+        // every tensor boundary inside it.  Small tensors (biases, norm scales) would pile up in a few
+        // CTAs and turn them into stragglers, so each small tensor is placed exactly at a CTA range
+        // boundary (big tensors are split there), spreading them over distinct CTAs.
         std::memset(&bt, 0, sizeof(bt));
-        uint32_t acc = 0;
+        constexpr uint32_t kSmall = 16;                     // tiles
+        uint32_t big[DF11_MAX_BATCH], small[DF11_MAX_BATCH], nbig = 0, nsmall = 0, total = 0;
         for (uint32_t i = 0; i < count; i++) {
             if (!ts[i].num_elements) continue;
-            bt.t[bt.count] = ts[i];
-            bt.tile_start[bt.count] = acc;
-            acc += ts[i].B;
-            bt.count++;
+            (ts[i].B < kSmall ? small[nsmall++] : big[nbig++]) = i;
+            total += ts[i].B;
         }
-        bt.tile_start[bt.count] = acc;
-        bt.total_tiles = acc;
+        const uint32_t G = df11::fast_grid(total, num_sms);
+        auto boundary = [&](uint32_t c) { return (uint32_t)(((uint64_t)total * c) / G); };
+        uint32_t pos = 0, bi = 0, boff = 0;
+        auto push = [&](uint32_t ti, uint32_t off, uint32_t n) {
+            bt.t[bt.count] = ts[ti];
+            bt.tile_start[bt.count] = pos;
+            bt.tile_off[bt.count] = off;
+            bt.count++;
+            pos += n;
+        };
+        auto fill_big_until = [&](uint32_t target) {
+            while (pos < target && bi < nbig) {
+                const uint32_t left = ts[big[bi]].B - boff, take = std::min(left, target - pos);
+                push(big[bi], boff, take);
+                boff += take;
+                if (boff == ts[big[bi]].B) { bi++; boff = 0; }
+            }
+        };
+        for (uint32_t k = 0; k < nsmall; k++) {
+            const uint32_t c = (uint32_t)(((uint64_t)(2 * k + 1) * G) / (2 * nsmall));
+            fill_big_until(boundary(c));
+            push(small[k], 0, ts[small[k]].B);
+        }
+        fill_big_until(total);
+        bt.tile_start[bt.count] = pos;
+        bt.total_tiles = pos;
+        bt.grid = G;
         const uint32_t kpow[8] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u, 1u};
         std::memcpy(bt.kpow, kpow, sizeof(kpow));
         e = df11::launch_fast(bt, dev, stream, &g_launches);

@@ -10,11 +10,15 @@ namespace df11 {
 // One launch decodes up to DF11_MAX_BATCH tensors ("decompress all DFloat11 weight matrices
 // within a transformer block as a single batch").  Passed by value as a __grid_constant__ kernel
 // parameter: no workspace, no H2D copy, graph-capturable.
+constexpr int kMaxEntries = 2 * DF11_MAX_BATCH;   // a tensor may be split into several tile ranges
+
 struct Batch {
-    df11_device_tensor t[DF11_MAX_BATCH];
-    uint32_t tile_start[DF11_MAX_BATCH + 1];   // exclusive prefix of format blocks B over the batch
+    df11_device_tensor t[kMaxEntries];
+    uint32_t tile_start[kMaxEntries + 1];      // exclusive prefix of the entries' tile counts
+    uint32_t tile_off[kMaxEntries];            // first format block of entry i within its tensor
     uint32_t count;
     uint32_t total_tiles;
+    uint32_t grid;                             // CTAs the launcher will use (fast kernel)
     // powers of two used as IMAD multipliers (field extraction on the FMA pipe); read from the
     // constant bank so the compiler cannot strength-reduce them into ALU shifts (set by the launcher)
     uint32_t kpow[8];

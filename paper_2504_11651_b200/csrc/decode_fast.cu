@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
     for (uint32_t seg_begin = c_begin; seg_begin < c_end; ti_idx++) {
         const df11_device_tensor &ts = bt.t[ti_idx];
         const uint32_t seg_end = min(c_end, bt.tile_start[ti_idx + 1]);
-        const uint32_t base_tile = bt.tile_start[ti_idx];
+        const uint32_t base_tile = bt.tile_start[ti_idx] - bt.tile_off[ti_idx];   // b = tile - base_tile
         if (seg_end <= seg_begin) continue;
 
         // =============================== derived tables for this tensor (CTA-wide)
@@ -578,6 +578,10 @@ int g_attr_set[64];
 
 }  // namespace
 
+uint32_t fast_grid(uint32_t total_tiles, int num_sms) {
+    return min((uint32_t)num_sms, (total_tiles + kGroups - 1) / kGroups);
+}
+
 bool fast_supports(const df11_device_tensor &t) {
     return t.T == kT && t.n == kN &&
            (reinterpret_cast<uintptr_t>(t.encoded_exponent) & 15) == 0 &&
@@ -596,8 +600,7 @@ cudaError_t launch_fast(const Batch &bt, int device, cudaStream_t stream, uint64
         if (e != cudaSuccess) return e;
         g_attr_set[device] = 1;
     }
-    const uint32_t want = (bt.total_tiles + kGroups - 1) / kGroups;
-    const uint32_t grid = min((uint32_t)num_sms, want);
+    const uint32_t grid = bt.grid ? bt.grid : min((uint32_t)num_sms, (bt.total_tiles + kGroups - 1) / kGroups);
     fast_kernel<<<grid, kCta, kSmemBytes, stream>>>(bt);
     if (launches) (*launches)++;
     return cudaGetLastError();
