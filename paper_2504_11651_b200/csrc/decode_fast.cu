@@ -154,6 +154,11 @@ __device__ __forceinline__ void tma_g2s(uint32_t dst, const void *src, uint32_t 
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+// Prefetch [src, src + bytes) into L2 (one TMA instruction, no registers, no SMEM).
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Stage format block b of tensor ts (EncodedExponent chunk + spill, and its gaps) into `stage`.
 __device__ __forceinline__ void issue_tile(const df11_device_tensor &ts, uint32_t b, uint32_t stage, uint32_t bar) {
     mbar_expect_tx(bar, kChunkBytes + kGapBytes);
@@ -357,6 +362,12 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             nlo = __ldg(ts.block_output_pos + tile - base_tile);
             nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
         }
+        // sign/mantissa bytes of a tile -> L2 ahead of its merge (clipped, 16-byte granular)
+        auto prefetch_sm = [&](uint32_t plo, uint32_t phi) {
+            const uint32_t a0 = min(plo, N) & ~15u, a1 = (min(max(phi, plo), N) + 15u) & ~15u;
+            if (a1 > a0) prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
+        };
+        if (t == 0 && tile < seg_end) prefetch_sm(nlo, nhi);
         for (; tile < seg_end; tile += kGroups, q++) {
             const uint32_t b = tile - base_tile;
             const uint32_t clo = nlo, chi = nhi;
@@ -450,7 +461,10 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             if (lane == 31) ws[wig] = incl;
             group_bar(g);                          // also: every thread has read this tile's stage
             parity ^= 1u;
-            if (t == 0 && has_next) issue_tile(ts, b + kGroups, stage, mbar);
+            if (t == 0 && has_next) {
+                issue_tile(ts, b + kGroups, stage, mbar);
+                prefetch_sm(nlo, nhi);                                         // next tile's sign/mantissa
+            }
             uint32_t wpre = 0;
             {
                 const uint4 v = *reinterpret_cast<const uint4 *>(ws);
