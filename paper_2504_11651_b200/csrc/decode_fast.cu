@@ -116,7 +116,10 @@ __device__ __forceinline__ void shift96(uint32_t &a, uint32_t &b, uint32_t &c, u
 }
 // Shift by 0..63 bits (escape path).
 __device__ __forceinline__ void shift96_long(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
-    if (s >= 32) { a = b; b = c; c = 0; s -= 32; }
+    const bool w = s >= 32;                                   // select, then funnel by s & 31
+    a = w ? b : a;
+    b = w ? c : b;
+    c = w ? 0u : c;
     shift96(a, b, c, s);
 }
 // PTX shifts clamp the shift amount: any amount >= 32 (incl. "negative" unsigned) yields 0.
@@ -349,6 +352,19 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             }
             return walk(a_, len);
         };
+        // packed form for the hot loops: sym | len << 8 (second-level table; the walk only on a miss)
+        auto escape_packed = [&](uint32_t a_, uint32_t id) -> uint32_t {
+            uint32_t v = 0;
+            if (id != 0)
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v)
+                             : "r"(sbase + kOffL2 + (((id - 1) << kR2) + ((a_ >> (32 - kR - kR2)) & ((1u << kR2) - 1u))) * 2));
+            if ((v >> 8) == 0) {                                       // rare: code longer than kR + kR2
+                uint32_t len;
+                const uint32_t sym = walk(a_, len);
+                v = sym | (len << 8);
+            }
+            return v;
+        };
         const uint32_t N = (uint32_t)ts.num_elements;
         const bool vec_out = ((reinterpret_cast<uintptr_t>(ts.out) & 15) == 0);
         const uint4 *__restrict__ psm4 = reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa);
@@ -422,19 +438,17 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 if (!__any_sync(FULL, actA || actB)) break;
                 const bool escA = actA && (eA1 & 0x7FFFFFu) == 0, escB = actB && (eB1 & 0x7FFFFFu) == 0;
                 if (__any_sync(FULL, escA || escB)) {                          // codes longer than R bits
+                    const uint32_t vA = escA ? escape_packed(aA, eA1 >> 23) : 0u;
+                    const uint32_t vB = escB ? escape_packed(aB, eB1 >> 23) : 0u;
                     if (escA) {
-                        uint32_t len;
-                        escape(aA, eA1 >> 23, len);
                         eA1 = 0;                                               // exactly one code: no fixup
-                        accA += len + (1u << 8);
-                        shift96_long(aA, bA, cA, len);
+                        accA += (vA >> 8) + (1u << 8);
+                        shift96_long(aA, bA, cA, vA >> 8);
                     }
                     if (escB) {
-                        uint32_t len;
-                        escape(aB, eB1 >> 23, len);
                         eB1 = 0;
-                        accB += len + (1u << 8);
-                        shift96_long(aB, bB, cB, len);
+                        accB += (vB >> 8) + (1u << 8);
+                        shift96_long(aB, bB, cB, vB >> 8);
                     }
                 }
             }
@@ -516,19 +530,17 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                     if (!__any_sync(FULL, actA || actB)) break;
                     const bool escA = actA && eA2 < (1u << 24), escB = actB && eB2 < (1u << 24);
                     if (__any_sync(FULL, escA || escB)) {
+                        const uint32_t vA = escA ? escape_packed(aA, eA2 & 0xFFu) : 0u;
+                        const uint32_t vB = escB ? escape_packed(aB, eB2 & 0xFFu) : 0u;
                         if (escA) {
-                            uint32_t len;
-                            const uint32_t sym = escape(aA, eA2 & 0xFFu, len);
-                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(wA), "r"(sym) : "memory");
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(wA), "r"(vA) : "memory");
                             wA++;
-                            shift96_long(aA, bA, cA, len);
+                            shift96_long(aA, bA, cA, vA >> 8);
                         }
                         if (escB) {
-                            uint32_t len;
-                            const uint32_t sym = escape(aB, eB2 & 0xFFu, len);
-                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(wB), "r"(sym) : "memory");
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(wB), "r"(vB) : "memory");
                             wB++;
-                            shift96_long(aB, bB, cB, len);
+                            shift96_long(aB, bB, cB, vB >> 8);
                         }
                     }
                 }
