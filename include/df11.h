@@ -119,6 +119,62 @@ df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t coun
 df11_status df11_decompress_host(const df11_host_tensor *h, const df11_device_tensor *d,
                                  uint16_t *host_out, void *stream);
 
+/* ---- device encoder (format P:97; Table `time` P:471-486) -------
+ * The same bytes as df11_encode, produced on the GPU in three steps so that the caller owns every
+ * device allocation:
+ *   1. df11_histogram_device   exponent histogram of a device BF16 tensor (one launch; accumulates).
+ *   2. df11_encode_plan_create codebook (Huffman, 32-bit cap, canonical codes, LUTs) and buffer sizes,
+ *                              on the host, from the histogram(s) copied back by the caller.
+ *   3. df11_encode_device      bit packing, PackedSignMantissa, Gaps and BlockOutputPos on the GPU
+ *                              (single pass with a decoupled look-back scan of per-segment bit counts).
+ * The output is byte-identical to df11_encode with the same options and histogram. */
+
+/* Device buffers written by df11_encode_device; sizes are the plan's *_bytes fields.  All pointers
+ * are caller-owned device pointers, 16-byte aligned. */
+typedef struct {
+    uint8_t  *encoded_exponent;       /* plan.encoded_exponent_bytes */
+    uint8_t  *packed_sign_mantissa;   /* plan.packed_sign_mantissa_bytes */
+    uint8_t  *gaps;                   /* plan.gaps_bytes */
+    uint8_t  *luts;                   /* plan.luts_bytes (>= 1) */
+    uint8_t  *code_lengths;           /* 256 */
+    uint32_t *block_output_pos;       /* plan.B + 1 entries */
+} df11_device_buffers;
+
+/* Codebook + geometry of one tensor, built on the host.  `luts` is library-owned host memory: free
+ * the plan with df11_encode_plan_free. */
+typedef struct {
+    uint64_t num_elements;            /* N = sum of tensor_hist */
+    uint64_t encoded_bits;            /* sum over the tensor of code lengths */
+    uint32_t T, n, B, k, lut_entry_bytes, max_code_len;
+    uint8_t  code_lengths[256];
+    uint32_t codes[256];              /* canonical codes, right-aligned, MSB-first when emitted */
+    uint8_t  *luts;             uint64_t luts_bytes;
+    uint64_t encoded_exponent_bytes, packed_sign_mantissa_bytes, gaps_bytes;
+    uint64_t workspace_bytes;         /* device scratch df11_encode_device needs */
+} df11_encode_plan;
+
+/* Adds the exponent histogram of d_bf16[0..n) to d_hist (256 uint64 counters in device memory;
+ * zero them first).  d_bf16 must be 2-byte aligned.  Enqueues on `stream`; does not synchronise. */
+df11_status df11_histogram_device(const uint16_t *d_bf16, uint64_t n, uint64_t *d_hist, void *stream);
+
+/* codebook_hist: host histogram the codebook is built from (the tensor's own, or the sum over a
+ * group for a shared codebook, R5).  tensor_hist: the tensor's own host histogram (NULL = same as
+ * codebook_hist); it fixes N and the encoded size.  Errors: every exponent in tensor_hist must have a
+ * code (DF11_E_INVALID_ARGUMENT), RESERVED_EXPONENT / LUT_OVERFLOW with NARROW, TOO_LARGE (N >= 2^32).
+ * On error *plan is zeroed. */
+df11_status df11_encode_plan_create(const uint64_t *codebook_hist, const uint64_t *tensor_hist,
+                                    const df11_encode_opts *opts, df11_encode_plan *plan);
+void df11_encode_plan_free(df11_encode_plan *plan);
+
+/* Encodes d_bf16[0..plan->num_elements) into `dst` on `stream` (memsets + kernels only; CodeLengths
+ * and LUTs travel as kernel parameters, so the call never waits for the stream).  d_bf16 must hold exactly the tensor the plan's tensor_hist was
+ * taken from; a mismatch yields a wrong encoding but no out-of-bounds access (the bit packer clips
+ * to the planned sizes).  `workspace`: >= plan->workspace_bytes of device memory, 16-byte aligned.
+ * Returns after enqueueing. */
+df11_status df11_encode_device(const uint16_t *d_bf16, const df11_encode_plan *plan,
+                               const df11_device_buffers *dst, void *workspace, uint64_t workspace_bytes,
+                               void *stream);
+
 /* ---- diagnostics ------------------------------------------------------------------------------ */
 const char *df11_status_string(df11_status s);
 int         df11_last_cuda_error(void);            /* cudaError_t of the last failing CUDA call */

@@ -114,8 +114,10 @@ class FormatError(ValueError):
         self.kind = kind
 
 
-def encode(w: np.ndarray, T: int = 256, n: int = 8, lut_mode: str = "auto") -> dict:
-    """E1..E8 for one tensor (codebook scope = the tensor, R5)."""
+def encode(w: np.ndarray, T: int = 256, n: int = 8, lut_mode: str = "auto", codebook_hist=None) -> dict:
+    """E1..E8 for one tensor.  Codebook scope (R5): the tensor's own histogram, or `codebook_hist`
+    (e.g. the summed histogram of a group sharing "a Huffman tree based on the distribution of
+    exponents in model weights"); it must give every exponent of `w` a code."""
     w = np.ascontiguousarray(w, dtype=np.uint16).reshape(-1)
     N = int(w.size)
     if N >= 1 << 32:
@@ -123,7 +125,10 @@ def encode(w: np.ndarray, T: int = 256, n: int = 8, lut_mode: str = "auto") -> d
     lib = _load()
     exp, psm = split(w)
     hist = histogram(exp)
-    lengths = huffman.code_lengths([int(h) for h in hist])
+    cb_hist = hist if codebook_hist is None else np.asarray(codebook_hist)
+    lengths = huffman.code_lengths([int(h) for h in cb_hist])
+    if any(int(hist[s]) and not lengths[s] for s in range(256)):
+        raise FormatError("invalid_argument", "codebook_hist gives an exponent of w no code")
     codes = huffman.canonical_codes(lengths)
     L = max(lengths)
     if L > 8 * n:

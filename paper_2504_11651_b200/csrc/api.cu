@@ -226,6 +226,8 @@ extern "C" const char *df11_status_string(df11_status s) {
     return "DF11_E_UNKNOWN";
 }
 
+extern "C" df11_status df11_cuda_fail(int e, const char *what) { return cuda_fail((cudaError_t)e, what); }
+extern "C" void df11_count_launches(uint64_t k) { g_launches += k; }
 extern "C" int df11_last_cuda_error(void) { return g_cuda_err; }
 extern "C" const char *df11_last_error_message(void) { return g_msg; }
 extern "C" const char *df11_version(void) { return "df11-b200 0.1 (sm_100a)"; }

@@ -489,3 +489,62 @@ extern "C" void df11_host_tensor_free(df11_host_tensor *t) {
     std::free(t->block_output_pos);
     std::memset(t, 0, sizeof(*t));
 }
+
+// ------------------------------------------------------------------------------------ device-encoder plan
+// Host half of the GPU encoder (NEXT-3): the codebook is tiny (256 symbols), so it is built here with
+// the same code as df11_encode; df11_encode_device (encode_gpu.cu) does the per-element work.
+extern "C" df11_status df11_encode_plan_create(const uint64_t *codebook_hist, const uint64_t *tensor_hist,
+                                               const df11_encode_opts *opts, df11_encode_plan *plan) {
+    if (!plan) return df11_fail(DF11_E_INVALID_ARGUMENT, "plan is NULL");
+    std::memset(plan, 0, sizeof(*plan));
+    if (!codebook_hist) return df11_fail(DF11_E_INVALID_ARGUMENT, "codebook_hist is NULL");
+    if (!tensor_hist) tensor_hist = codebook_hist;
+    df11_encode_opts o;
+    df11_status st = check_opts(opts, o);
+    if (st != DF11_OK) return st;
+    try {
+        Codebook cb;
+        st = make_codebook(codebook_hist, (int)o.lut_mode, cb);
+        if (st != DF11_OK) return df11_fail(st, st == DF11_E_RESERVED_EXPONENT ? "exponent >= 240 with NARROW LUTs"
+                                                                          : "more than 16 child LUTs with NARROW LUTs");
+        uint64_t n = 0, bits = 0;
+        for (int s = 0; s < 256; s++) {
+            if (tensor_hist[s] && !cb.len[s])
+                return df11_fail(DF11_E_INVALID_ARGUMENT, "tensor_hist has an exponent the codebook does not code");
+            n += tensor_hist[s];
+            bits += tensor_hist[s] * cb.len[s];
+        }
+        if (n >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "N >= 2^32 (BlockOutputPos is uint32)");
+        const uint64_t block_bits = 8ull * o.bytes_per_thread * o.threads_per_block;
+        const uint64_t B = (bits + block_bits - 1) / block_bits;
+        plan->luts = (uint8_t *)std::calloc(std::max<size_t>(cb.luts.size(), 1), 1);
+        if (!plan->luts) return df11_fail(DF11_E_ALLOC, "host allocation failed");
+        if (!cb.luts.empty()) std::memcpy(plan->luts, cb.luts.data(), cb.luts.size());
+        plan->luts_bytes = cb.luts.size();
+        plan->num_elements = n;
+        plan->encoded_bits = bits;
+        plan->T = o.threads_per_block;
+        plan->n = o.bytes_per_thread;
+        plan->B = (uint32_t)B;
+        plan->k = cb.k;
+        plan->lut_entry_bytes = cb.entry_bytes;
+        plan->max_code_len = cb.max_len;
+        std::memcpy(plan->code_lengths, cb.len, 256);
+        std::memcpy(plan->codes, cb.code, sizeof(plan->codes));
+        plan->encoded_exponent_bytes = B * o.threads_per_block * o.bytes_per_thread + 16;
+        plan->packed_sign_mantissa_bytes = roundup(n, 16) + 16;
+        plan->gaps_bytes = roundup((5ull * B * o.threads_per_block + 7) / 8, 16) + 16;
+        // workspace: one gap byte per format thread | one look-back word per pack segment | ticket
+        const uint64_t segments = (n + DF11_ENCODE_SEGMENT - 1) / DF11_ENCODE_SEGMENT;
+        plan->workspace_bytes = roundup(B * o.threads_per_block, 16) + 8 * roundup(segments, 2) + 16;
+        return DF11_OK;
+    } catch (const std::bad_alloc &) {
+        return df11_fail(DF11_E_ALLOC, "host allocation failed");
+    }
+}
+
+extern "C" void df11_encode_plan_free(df11_encode_plan *plan) {
+    if (!plan) return;
+    std::free(plan->luts);
+    std::memset(plan, 0, sizeof(*plan));
+}

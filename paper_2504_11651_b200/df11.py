@@ -25,7 +25,8 @@ MAX_BATCH = 64
 EXPORTED_SYMBOLS = ("df11_encode", "df11_encode_group", "df11_host_tensor_free", "df11_decompress",
                     "df11_decompress_block", "df11_decompress_block_ex", "df11_decompress_host",
                     "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
-                    "df11_launch_count")
+                    "df11_launch_count", "df11_histogram_device", "df11_encode_plan_create",
+                    "df11_encode_plan_free", "df11_encode_device")
 
 
 class Df11Error(RuntimeError):
@@ -62,6 +63,22 @@ class DeviceTensorC(ctypes.Structure):
                 ("reserved", ctypes.c_uint32)]
 
 
+class EncodePlanC(ctypes.Structure):
+    _fields_ = [("num_elements", ctypes.c_uint64), ("encoded_bits", ctypes.c_uint64),
+                ("T", ctypes.c_uint32), ("n", ctypes.c_uint32), ("B", ctypes.c_uint32), ("k", ctypes.c_uint32),
+                ("lut_entry_bytes", ctypes.c_uint32), ("max_code_len", ctypes.c_uint32),
+                ("code_lengths", ctypes.c_uint8 * 256), ("codes", ctypes.c_uint32 * 256),
+                ("luts", ctypes.POINTER(ctypes.c_uint8)), ("luts_bytes", ctypes.c_uint64),
+                ("encoded_exponent_bytes", ctypes.c_uint64), ("packed_sign_mantissa_bytes", ctypes.c_uint64),
+                ("gaps_bytes", ctypes.c_uint64), ("workspace_bytes", ctypes.c_uint64)]
+
+
+class DeviceBuffersC(ctypes.Structure):
+    _fields_ = [("encoded_exponent", ctypes.c_void_p), ("packed_sign_mantissa", ctypes.c_void_p),
+                ("gaps", ctypes.c_void_p), ("luts", ctypes.c_void_p), ("code_lengths", ctypes.c_void_p),
+                ("block_output_pos", ctypes.c_void_p)]
+
+
 _lib = None
 
 
@@ -80,8 +97,13 @@ def lib():
         L.df11_decompress_block.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P]
         L.df11_decompress_block_ex.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P, ctypes.c_int]
         L.df11_decompress_host.argtypes = [ctypes.POINTER(HostTensorC), ctypes.POINTER(DeviceTensorC), P, P]
+        L.df11_histogram_device.argtypes = [P, U64, P, P]
+        L.df11_encode_plan_create.argtypes = [P, P, ctypes.POINTER(EncodeOpts), ctypes.POINTER(EncodePlanC)]
+        L.df11_encode_plan_free.argtypes = [ctypes.POINTER(EncodePlanC)]
+        L.df11_encode_device.argtypes = [P, ctypes.POINTER(EncodePlanC), ctypes.POINTER(DeviceBuffersC), P, U64, P]
         for f in ("df11_encode", "df11_encode_group", "df11_decompress", "df11_decompress_block",
-                  "df11_decompress_block_ex", "df11_decompress_host"):
+                  "df11_decompress_block_ex", "df11_decompress_host", "df11_histogram_device",
+                  "df11_encode_plan_create", "df11_encode_device"):
             getattr(L, f).restype = ctypes.c_int
         L.df11_status_string.argtypes = [ctypes.c_int]
         L.df11_status_string.restype = ctypes.c_char_p
@@ -341,3 +363,117 @@ def decompress_host(h: HostTensor, dt: DeviceTensor, host_out, stream=None):
     _check(lib().df11_decompress_host(ctypes.byref(h._c), ctypes.byref(c_d),
                                       ctypes.c_void_p(host_out.data_ptr()), _stream_ptr(stream)))
     return host_out
+
+
+# --------------------------------------------------------------------------- device encoder (NEXT-3)
+class EncodePlan:
+    """df11_encode_plan: codebook + geometry of one tensor (host); frees its LUT copy on deletion."""
+
+    def __init__(self, codebook_hist, tensor_hist=None, T: int = 256, n: int = 8, lut_mode: str = "auto"):
+        cb = np.ascontiguousarray(codebook_hist, dtype=np.uint64)
+        th = None if tensor_hist is None else np.ascontiguousarray(tensor_hist, dtype=np.uint64)
+        if cb.shape != (256,) or (th is not None and th.shape != (256,)):
+            raise ValueError("histograms have 256 bins")
+        self._c = EncodePlanC()
+        o = _opts(T, n, lut_mode, 0)
+        _check(lib().df11_encode_plan_create(ctypes.c_void_p(cb.ctypes.data),
+                                             None if th is None else ctypes.c_void_p(th.ctypes.data),
+                                             ctypes.byref(o), ctypes.byref(self._c)))
+
+    def __del__(self):
+        try:
+            lib().df11_encode_plan_free(ctypes.byref(self._c))
+        except Exception:
+            pass
+
+    def __getattr__(self, name):
+        if name in ("num_elements", "encoded_bits", "T", "n", "B", "k", "lut_entry_bytes", "max_code_len",
+                    "luts_bytes", "encoded_exponent_bytes", "packed_sign_mantissa_bytes", "gaps_bytes",
+                    "workspace_bytes"):
+            return int(getattr(self.__dict__["_c"], name))
+        raise AttributeError(name)
+
+    @property
+    def code_lengths(self):
+        return np.frombuffer(bytes(self._c.code_lengths), np.uint8).copy()
+
+
+def _dev_u16(x):
+    import torch
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if x.dtype not in _u16_dtypes():
+        raise ValueError("expected a 16-bit tensor (BF16 bit patterns)")
+    return x.contiguous()
+
+
+def histogram_device(x, out=None, stream=None):
+    """df11_histogram_device: exponent histogram of a device BF16 tensor, accumulated into `out`
+    (int64[256] on the same device; zeroed when created here)."""
+    import torch
+    x = _dev_u16(x)
+    if out is None:
+        out = torch.zeros(256, dtype=torch.int64, device=x.device)
+    _check(lib().df11_histogram_device(ctypes.c_void_p(x.data_ptr()), x.numel(), ctypes.c_void_p(out.data_ptr()),
+                                       _stream_ptr(stream)))
+    return out
+
+
+def encode_device(x, T: int = 256, n: int = 8, lut_mode: str = "auto", codebook_hist=None, stream=None,
+                  out=None) -> "DeviceTensor":
+    """GPU encoder: device BF16 tensor -> DeviceTensor (histogram on the GPU, codebook on the host,
+    packing on the GPU).  Byte-identical to encode(x.cpu()) with the same options; with
+    `codebook_hist` (host, 256 bins, e.g. a group's summed histogram) the codebook is built from it."""
+    import torch
+    x = _dev_u16(x)
+    th = histogram_device(x, stream=stream).cpu().numpy().view(np.uint64)   # synchronises
+    plan = EncodePlan(th if codebook_hist is None else codebook_hist, th, T, n, lut_mode)
+    return encode_device_with_plan(x, plan, stream=stream, out=out)
+
+
+def encode_device_with_plan(x, plan: EncodePlan, stream=None, out=None) -> "DeviceTensor":
+    import torch
+    x = _dev_u16(x)
+    if x.numel() != plan.num_elements:
+        raise ValueError("tensor size does not match the plan")
+    dev = x.device
+
+    def buf(nbytes):
+        return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=dev)
+
+    dt = DeviceTensor.__new__(DeviceTensor)
+    dt.shape = tuple(x.shape)
+    dt.num_elements = plan.num_elements
+    dt.meta = {k: getattr(plan, k) for k in ("T", "n", "B", "k", "lut_entry_bytes", "encoded_bits", "max_code_len")}
+    dt.encoded_exponent = buf(plan.encoded_exponent_bytes)
+    dt.packed_sign_mantissa = buf(plan.packed_sign_mantissa_bytes)
+    dt.gaps = buf(plan.gaps_bytes)
+    dt.luts = buf(plan.luts_bytes)
+    dt.code_lengths = buf(256)
+    dt.block_output_pos = buf(4 * (plan.B + 1))
+    B, T = plan.B, plan.T
+    dt.compressed_bytes = ((plan.encoded_bits + 7) // 8 + plan.num_elements + (5 * B * T + 7) // 8
+                           + 4 * (B + 1) + plan.luts_bytes + 256)
+    dt.out = out if out is not None else torch.empty(max(plan.num_elements, 1), dtype=torch.bfloat16, device=dev)
+    ws = buf(plan.workspace_bytes)
+    d = DeviceBuffersC(dt.encoded_exponent.data_ptr(), dt.packed_sign_mantissa.data_ptr(), dt.gaps.data_ptr(),
+                       dt.luts.data_ptr(), dt.code_lengths.data_ptr(), dt.block_output_pos.data_ptr())
+    _check(lib().df11_encode_device(ctypes.c_void_p(x.data_ptr() if x.numel() else 0), ctypes.byref(plan._c),
+                                    ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                    _stream_ptr(stream)))
+    dt._workspace = ws     # keep alive until the stream has consumed it
+    return dt
+
+
+def encode_device_group(xs, T: int = 256, n: int = 8, lut_mode: str = "auto", shared_codebook: bool = True,
+                        stream=None):
+    """GPU encoder for a group of tensors (e.g. one transformer block); shared_codebook builds one
+    codebook from the summed histogram (R5)."""
+    hists = [histogram_device(x, stream=stream) for x in xs]
+    hs = [h.cpu().numpy().view(np.uint64) for h in hists]
+    total = np.sum(np.stack(hs), axis=0, dtype=np.uint64) if hs else np.zeros(256, np.uint64)
+    res = []
+    for x, h in zip(xs, hs):
+        plan = EncodePlan(total if shared_codebook else h, h, T, n, lut_mode)
+        res.append(encode_device_with_plan(x, plan, stream=stream))
+    return res

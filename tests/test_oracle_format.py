@@ -188,3 +188,24 @@ def test_corrupt_stream_detected(oracle_mod):
     bad["block_output_pos"][1] += 1
     with pytest.raises(oracle_mod.FormatError):
         oracle_mod.decode_alg1(bad, check_counts=True)
+
+
+def test_shared_codebook_scope(oracle_mod):
+    """R5 codebook scope: a group histogram yields the group's code lengths, stays lossless, equals the
+    per-tensor encoding when the group is the tensor itself, and rejects uncoded exponents."""
+    a = workloads.gaussian_bf16((50001,), seed=11)
+    b = workloads.gaussian_bf16((7777,), seed=12, sigma=0.2)
+    ha = oracle_mod.histogram(oracle_mod.split(a)[0])
+    hb = oracle_mod.histogram(oracle_mod.split(b)[0])
+    own = oracle_mod.encode(a)
+    same = oracle_mod.encode(a, codebook_hist=ha)
+    for key in ("encoded_exponent", "gaps", "block_output_pos", "luts", "code_lengths"):
+        assert np.array_equal(own[key], same[key]), key
+    group = ha + hb
+    fa = oracle_mod.encode(a, codebook_hist=group)
+    from oracle import huffman
+    assert list(fa["code_lengths"]) == huffman.code_lengths([int(x) for x in group])
+    assert np.array_equal(oracle_mod.decode_sequential(fa), a)
+    assert fa["encoded_bits"] >= own["encoded_bits"]          # the tensor's own Huffman code is optimal
+    with pytest.raises(oracle_mod.FormatError):
+        oracle_mod.encode(b, codebook_hist=ha * (hb == 0))
