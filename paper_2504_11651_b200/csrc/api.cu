@@ -145,7 +145,7 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
         bt.tile_start[bt.count] = pos;
         bt.total_tiles = pos;
         bt.grid = G;
-        const uint32_t kpow[8] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u, 1u};
+        const uint32_t kpow[8] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7};
         std::memcpy(bt.kpow, kpow, sizeof(kpow));
         e = df11::launch_fast(bt, dev, stream, &g_launches);
         if (e != cudaSuccess) return cuda_fail(e, "fast decode launch");

@@ -32,6 +32,14 @@
 namespace df11 {
 namespace {
 
+#ifndef DF11_STEPS_FIRST
+#define DF11_STEPS_FIRST 4
+#endif
+#ifndef DF11_STEPS_EACH
+#define DF11_STEPS_EACH 2
+#endif
+constexpr int kStepsFirst = DF11_STEPS_FIRST;   // decode steps before the first warp check
+constexpr int kStepsEach = DF11_STEPS_EACH;     // decode steps between later warp checks
 constexpr uint32_t kT = 256;               // format threads per block
 constexpr uint32_t kN = 8;                 // bytes per format thread
 constexpr uint32_t kCpl = 2;               // chunks per lane
@@ -226,9 +234,29 @@ __device__ __forceinline__ uint32_t compose2(uint32_t E, uint32_t S) {
 
 // Four BF16 from 4 exponents E and 4 sign/mantissa bytes S, as byte planes: the high byte of each
 // BF16 is sign | E >> 1, the low byte (E & 1) << 7 | mantissa; PRMT interleaves them.
-__device__ __forceinline__ void compose4(uint32_t E, uint32_t S, uint32_t &lo2, uint32_t &hi2) {
+// (m ? c : a) bitwise, one LOP3 (truth table 0xB8 for a=0xF0, b=0xCC, c=0xAA)
+template <uint32_t m>
+__device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xB8;" : "=r"(d) : "r"(a), "n"(m), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t mullo(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+// E >> 1 and E << 7 as IMAD.HI / IMAD by constant-bank multipliers k_half = 2^31, k_128 = 2^7 (FMA
+// pipe), the byte-plane selects as one LOP3 each and the interleave as two PRMT (ALU pipe).
+__device__ __forceinline__ void compose4(uint32_t E, uint32_t S, uint32_t &lo2, uint32_t &hi2, uint32_t k_half,
+                                         uint32_t k_128) {
+#ifdef DF11_OLD_COMPOSE
     const uint32_t H = (S & 0x80808080u) | ((E >> 1) & 0x7F7F7F7Fu);
     const uint32_t L = ((E << 7) & 0x80808080u) | (S & 0x7F7F7F7Fu);
+#else
+    const uint32_t H = bitsel<0x80808080u>(mulhi(E, k_half), S);
+    const uint32_t L = bitsel<0x7F7F7F7Fu>(mullo(E, k_128), S);
+#endif
     lo2 = prmt(L, H, 0x5140u);
     hi2 = prmt(L, H, 0x7362u);
 }
@@ -246,6 +274,8 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
 #define K_S8 bt.kpow[3]
 #define K_S16 bt.kpow[4]
 #define K_S29 bt.kpow[5]
+#define K_HALF bt.kpow[6]
+#define K_SH7 bt.kpow[7]
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
     const uint32_t t1_lane = sbase + kOffT1 + lane * 4u;         // row r at + r*128
@@ -424,16 +454,20 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             shift96(aA, bA, cA, gapA);
             shift96(aB, bB, cB, gapB);
             uint32_t accA = gapA, accB = 64u + gapB, eA1 = 1, eB1 = 1;          // acc = offset | count << 8
-            for (;;) {
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const uint32_t eA = lds32(madlo(mulhi(aA, K_ROW), K_128, t1_lane));
+            // lockstep schedule: 4 steps, then a warp check (end / escapes) every 2 steps -- a chain
+            // needs ~8.2 lookups and the warp waits for its slowest lane, so checking every 4 steps
+            // wasted ~25 % of the steps
+            auto p1_step = [&]() {
+                const uint32_t eA = lds32(madlo(mulhi(aA, K_ROW), K_128, t1_lane));
                     const uint32_t eB = lds32(madlo(mulhi(aB, K_ROW), K_128, t1_lane));
-                    if ((accA & 0xC0u) == 0) { accA += eA; eA1 = eA; }         // offset < 64
-                    if ((accB & 0x80u) == 0) { accB += eB; eB1 = eB; }         // offset < 128
-                    shift96(aA, bA, cA, eA);                                   // e & 31 = consumed bits
-                    shift96(aB, bB, cB, eB);
-                }
+                if ((accA & 0xC0u) == 0) { accA += eA; eA1 = eA; }             // offset < 64
+                if ((accB & 0x80u) == 0) { accB += eB; eB1 = eB; }             // offset < 128
+                shift96(aA, bA, cA, eA);                                       // e & 31 = consumed bits
+                shift96(aB, bB, cB, eB);
+            };
+#pragma unroll
+            for (int u = 0; u < kStepsFirst; u++) p1_step();
+            for (;;) {
                 const bool actA = (accA & 0xC0u) == 0, actB = (accB & 0x80u) == 0;
                 if (!__any_sync(FULL, actA || actB)) break;
                 const bool escA = actA && (eA1 & 0x7FFFFFu) == 0, escB = actB && (eB1 & 0x7FFFFFu) == 0;
@@ -451,6 +485,8 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                         shift96_long(aB, bB, cB, vB >> 8);
                     }
                 }
+#pragma unroll
+                for (int u = 0; u < kStepsEach; u++) p1_step();
             }
             // each chain's last T1 group may hold complete codes starting past its end: not ours
             uint32_t cntA = (accA >> 8) & 0xFFu, cntB = (accB >> 8) & 0xFFu;
@@ -510,22 +546,23 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 shift96(aA, bA, cA, gapA);
                 shift96(aB, bB, cB, gapB);
                 uint32_t wA = wp0, wB = wpAe, eA2 = 1, eB2 = 1;
-                for (;;) {
+                auto p2_step = [&]() {
+                    eA2 = lds32(madlo(mulhi(aA, K_ROW), K_128, t2_lane));
+                    eB2 = lds32(madlo(mulhi(aB, K_ROW), K_128, t2_lane));
+                    sts8_if<0>(wA, eA2, wA, wpAe);
+                    sts8_if<1>(wA, mulhi(eA2, K_S8), wA, wpAe - 1);
+                    sts8_if<2>(wA, mulhi(eA2, K_S16), wA, wpAe - 2);
+                    sts8_if<0>(wB, eB2, wB, wend);
+                    sts8_if<1>(wB, mulhi(eB2, K_S8), wB, wend - 1);
+                    sts8_if<2>(wB, mulhi(eB2, K_S16), wB, wend - 2);
+                    wA += eA2 >> 29;                                           // count (LEA.HI)
+                    wB += eB2 >> 29;
+                    shift96(aA, bA, cA, mulhi(eA2, K_S24));                    // (e >> 24) & 31 = consumed
+                    shift96(aB, bB, cB, mulhi(eB2, K_S24));
+                };
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        eA2 = lds32(madlo(mulhi(aA, K_ROW), K_128, t2_lane));
-                        eB2 = lds32(madlo(mulhi(aB, K_ROW), K_128, t2_lane));
-                        sts8_if<0>(wA, eA2, wA, wpAe);
-                        sts8_if<1>(wA, mulhi(eA2, K_S8), wA, wpAe - 1);
-                        sts8_if<2>(wA, mulhi(eA2, K_S16), wA, wpAe - 2);
-                        sts8_if<0>(wB, eB2, wB, wend);
-                        sts8_if<1>(wB, mulhi(eB2, K_S8), wB, wend - 1);
-                        sts8_if<2>(wB, mulhi(eB2, K_S16), wB, wend - 2);
-                        wA += eA2 >> 29;                                       // count (LEA.HI)
-                        wB += eB2 >> 29;
-                        shift96(aA, bA, cA, mulhi(eA2, K_S24));                // (e >> 24) & 31 = consumed
-                        shift96(aB, bB, cB, mulhi(eB2, K_S24));
-                    }
+                for (int u = 0; u < kStepsFirst; u++) p2_step();
+                for (;;) {
                     const bool actA = wA < wpAe, actB = wB < wend;
                     if (!__any_sync(FULL, actA || actB)) break;
                     const bool escA = actA && eA2 < (1u << 24), escB = actB && eB2 < (1u << 24);
@@ -543,6 +580,8 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                             shift96_long(aB, bB, cB, vB >> 8);
                         }
                     }
+#pragma unroll
+                    for (int u = 0; u < kStepsEach; u++) p2_step();
                 }
             } else {
                 // direct mode (more than kCap outputs in this tile): compose and store to HBM per code
@@ -584,10 +623,10 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
                 const uint4 sm = it == 0 ? smA : (it == 1 ? smB : __ldg(psm4 + gi));
                 const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - f));
                 uint4 o0, o1;
-                compose4(ex.x, sm.x, o0.x, o0.y);
-                compose4(ex.y, sm.y, o0.z, o0.w);
-                compose4(ex.z, sm.z, o1.x, o1.y);
-                compose4(ex.w, sm.w, o1.z, o1.w);
+                compose4(ex.x, sm.x, o0.x, o0.y, K_HALF, K_SH7);
+                compose4(ex.y, sm.y, o0.z, o0.w, K_HALF, K_SH7);
+                compose4(ex.z, sm.z, o1.x, o1.y, K_HALF, K_SH7);
+                compose4(ex.w, sm.w, o1.z, o1.w, K_HALF, K_SH7);
                 uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
                 dst[0] = o0;
                 dst[1] = o1;

@@ -13,7 +13,8 @@ import os
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdf11.so")
+_LIB_PATH = os.environ.get("DF11_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                        "libdf11.so")   # DF11_LIB: A/B builds
 
 DF11_OK = 0
 STATUS = {0: "DF11_OK", 1: "DF11_E_INVALID_ARGUMENT", 2: "DF11_E_RESERVED_EXPONENT", 3: "DF11_E_LUT_OVERFLOW",
