@@ -44,8 +44,11 @@ constexpr uint32_t kT = 256;               // format threads per block
 constexpr uint32_t kN = 8;                 // bytes per format thread
 constexpr uint32_t kCpl = 2;               // chunks per lane
 constexpr uint32_t kLanes = kT / kCpl;     // 128 threads per group (one tile)
-constexpr uint32_t kGroups = 8;
-constexpr uint32_t kCta = kLanes * kGroups;  // 1024 threads
+#ifndef DF11_GROUPS
+#define DF11_GROUPS 8
+#endif
+constexpr uint32_t kGroups = DF11_GROUPS;    // tile groups (of kLanes threads) per CTA
+constexpr uint32_t kCta = kLanes * kGroups;  // 1024 threads by default
 constexpr uint32_t kWarps = kLanes / 32;   // 4 warps per group
 constexpr uint32_t kBits = 8 * kN * kCpl;  // 128 bits decoded per lane
 constexpr uint32_t kR = 9;                 // root bits of the derived tables
@@ -234,6 +237,14 @@ __device__ __forceinline__ uint32_t compose2(uint32_t E, uint32_t S) {
 
 // Four BF16 from 4 exponents E and 4 sign/mantissa bytes S, as byte planes: the high byte of each
 // BF16 is sign | E >> 1, the low byte (E & 1) << 7 | mantissa; PRMT interleaves them.
+// Phase-1 update "if ((acc & M) == 0) { acc += e; e1 = e; }" as one predicate-setting LOP3 and two
+// predicated instructions.
+template <uint32_t M>
+__device__ __forceinline__ void p1_apply(uint32_t &acc, uint32_t &e1, uint32_t e) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %0, %3;\n\tsetp.eq.u32 p, t, 0;\n\t"
+        "@p add.u32 %0, %0, %2;\n\t@p mov.b32 %1, %2;\n\t}"
+        : "+r"(acc), "+r"(e1) : "r"(e), "n"(M));
+}
 // (m ? c : a) bitwise, one LOP3 (truth table 0xB8 for a=0xF0, b=0xCC, c=0xAA)
 template <uint32_t m>
 __device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t c) {
@@ -460,8 +471,8 @@ __global__ void __launch_bounds__(kCta, 1) fast_kernel(const __grid_constant__ B
             auto p1_step = [&]() {
                 const uint32_t eA = lds32(madlo(mulhi(aA, K_ROW), K_128, t1_lane));
                     const uint32_t eB = lds32(madlo(mulhi(aB, K_ROW), K_128, t1_lane));
-                if ((accA & 0xC0u) == 0) { accA += eA; eA1 = eA; }             // offset < 64
-                if ((accB & 0x80u) == 0) { accB += eB; eB1 = eB; }             // offset < 128
+                p1_apply<0xC0u>(accA, eA1, eA);                                // offset < 64
+                p1_apply<0x80u>(accB, eB1, eB);                                // offset < 128
                 shift96(aA, bA, cA, eA);                                       // e & 31 = consumed bits
                 shift96(aB, bB, cB, eB);
             };
