@@ -15,6 +15,7 @@
 namespace df11 {
 cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_fast(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
+cudaError_t launch_sp(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 bool fast_supports(const df11_device_tensor &t);
 uint32_t fast_grid(uint32_t total_tiles, int num_sms);
 }  // namespace df11
@@ -147,7 +148,11 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
         bt.grid = G;
         const uint32_t kpow[8] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7};
         std::memcpy(bt.kpow, kpow, sizeof(kpow));
-        e = df11::launch_fast(bt, dev, stream, &g_launches);
+#ifdef DF11_TWO_PASS
+        e = df11::launch_fast(bt, dev, stream, &g_launches);    // two decode passes (decode_fast.cu)
+#else
+        e = df11::launch_sp(bt, dev, stream, &g_launches);      // single pass (decode_sp.cu)
+#endif
         if (e != cudaSuccess) return cuda_fail(e, "fast decode launch");
         return DF11_OK;
     }
