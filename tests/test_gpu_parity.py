@@ -53,7 +53,8 @@ def _check_oracle_format(df11, oracle_mod, w, kernel, **kw):
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("case", ["gauss_1m", "gauss_ragged", "constant_1bit", "two_symbol", "all_patterns_wide",
                                   "overflow_wide", "fibonacci_32bit", "one_element", "tiny_17", "sigma_large",
-                                  "random_bits", "escape_heavy", "escape_deep"])
+                                  "random_bits", "escape_heavy", "escape_deep", "uniform8_short_codes",
+                                  "one_bit_with_tail"])
 def test_parity_cases(df11, oracle_mod, kernel, case):
     if case == "gauss_1m":
         w = workloads.gaussian_bf16((1 << 20,), seed=1)
@@ -84,6 +85,15 @@ def test_parity_cases(df11, oracle_mod, kernel, case):
         counts.update({i: 200 for i in range(1, 100)})
         counts.update({116 + i: 200 for i in range(101)})
         w = workloads.from_exponent_histogram(counts, seed=7)
+    elif case == "uniform8_short_codes":
+        # 8 equally likely exponents: every code is 3 bits (no code longer than the 9-bit root, so
+        # the kernel cannot use one-bit chain-end sentinels and walks back instead)
+        w = workloads.from_exponent_histogram({100 + i: 40000 for i in range(8)}, seed=9)
+    elif case == "one_bit_with_tail":
+        # a 1-bit codeword (p > 1/2) plus a geometric tail of long codes: count + direct path
+        counts = {127: 600000}
+        counts.update({e: max(1, int(50000 * 0.6 ** i)) for i, e in enumerate(range(100, 127))})
+        w = workloads.from_exponent_histogram(counts, seed=10)
     elif case == "escape_deep":
         # geometric tail: codes up to ~26 bits, some beyond the second level (walk path)
         counts = {e: max(1, int(400000 * 0.72 ** i)) for i, e in enumerate(range(60, 200))}
