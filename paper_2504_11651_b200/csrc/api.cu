@@ -16,6 +16,7 @@ namespace df11 {
 cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_fast(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_sp(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
+cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 bool fast_supports(const df11_device_tensor &t);
 uint32_t fast_grid(uint32_t total_tiles, int num_sms);
 }  // namespace df11
@@ -146,12 +147,15 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
         bt.tile_start[bt.count] = pos;
         bt.total_tiles = pos;
         bt.grid = G;
-        const uint32_t kpow[8] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7};
+        const uint32_t kpow[10] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7,
+                                   1u << 12, 8u};
         std::memcpy(bt.kpow, kpow, sizeof(kpow));
 #ifdef DF11_TWO_PASS
         e = df11::launch_fast(bt, dev, stream, &g_launches);    // two decode passes (decode_fast.cu)
+#elif defined(DF11_SP9)
+        e = df11::launch_sp(bt, dev, stream, &g_launches);      // single pass, 9-bit table (decode_sp.cu)
 #else
-        e = df11::launch_sp(bt, dev, stream, &g_launches);      // single pass (decode_sp.cu)
+        e = df11::launch_sp12(bt, dev, stream, &g_launches);    // single pass, 12-bit table (decode_sp12.cu)
 #endif
         if (e != cudaSuccess) return cuda_fail(e, "fast decode launch");
         return DF11_OK;

@@ -1,0 +1,511 @@
+// decode_sp12.cu — single-pass persistent sm_100a DF11 decode kernel with a 12-bit multi-code table.
+//
+// Same schedule and result as decode_sp.cu: persistent 1024-thread CTAs of 8 groups, a
+// group owns one format block ("tile") at a time, each lane decodes two chunks as two interleaved
+// chains into private SMEM slots, a group scan gives the output positions (Alg. 1), the
+// slots are compacted per warp and merged with PackedSignMantissa into coalesced BF16 stores.
+// What differs is the decode table and the byte format of the exponents between decode and merge:
+//
+//  * T12: 4096 entries of 8 bytes indexed by the next 12 bits of the stream.  An entry holds up to 4
+//    complete codes: lo = their exponents (one byte each), hi = consumed bits | count << 29.  12 bits
+//    decode 3.8 codes per lookup on LLM-like exponents vs 2.8 for a 9-bit, 3-code table, and codes
+//    longer than 12 bits (resolved by the paper's LUT walk) are 8x rarer.  The table is not
+//    lane-replicated (32 KB); its LDS.64 bank conflicts are the price of 1.35x fewer lookups.
+//  * Exponents are stored rotated right by one bit, r = (e >> 1) | (e & 1) << 7: the BF16 high byte is
+//    then sign | (r & 0x7F) and the low byte (r & 0x80) | mantissa, two bit-selects per 4
+//    elements in the merge instead of a shift, a multiply and two bit-selects.
+//  * One step per chain: row = a >> 20, one LDS.64, x += hi, the 96-bit bit-buffer shift by hi & 31
+//    (funnel shifts use the low 5 bits), and the exponents are appended to the chain's slot through a
+//    pending word: m = acc | lo << fb is stored with ONE 32-bit STS, and the word pointer advances when
+//    the word is full.  Slots are lane-column-major (word k of lane l at k*128 + 4l), so every slot
+//    access of a warp hits 32 distinct banks.  hi = consumed | (8*count) << 24; x accumulates the
+//    consumed bits in its low 24 bits (the count garbage sits above).
+#include "fast_helpers.cuh"
+
+namespace df11 {
+namespace {
+
+#ifndef SP12_FIRST
+#define SP12_FIRST 6
+#endif
+#ifndef SP12_EACH
+#define SP12_EACH 1
+#endif
+constexpr int kFirst = SP12_FIRST;          // decode steps before the first warp check
+constexpr int kEach = SP12_EACH;            // decode steps between later warp checks
+constexpr uint32_t kGroups12 = 8;
+constexpr uint32_t kCta12 = kLanes * kGroups12;
+constexpr uint32_t kWarps12 = kLanes / 32;
+constexpr uint32_t kR = 12;                 // root bits of T12
+constexpr uint32_t kRows = 1u << kR;
+constexpr uint32_t kCodes = 4;              // codes per entry
+constexpr uint32_t kLutSmem = 8192;
+constexpr uint32_t kSubW = 12;              // slot words per chain: <= 32 codes + overshoot
+constexpr uint32_t kWarpReg12 = 16 + 2 * kSubW * 128;   // frame pad + lane-column slots of 2 chains
+constexpr uint32_t kXMask = (1u << 24) - 1u;
+
+constexpr uint32_t kOffT = 0;                                       // uint2 [kRows] + null entry
+constexpr uint32_t kOffLut = kOffT + kRows * 8 + 16;
+constexpr uint32_t kOffLen = kOffLut + kLutSmem;                    // CodeLengths[e]
+constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengths[unrot(r)]
+constexpr uint32_t kOffWsum = kOffRLen + 256;                       // [groups][2][warps]
+constexpr uint32_t kOffReg = kOffWsum + kGroups12 * 2 * kWarps12 * 4;
+constexpr uint32_t kOffStage = kOffReg + kGroups12 * kWarps12 * kWarpReg12;
+constexpr uint32_t kOffMbar = kOffStage + kGroups12 * kStageBytes;
+constexpr uint32_t kSmem12 = kOffMbar + kGroups12 * 8;
+static_assert(kOffReg % 16 == 0 && kWarpReg12 % 16 == 0 && kOffStage % 16 == 0 && kOffMbar % 8 == 0,
+              "alignment");
+static_assert(kSmem12 <= 232448, "SMEM budget");
+
+__device__ __forceinline__ uint32_t rot8(uint32_t e) { return ((e >> 1) | (e << 7)) & 0xFFu; }
+__device__ __forceinline__ uint32_t unrot8(uint32_t r) { return ((r << 1) | (r >> 7)) & 0xFFu; }
+
+__device__ __forceinline__ void st8(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+template <int k>
+__device__ __forceinline__ void st8k(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u8 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(k) : "memory");
+}
+__device__ __forceinline__ uint32_t ld8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void lds64(uint32_t addr, uint32_t &lo, uint32_t &hi) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(addr));
+}
+__device__ __forceinline__ void lds128(uint32_t addr, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Append the n <= 4 bytes of lo (n*8 = hi >> 24) to a lane-column slot through the pending word acc
+// (fb valid bits, < 32) at word address wp.  The partial word is stored every time; it is completed
+// (and rewritten) by later appends.
+__device__ __forceinline__ void pack(uint32_t lo, uint32_t hi, uint32_t &acc, uint32_t &fb, uint32_t &wp,
+                                     uint32_t k_s24) {
+    const uint32_t m = acc | (lo << fb);
+    const uint32_t sp = __funnelshift_l(lo, 0u, fb);        // bytes that spill into the next word
+    sts32(wp, m);
+    fb = madhi(hi, k_s24, fb);
+    const bool full = fb >= 32u;
+    wp = full ? wp + 128u : wp;
+    acc = full ? sp : m;
+    fb &= 31u;
+}
+
+// 96-bit bit buffer shifts that pull in one-bits (the chain-end sentinel, see the kernel)
+__device__ __forceinline__ void shift96_ones(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
+    a = __funnelshift_l(b, a, s);
+    b = __funnelshift_l(c, b, s);
+    c = __funnelshift_l(0xFFFFFFFFu, c, s);
+}
+__device__ __forceinline__ void shift96_long_ones(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
+    const bool w = s >= 32;
+    a = w ? b : a;
+    b = w ? c : b;
+    c = w ? 0xFFFFFFFFu : c;
+    shift96_ones(a, b, c, s);
+}
+__device__ __forceinline__ void sts32_if(uint32_t addr, uint32_t v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
+                 ::"r"(addr), "r"(v), "r"((uint32_t)p) : "memory");
+}
+
+// Copy n (<= 32) bytes held in w[0..7] (little-endian byte stream) to SMEM byte address d.  Phase A:
+// the whole words of the destination (the last may carry garbage past the end: the next chain's phase B
+// rewrites those bytes).  Phase B (after a __syncwarp): the first, partial word.
+__device__ __forceinline__ void compact_words(uint32_t d, const uint32_t (&w)[8], uint32_t n) {
+    const uint32_t r = d & 3u, db = d - r, sh = r * 8u;
+    const uint32_t nw = (r + n + 3u) >> 2;                 // <= 9
+#pragma unroll
+    for (int k = 0; k < 9; k++) {
+        const uint32_t v = k == 0 ? w[0] : __funnelshift_l(w[k - 1], k < 8 ? w[k] : 0u, sh);
+        sts32_if(db + 4u * k, v, (uint32_t)k < nw && (k > 0 || r == 0));
+    }
+}
+__device__ __forceinline__ void compact_head(uint32_t d, uint32_t w0, uint32_t n) {
+    const uint32_t r = d & 3u, db = d - r;
+    if (r == 0) return;
+    const uint32_t v0 = w0 << (r * 8u);
+#pragma unroll
+    for (uint32_t i = 1; i < 4; i++)
+        if (i >= r && i < r + n) st8(db + i, v0 >> (8u * i));
+}
+
+// Four BF16 from 4 rotated exponents R and 4 sign/mantissa bytes S (byte planes):
+// high byte = sign | (R & 0x7F), low byte = (R & 0x80) | mantissa; PRMT interleaves them.
+__device__ __forceinline__ void compose4r(uint32_t R, uint32_t S, uint32_t &lo2, uint32_t &hi2) {
+    const uint32_t H = bitsel<0x80808080u>(R, S);
+    const uint32_t L = bitsel<0x7F7F7F7Fu>(R, S);
+    lo2 = prmt(L, H, 0x5140u);
+    hi2 = prmt(L, H, 0x7362u);
+}
+__device__ __forceinline__ uint16_t compose_r(uint32_t r, uint32_t psm) {
+    return (uint16_t)(((psm & 0x80u) << 8) | ((r & 0x7Fu) << 8) | (r & 0x80u) | (psm & 0x7Fu));
+}
+
+__global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__ Batch bt) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t g = tid / kLanes;
+    const uint32_t t = tid % kLanes;
+    const uint32_t lane = tid & 31, wig = t >> 5;
+    const uint32_t FULL = 0xFFFFFFFFu;
+#define K_ROW bt.kpow[8]   // 2^12: a >> 20
+#define K_ENT bt.kpow[9]   // 8: entry bytes
+#define K_S8 bt.kpow[3]    // 2^24: >> 8
+#define K_S16 bt.kpow[4]   // 2^16: >> 16
+#define K_S24 bt.kpow[2]   // 2^8: >> 24
+    uint8_t *sb = smem_b();
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
+    const uint32_t tab = sbase + kOffT;
+    const uint32_t null_ent = sbase + kOffT + kRows * 8u;   // all-zero entry: advances nothing
+    const uint32_t wreg = kOffReg + (g * kWarps12 + wig) * kWarpReg12;   // this warp's region (byte offset)
+    uint32_t *wsum = smem_w + kOffWsum / 4 + g * 2 * kWarps12;
+    const uint32_t stage = sbase + kOffStage + g * kStageBytes;
+    const uint32_t mbar = sbase + kOffMbar + g * 8;
+    const uint32_t slotA = sbase + wreg + 16u + lane * 4u, slotB = slotA + kSubW * 128u;
+    const uint32_t rlenb = sbase + kOffRLen;
+
+    const uint32_t total = bt.total_tiles;
+    const uint32_t c_begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
+    const uint32_t c_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
+    if (c_begin >= c_end) return;
+    if (t == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < 4) smem_w[(kOffT + kRows * 8u) / 4 + tid] = 0;
+    uint32_t q = 0, parity = 0;
+
+    int ti_idx = tensor_of_tile(bt, c_begin);
+    for (uint32_t seg_begin = c_begin; seg_begin < c_end; ti_idx++) {
+        const df11_device_tensor &ts = bt.t[ti_idx];
+        const uint32_t seg_end = min(c_end, bt.tile_start[ti_idx + 1]);
+        const uint32_t base_tile = bt.tile_start[ti_idx] - bt.tile_off[ti_idx];
+        if (seg_end <= seg_begin) continue;
+
+        // =============================== T12 for this tensor (CTA-wide)
+        __syncthreads();
+        const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
+        const uint32_t lut_bytes = kk * 256u * eb_bytes;
+        const bool lut_in_smem = lut_bytes <= kLutSmem;
+        if (lut_in_smem)
+            for (uint32_t i = tid; i < lut_bytes; i += kCta12) sb[kOffLut + i] = __ldg(ts.luts + i);
+        if (tid < 256u) {
+            const uint32_t l = __ldg(ts.code_lengths + tid);
+            sb[kOffLen + tid] = (uint8_t)l;
+            sb[kOffRLen + rot8(tid)] = (uint8_t)(l ? l : 32u);
+        }
+        __syncthreads();
+        auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
+            if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, len);
+            return lut_walk_global(w, ts, len);
+        };
+        bool row_esc_last = false;
+        for (uint32_t row = tid; row < kRows; row += kCta12) {
+            const uint32_t W = row << (32 - kR);
+            uint32_t s = 0, syms = 0, c2 = 0;
+            while (s < kR && c2 < kCodes) {
+                uint32_t len;
+                const uint32_t sym = walk(W << s, len);
+                if (len > kR - s) break;
+                s += len;
+                syms |= rot8(sym) << (8 * c2);
+                c2++;
+            }
+            *reinterpret_cast<uint2 *>(sb + kOffT + row * 8u) = make_uint2(syms, s | (c2 << 27));
+            if (row == kRows - 1) row_esc_last = c2 == 0;
+        }
+        // a 1-bit codeword allows 64 codes per chain: such tensors take the count + direct path
+        const bool safe = __syncthreads_or(tid < 256u && sb[kOffLen + tid] == 1) != 0;
+        // if 12 one-bits hold no complete code (true for canonical codes longer than 12 bits), one-bits
+        // after a chain's last bit stall it exactly there
+        const bool long_codes = __syncthreads_or(row_esc_last) != 0;
+
+        const uint32_t N = (uint32_t)ts.num_elements;
+        const bool vec_out = ((reinterpret_cast<uintptr_t>(ts.out) & 15) == 0);
+        const uint4 *__restrict__ psm4 = reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa);
+        uint16_t *__restrict__ out = ts.out;
+
+        // =============================== tiles of this group
+        uint32_t tile = seg_begin + g;
+        if (t == 0 && tile < seg_end) issue_tile(ts, tile - base_tile, stage, mbar);
+        uint32_t nlo = 0, nhi = 0;
+        if (tile < seg_end) {
+            nlo = __ldg(ts.block_output_pos + tile - base_tile);
+            nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
+        }
+        auto prefetch_sm = [&](uint32_t plo, uint32_t phi) {
+            const uint32_t a0 = min(plo, N) & ~15u, a1 = (min(max(phi, plo), N) + 15u) & ~15u;
+            if (a1 > a0) prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
+        };
+        if (t == 0 && tile < seg_end) prefetch_sm(nlo, nhi);
+        for (; tile < seg_end; tile += kGroups12, q++) {
+            const uint32_t b = tile - base_tile;
+            const uint32_t clo = nlo, chi = nhi;
+            const bool has_next = tile + kGroups12 < seg_end;
+            if (has_next) {
+                nlo = __ldg(ts.block_output_pos + b + kGroups12);
+                nhi = __ldg(ts.block_output_pos + b + kGroups12 + 1);
+            }
+            mbar_wait(mbar, q & 1u);
+            uint32_t r0, r1, r2, r3, r4, gapA, gapB, gapC;
+            {
+                lds128(stage + t * 16, r0, r1, r2, r3);
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r4) : "r"(stage + t * 16 + 16));
+                const uint32_t gb0 = stage + kChunkBytes + ((t * 10) >> 3);
+                // gaps of chunks 2t, 2t+1 and 2t+2 (the next tile's first for t = 127: the stage holds
+                // 16 bytes of gaps past the tile) start at bit 10t
+                const uint32_t h0 = ld8(gb0), h1 = ld8(gb0 + 1), h2 = ld8(gb0 + 2), h3 = ld8(gb0 + 3);
+                const uint32_t g32 = (h0 << 24) | (h1 << 16) | (h2 << 8) | h3;
+                const uint32_t g15 = (g32 >> (17u - ((t * 10) & 7u))) & 32767u;
+                gapA = g15 >> 10;
+                gapB = (g15 >> 5) & 31u;
+                gapC = g15 & 31u;
+            }
+            const uint32_t lo = min(clo, N);
+            const uint32_t hi = min(max(min(chi, N), lo), lo + 8 * kN * kT);
+            const uint32_t W0 = bswap32(r0), W1 = bswap32(r1), W2 = bswap32(r2), W3 = bswap32(r3),
+                           W4 = bswap32(r4);
+
+            uint32_t cntA, cntB;
+            if (!safe) {
+                // ---- single decode pass into the private slots (chains A: [gapA, 64), B: [64+gapB, 128))
+                // exact chain ends when the next chunk's gap marks a code start (every tile but the
+                // one holding the tensor's last code): A = [gapA, 64 + gapB), B = [64 + gapB, 128 + gapC),
+                // enforced by one-bits after the end; otherwise [.., 64) / [.., 128) + walk back
+                const bool exact = long_codes && hi < N;
+                const uint32_t limA = exact ? 64u + gapB - gapA : 64u - gapA;
+                const uint32_t limB = exact ? 64u + gapC - gapB : 64u - gapB;
+                uint32_t aA = W0, bA = W1, cA = exact ? W2 | (0xFFFFFFFFu >> gapB) : W2;
+                uint32_t aB = W2, bB = W3, cB = exact ? W4 | (0xFFFFFFFFu >> gapC) : W4;
+                shift96_ones(aA, bA, cA, gapA);
+                shift96_ones(aB, bB, cB, gapB);
+                uint32_t wA = slotA, wB = slotB, xA = 0, xB = 0, tA = tab, tB = tab;
+                uint32_t accA = 0, accB = 0, fA = 0, fB = 0;
+                uint32_t hA = 1, hB = 1;
+                auto step = [&]() {
+                    uint32_t lA, lB;
+                    lds64(madlo(mulhi(aA, K_ROW), K_ENT, tA), lA, hA);
+                    lds64(madlo(mulhi(aB, K_ROW), K_ENT, tB), lB, hB);
+                    pack(lA, hA, accA, fA, wA, K_S24);
+                    pack(lB, hB, accB, fB, wB, K_S24);
+                    xA += hA;
+                    xB += hB;
+                    shift96_ones(aA, bA, cA, hA);
+                    shift96_ones(aB, bB, cB, hB);
+                };
+#pragma unroll
+                for (int u = 0; u < kFirst; u++) step();
+                for (;;) {
+                    const bool actA = (xA & kXMask) < limA, actB = (xB & kXMask) < limB;
+                    if (!__any_sync(FULL, actA || actB)) break;
+                    if (!actA) { tA = null_ent; aA = 0; }                      // freeze on the null entry
+                    if (!actB) { tB = null_ent; aB = 0; }
+                    const bool escA = actA && hA == 0, escB = actB && hB == 0;
+                    if (__any_sync(FULL, escA || escB)) {
+                        if (escA) {
+                            uint32_t len;
+                            const uint32_t sym = walk(aA, len);
+                            pack(rot8(sym), 8u << 24, accA, fA, wA, K_S24);
+                            xA += len;
+                            shift96_long_ones(aA, bA, cA, len);
+                        }
+                        if (escB) {
+                            uint32_t len;
+                            const uint32_t sym = walk(aB, len);
+                            pack(rot8(sym), 8u << 24, accB, fB, wB, K_S24);
+                            xB += len;
+                            shift96_long_ones(aB, bB, cB, len);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kEach; u++) step();
+                }
+                sts32(wA, accA);                                               // the last partial word
+                sts32(wB, accB);
+                uint32_t nA = ((wA - slotA) >> 5) + (fA >> 3);                 // bytes: 4 per 128-byte row
+                uint32_t nB = ((wB - slotB) >> 5) + (fB >> 3);
+                // drop the codes decoded past each chain's end (they start at or after it)
+                if (!exact) {
+                    uint32_t offA = xA & kXMask;
+                    while (nA > 0) {
+                        const uint32_t j = nA - 1;
+                        const uint32_t l = ld8(rlenb + ld8(slotA + (j >> 2) * 128u + (j & 3u)));
+                        if (offA - l < limA) break;
+                        offA -= l;
+                        nA--;
+                    }
+                    uint32_t offB = xB & kXMask;
+                    while (nB > 0) {
+                        const uint32_t j = nB - 1;
+                        const uint32_t l = ld8(rlenb + ld8(slotB + (j >> 2) * 128u + (j & 3u)));
+                        if (offB - l < limB) break;
+                        offB -= l;
+                        nB--;
+                    }
+                }
+                cntA = nA;
+                cntB = nB;
+            } else {
+                // ---- count-only pass, one code at a time (1-bit codewords)
+                auto count_chain = [&](uint32_t a, uint32_t bb, uint32_t c, uint32_t off, uint32_t lim) {
+                    uint32_t n = 0;
+                    while (off < lim) {
+                        uint32_t el, eh, len;
+                        lds64(madlo(mulhi(a, K_ROW), K_ENT, tab), el, eh);
+                        if (eh != 0) len = ld8(rlenb + (el & 0xFFu));
+                        else walk(a, len);
+                        n++;
+                        off += len;
+                        shift96_long(a, bb, c, len);
+                    }
+                    return n;
+                };
+                uint32_t a = W0, bb = W1, c = W2;
+                shift96(a, bb, c, gapA);
+                cntA = count_chain(a, bb, c, gapA, 64u);
+                a = W2; bb = W3; c = W4;
+                shift96(a, bb, c, gapB);
+                cntB = count_chain(a, bb, c, 64u + gapB, 128u);
+            }
+            const uint32_t cnt = cntA + cntB;
+
+            // ---- exclusive scan of the counts over the tile: warp shuffles + 4 warp totals
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t v = __shfl_up_sync(FULL, incl, d);
+                if (lane >= (uint32_t)d) incl += v;
+            }
+            uint32_t *ws = wsum + parity * kWarps12;
+            if (lane == 31) ws[wig] = incl;
+            group_bar(g);                          // also: every thread has read this tile's stage
+            parity ^= 1u;
+            if (t == 0 && has_next) {
+                issue_tile(ts, b + kGroups12, stage, mbar);
+                prefetch_sm(nlo, nhi);
+            }
+            uint32_t wpre = 0;
+            {
+                const uint4 v = *reinterpret_cast<const uint4 *>(ws);
+                wpre = (wig > 0 ? v.x : 0u) + (wig > 1 ? v.y : 0u) + (wig > 2 ? v.z : 0u);
+            }
+            const uint32_t wtot = __shfl_sync(FULL, incl, 31);
+            const uint32_t lpos = incl - cnt;                                  // first output in the warp
+            const uint32_t wbeg = lo + wpre;                                   // the warp's first output
+
+            if (safe) {
+                // direct mode: compose and store to HBM per code
+                uint32_t p = wbeg + lpos;
+                const uint32_t pend = min(p + cnt, hi);
+#pragma unroll 1
+                for (int sub = 0; sub < 2; sub++) {
+                    uint32_t a, bb, c;
+                    if (sub) { a = W2; bb = W3; c = W4; shift96(a, bb, c, gapB); }
+                    else { a = W0; bb = W1; c = W2; shift96(a, bb, c, gapA); }
+                    uint32_t off = sub ? 64u + gapB : gapA;
+                    const uint32_t lim_off = sub ? 128u : 64u;
+                    while (p < pend && off < lim_off) {
+                        uint32_t el, eh, len, sym;
+                        lds64(madlo(mulhi(a, K_ROW), K_ENT, tab), el, eh);
+                        if (eh != 0) { sym = unrot8(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
+                        else sym = walk(a, len);
+                        out[p] = compose(sym, __ldg(ts.packed_sign_mantissa + p));
+                        p++;
+                        off += len;
+                        shift96_long(a, bb, c, len);
+                    }
+                }
+                continue;
+            }
+
+            // ---- this warp's output range and its sign/mantissa prefetch
+            const uint32_t F = wbeg & ~15u;                                    // region byte of e: e - F
+            const uint32_t ra = min(wbeg, hi), rb = min(wbeg + wtot, hi);
+            const uint32_t ga = vec_out ? (ra + 15) >> 4 : 0, gb = vec_out ? max(rb >> 4, ga) : 0;
+            const uint32_t ha = vec_out ? min(ga << 4, rb) : rb, tb = vec_out ? max(gb << 4, ha) : rb;
+            uint4 smA = make_uint4(0, 0, 0, 0), smB = make_uint4(0, 0, 0, 0);
+            if (ga + lane < gb) smA = __ldg(psm4 + ga + lane);
+            if (ga + lane + 32 < gb) smB = __ldg(psm4 + ga + lane + 32);
+            const uint32_t es = lane < 16 ? ra + lane : tb + (lane - 16);
+            const bool edge = vec_out && (lane < 16 ? es < ha : es < rb);
+            uint32_t sm1 = 0;
+            if (edge) sm1 = __ldg(ts.packed_sign_mantissa + es);
+
+            // ---- compaction of the slots into [F, ...) of the warp region (in place: load all first)
+            {
+                uint32_t wa[8], wb[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    wa[k] = lds32(slotA + 128u * k);
+                    wb[k] = lds32(slotB + 128u * k);
+                }
+                __syncwarp();
+                const uint32_t dA = sbase + wreg + (wbeg - F) + lpos, dB = dA + cntA;
+                compact_words(dA, wa, cntA);
+                compact_words(dB, wb, cntB);
+                __syncwarp();
+                compact_head(dA, wa[0], cntA);
+                compact_head(dB, wb[0], cntB);
+            }
+            __syncwarp();
+
+            // ---- per-warp merge of [ra, rb): compose BF16 and store
+            const uint8_t *ebf = sb + wreg;                                    // ebf[e - F]
+            if (edge) out[es] = compose_r(ebf[es - F], sm1);
+            auto merge16 = [&](uint32_t gi, const uint4 &sm) {
+                const uint32_t e0 = gi << 4;
+                const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - F));
+                uint4 o0, o1;
+                compose4r(ex.x, sm.x, o0.x, o0.y);
+                compose4r(ex.y, sm.y, o0.z, o0.w);
+                compose4r(ex.z, sm.z, o1.x, o1.y);
+                compose4r(ex.w, sm.w, o1.z, o1.w);
+                uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
+                dst[0] = o0;
+                dst[1] = o1;
+            };
+            uint32_t gi = ga + lane;
+            if (gi < gb) merge16(gi, smA);
+            gi += 32;
+            if (gi < gb) merge16(gi, smB);
+            for (gi += 32; gi < gb; gi += 32) merge16(gi, __ldg(psm4 + gi));
+            if (!vec_out)                                                      // unaligned output: scalar
+                for (uint32_t e = ra + lane; e < rb; e += 32)
+                    out[e] = compose_r(ebf[e - F], __ldg(ts.packed_sign_mantissa + e));
+        }
+        seg_begin = seg_end;
+    }
+#undef K_ROW
+#undef K_ENT
+#undef K_S8
+#undef K_S16
+#undef K_S24
+}
+
+int g_sp12_attr_set[64];
+
+}  // namespace
+
+cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches) {
+    if (bt.total_tiles == 0) return cudaSuccess;
+    int num_sms = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return e;
+    if (device >= 0 && device < 64 && !g_sp12_attr_set[device]) {
+        e = cudaFuncSetAttribute(sp12_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem12);
+        if (e != cudaSuccess) return e;
+        g_sp12_attr_set[device] = 1;
+    }
+    const uint32_t grid = bt.grid ? bt.grid
+                                  : min((uint32_t)num_sms, (bt.total_tiles + kGroups12 - 1) / kGroups12);
+    sp12_kernel<<<grid, kCta12, kSmem12, stream>>>(bt);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+}  // namespace df11

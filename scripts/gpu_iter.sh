@@ -16,6 +16,6 @@ timeout 600 python bench.py --steps 400 --warmup 10 --no-cpu-baseline 2>&1 | tai
 } > gpurun_out/${TAG}.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 12 --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --kernel fast --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"(fast|sp)_kernel" -s 2 -c 1 -o gpurun_out/${TAG}_prof \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"(fast|sp|sp12)_kernel" -s 2 -c 1 -o gpurun_out/${TAG}_prof \
   python bench.py --kernel fast --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu.log 2>&1
 tail -8 gpurun_out/${TAG}.log
