@@ -51,9 +51,13 @@ constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengt
 constexpr uint32_t kOffWsum = kOffRLen + 256;                       // [groups][2][warps]
 constexpr uint32_t kOffReg = kOffWsum + kGroups12 * 2 * kWarps12 * 4;
 constexpr uint32_t kOffStage = kOffReg + kGroups12 * kWarps12 * kWarpReg12;
-constexpr uint32_t kOffMbar = kOffStage + kGroups12 * kStageBytes;
-constexpr uint32_t kSmem12 = kOffMbar + kGroups12 * 8;
-static_assert(kOffReg % 16 == 0 && kWarpReg12 % 16 == 0 && kOffStage % 16 == 0 && kOffMbar % 8 == 0,
+constexpr uint32_t kSmCap = 7168;           // PackedSignMantissa bytes of one tile staged in SMEM
+constexpr uint32_t kOffSm = kOffStage + kGroups12 * kStageBytes;    // [groups][kSmCap]
+constexpr uint32_t kOffCnt = kOffSm + kGroups12 * kSmCap;          // [groups] warps done with the merge
+constexpr uint32_t kOffMbar = kOffCnt + kGroups12 * 4;             // [groups][stage, sign/mantissa]
+constexpr uint32_t kSmem12 = kOffMbar + kGroups12 * 16;
+static_assert(kOffReg % 16 == 0 && kWarpReg12 % 16 == 0 && kOffStage % 16 == 0 && kOffSm % 16 == 0 &&
+                  kOffMbar % 8 == 0,
               "alignment");
 static_assert(kSmem12 <= 232448, "SMEM budget");
 
@@ -165,7 +169,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     const uint32_t wreg = kOffReg + (g * kWarps12 + wig) * kWarpReg12;   // this warp's region (byte offset)
     uint32_t *wsum = smem_w + kOffWsum / 4 + g * 2 * kWarps12;
     const uint32_t stage = sbase + kOffStage + g * kStageBytes;
-    const uint32_t mbar = sbase + kOffMbar + g * 8;
+    const uint32_t mbar = sbase + kOffMbar + g * 16;
+    const uint32_t smbar = mbar + 8;                        // the tile's PackedSignMantissa has landed
+    const uint32_t smb = sbase + kOffSm + g * kSmCap;
+    uint32_t *mcnt = smem_w + kOffCnt / 4 + g;
     const uint32_t slotA = sbase + wreg + 16u + lane * 4u, slotB = slotA + kSubW * 128u;
     const uint32_t rlenb = sbase + kOffRLen;
 
@@ -175,10 +182,12 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     if (c_begin >= c_end) return;
     if (t == 0) {
         mbar_init(mbar, 1);
+        mbar_init(smbar, 1);
+        *mcnt = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < 4) smem_w[(kOffT + kRows * 8u) / 4 + tid] = 0;
-    uint32_t q = 0, parity = 0;
+    uint32_t q = 0, parity = 0, qs = 0;
 
     int ti_idx = tensor_of_tile(bt, c_begin);
     for (uint32_t seg_begin = c_begin; seg_begin < c_end; ti_idx++) {
@@ -238,11 +247,26 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             nlo = __ldg(ts.block_output_pos + tile - base_tile);
             nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
         }
-        auto prefetch_sm = [&](uint32_t plo, uint32_t phi) {
-            const uint32_t a0 = min(plo, N) & ~15u, a1 = (min(max(phi, plo), N) + 15u) & ~15u;
-            if (a1 > a0) prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
+        // PackedSignMantissa of a tile, [a0, a1) = its output range widened to 16 bytes, is staged in
+        // SMEM by one TMA bulk copy (issued by the last warp to finish the previous tile's merge) when
+        // it fits kSmCap; otherwise it is prefetched into L2 and read with LDG in the merge.
+        const bool sm_tma = vec_out && !safe && (reinterpret_cast<uintptr_t>(ts.packed_sign_mantissa) & 15) == 0;
+        auto sm_range = [&](uint32_t plo, uint32_t phi, uint32_t &a0, uint32_t &a1) {
+            const uint32_t l = min(plo, N), h = min(max(min(phi, N), l), l + 8 * kN * kT);
+            a0 = l & ~15u;
+            a1 = (h + 15u) & ~15u;
+            return sm_tma && a1 > a0 && a1 - a0 <= kSmCap;
         };
-        if (t == 0 && tile < seg_end) prefetch_sm(nlo, nhi);
+        auto stage_sm = [&](uint32_t plo, uint32_t phi) {
+            uint32_t a0, a1;
+            if (sm_range(plo, phi, a0, a1)) {
+                mbar_expect_tx(smbar, a1 - a0);
+                tma_g2s(smb, ts.packed_sign_mantissa + a0, a1 - a0, smbar);
+            } else if (a1 > a0) {
+                prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
+            }
+        };
+        if (t == 0 && tile < seg_end) stage_sm(nlo, nhi);
         for (; tile < seg_end; tile += kGroups12, q++) {
             const uint32_t b = tile - base_tile;
             const uint32_t clo = nlo, chi = nhi;
@@ -385,10 +409,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             if (lane == 31) ws[wig] = incl;
             group_bar(g);                          // also: every thread has read this tile's stage
             parity ^= 1u;
-            if (t == 0 && has_next) {
-                issue_tile(ts, b + kGroups12, stage, mbar);
-                prefetch_sm(nlo, nhi);
-            }
+            if (t == 0 && has_next) issue_tile(ts, b + kGroups12, stage, mbar);
             uint32_t wpre = 0;
             {
                 const uint4 v = *reinterpret_cast<const uint4 *>(ws);
@@ -423,18 +444,13 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 continue;
             }
 
-            // ---- this warp's output range and its sign/mantissa prefetch
+            // ---- this warp's output range
             const uint32_t F = wbeg & ~15u;                                    // region byte of e: e - F
             const uint32_t ra = min(wbeg, hi), rb = min(wbeg + wtot, hi);
             const uint32_t ga = vec_out ? (ra + 15) >> 4 : 0, gb = vec_out ? max(rb >> 4, ga) : 0;
             const uint32_t ha = vec_out ? min(ga << 4, rb) : rb, tb = vec_out ? max(gb << 4, ha) : rb;
-            uint4 smA = make_uint4(0, 0, 0, 0), smB = make_uint4(0, 0, 0, 0);
-            if (ga + lane < gb) smA = __ldg(psm4 + ga + lane);
-            if (ga + lane + 32 < gb) smB = __ldg(psm4 + ga + lane + 32);
             const uint32_t es = lane < 16 ? ra + lane : tb + (lane - 16);
             const bool edge = vec_out && (lane < 16 ? es < ha : es < rb);
-            uint32_t sm1 = 0;
-            if (edge) sm1 = __ldg(ts.packed_sign_mantissa + es);
 
             // ---- compaction of the slots into [F, ...) of the warp region (in place: load all first)
             {
@@ -456,27 +472,56 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 
             // ---- per-warp merge of [ra, rb): compose BF16 and store
             const uint8_t *ebf = sb + wreg;                                    // ebf[e - F]
-            if (edge) out[es] = compose_r(ebf[es - F], sm1);
-            auto merge16 = [&](uint32_t gi, const uint4 &sm) {
-                const uint32_t e0 = gi << 4;
-                const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - F));
-                uint4 o0, o1;
-                compose4r(ex.x, sm.x, o0.x, o0.y);
-                compose4r(ex.y, sm.y, o0.z, o0.w);
-                compose4r(ex.z, sm.z, o1.x, o1.y);
-                compose4r(ex.w, sm.w, o1.z, o1.w);
-                uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
-                dst[0] = o0;
-                dst[1] = o1;
-            };
-            uint32_t gi = ga + lane;
-            if (gi < gb) merge16(gi, smA);
-            gi += 32;
-            if (gi < gb) merge16(gi, smB);
-            for (gi += 32; gi < gb; gi += 32) merge16(gi, __ldg(psm4 + gi));
-            if (!vec_out)                                                      // unaligned output: scalar
-                for (uint32_t e = ra + lane; e < rb; e += 32)
-                    out[e] = compose_r(ebf[e - F], __ldg(ts.packed_sign_mantissa + e));
+            uint32_t a0, a1;
+            if (sm_range(lo, hi, a0, a1)) {
+                mbar_wait(smbar, qs & 1u);                                     // PackedSignMantissa staged
+                qs++;
+                if (edge) out[es] = compose_r(ebf[es - F], ld8(smb + (es - a0)));
+                for (uint32_t gi = ga + lane; gi < gb; gi += 32) {
+                    const uint32_t e0 = gi << 4;
+                    uint4 sm;
+                    lds128(smb + (e0 - a0), sm.x, sm.y, sm.z, sm.w);
+                    const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - F));
+                    uint4 o0, o1;
+                    compose4r(ex.x, sm.x, o0.x, o0.y);
+                    compose4r(ex.y, sm.y, o0.z, o0.w);
+                    compose4r(ex.z, sm.z, o1.x, o1.y);
+                    compose4r(ex.w, sm.w, o1.z, o1.w);
+                    uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
+                    dst[0] = o0;
+                    dst[1] = o1;
+                }
+                // the last warp done with this tile's buffer stages the group's next tile into it
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    if (atomicAdd(mcnt, 1u) == kWarps12 - 1) {
+                        *mcnt = 0;
+                        __threadfence_block();
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        if (has_next) stage_sm(nlo, nhi);
+                    }
+                }
+            } else {
+                if (edge) out[es] = compose_r(ebf[es - F], __ldg(ts.packed_sign_mantissa + es));
+                for (uint32_t gi = ga + lane; gi < gb; gi += 32) {
+                    const uint32_t e0 = gi << 4;
+                    const uint4 sm = __ldg(psm4 + gi);
+                    const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - F));
+                    uint4 o0, o1;
+                    compose4r(ex.x, sm.x, o0.x, o0.y);
+                    compose4r(ex.y, sm.y, o0.z, o0.w);
+                    compose4r(ex.z, sm.z, o1.x, o1.y);
+                    compose4r(ex.w, sm.w, o1.z, o1.w);
+                    uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
+                    dst[0] = o0;
+                    dst[1] = o1;
+                }
+                if (!vec_out)                                                  // unaligned output: scalar
+                    for (uint32_t e = ra + lane; e < rb; e += 32)
+                        out[e] = compose_r(ebf[e - F], __ldg(ts.packed_sign_mantissa + e));
+                if (t == 0 && has_next) stage_sm(nlo, nhi);
+            }
         }
         seg_begin = seg_end;
     }
