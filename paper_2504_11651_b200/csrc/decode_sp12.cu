@@ -33,7 +33,10 @@ namespace {
 #endif
 constexpr int kFirst = SP12_FIRST;          // decode steps before the first warp check
 constexpr int kEach = SP12_EACH;            // decode steps between later warp checks
-constexpr uint32_t kGroups12 = 8;
+#ifndef SP12_GROUPS
+#define SP12_GROUPS 8
+#endif
+constexpr uint32_t kGroups12 = SP12_GROUPS;
 constexpr uint32_t kCta12 = kLanes * kGroups12;
 constexpr uint32_t kWarps12 = kLanes / 32;
 constexpr uint32_t kR = 12;                 // root bits of T12
@@ -54,7 +57,7 @@ constexpr uint32_t kOffStage = kOffReg + kGroups12 * kWarps12 * kWarpReg12;
 constexpr uint32_t kSmCap = 7168;           // PackedSignMantissa bytes of one tile staged in SMEM
 constexpr uint32_t kOffSm = kOffStage + kGroups12 * kStageBytes;    // [groups][kSmCap]
 constexpr uint32_t kOffCnt = kOffSm + kGroups12 * kSmCap;          // [groups] warps done with the merge
-constexpr uint32_t kOffMbar = kOffCnt + kGroups12 * 4;             // [groups][stage, sign/mantissa]
+constexpr uint32_t kOffMbar = kOffCnt + kGroups12 * 8;             // [groups][stage, sign/mantissa]
 constexpr uint32_t kSmem12 = kOffMbar + kGroups12 * 16;
 static_assert(kOffReg % 16 == 0 && kWarpReg12 % 16 == 0 && kOffStage % 16 == 0 && kOffSm % 16 == 0 &&
                   kOffMbar % 8 == 0,

@@ -54,7 +54,7 @@ def _check_oracle_format(df11, oracle_mod, w, kernel, **kw):
 @pytest.mark.parametrize("case", ["gauss_1m", "gauss_ragged", "constant_1bit", "two_symbol", "all_patterns_wide",
                                   "overflow_wide", "fibonacci_32bit", "one_element", "tiny_17", "sigma_large",
                                   "random_bits", "escape_heavy", "escape_deep", "uniform8_short_codes",
-                                  "one_bit_with_tail"])
+                                  "one_bit_with_tail", "maxlen_12", "maxlen_13", "four_symbol_2bit"])
 def test_parity_cases(df11, oracle_mod, kernel, case):
     if case == "gauss_1m":
         w = workloads.gaussian_bf16((1 << 20,), seed=1)
@@ -94,6 +94,26 @@ def test_parity_cases(df11, oracle_mod, kernel, case):
         counts = {127: 600000}
         counts.update({e: max(1, int(50000 * 0.6 ** i)) for i, e in enumerate(range(100, 127))})
         w = workloads.from_exponent_histogram(counts, seed=10)
+    elif case == "maxlen_12" or case == "maxlen_13":
+        # geometric exponent distribution whose longest code is exactly 12 (every code fits the
+        # 12-bit decode table: chain ends are found by walking back) or 13 bits (the all-ones row
+        # is an escape: exact chain ends through one-bit sentinels)
+        L = 12 if case == "maxlen_12" else 13
+        from oracle import huffman
+        for r in np.linspace(0.76, 0.90, 300):
+            counts = {90 + i: max(1, int(200000 * r ** i)) for i in range(40)}
+            h = np.zeros(256, np.int64)
+            for e, c in counts.items():
+                h[e] = c
+            if max(huffman.code_lengths(h)) == L:
+                break
+        else:
+            pytest.fail("no histogram with the requested maximum code length")
+        w = workloads.from_exponent_histogram(counts, seed=11)
+    elif case == "four_symbol_2bit":
+        # four equally likely exponents: 2-bit codes, 8192 outputs per format block, more than the
+        # kernel stages in SMEM per tile (its PackedSignMantissa is read from global memory instead)
+        w = workloads.from_exponent_histogram({110 + i: 60000 for i in range(4)}, seed=12)
     elif case == "escape_deep":
         # geometric tail: codes up to ~26 bits, some beyond the second level (walk path)
         counts = {e: max(1, int(400000 * 0.72 ** i)) for i, e in enumerate(range(60, 200))}
