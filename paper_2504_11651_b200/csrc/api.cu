@@ -147,8 +147,8 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
         bt.tile_start[bt.count] = pos;
         bt.total_tiles = pos;
         bt.grid = G;
-        const uint32_t kpow[10] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7,
-                                   1u << 12, 8u};
+        const uint32_t kpow[12] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7,
+                                   1u << 12, 8u, 1u << 9, 128u};
         std::memcpy(bt.kpow, kpow, sizeof(kpow));
 #ifdef DF11_TWO_PASS
         e = df11::launch_fast(bt, dev, stream, &g_launches);    // two decode passes (decode_fast.cu)

@@ -21,7 +21,7 @@ struct Batch {
     uint32_t grid;                             // CTAs the launcher will use (fast kernel)
     // powers of two used as IMAD multipliers (field extraction on the FMA pipe); read from the
     // constant bank so the compiler cannot strength-reduce them into ALU shifts (set by the launcher)
-    uint32_t kpow[10];
+    uint32_t kpow[12];
 };
 
 // Tensor owning global tile `g` (binary search over tile_start).

@@ -39,22 +39,39 @@ constexpr int kEach = SP12_EACH;            // decode steps between later warp c
 constexpr uint32_t kGroups12 = SP12_GROUPS;
 constexpr uint32_t kCta12 = kLanes * kGroups12;
 constexpr uint32_t kWarps12 = kLanes / 32;
+#ifdef SP12_R9
+// 9-bit table replicated 16x: replica j lives in bank pair j, lane l reads replica l % 16, so the two
+// half-warp passes of an LDS.64 are conflict-free (2 wavefronts); 3.1 codes per lookup
+constexpr uint32_t kR = 9;
+constexpr uint32_t kRep = 16;
+constexpr uint32_t kEscRows = 4;            // escape rows with a second-level table (next 9 bits)
+constexpr uint32_t kLutSmem = 0;            // the format LUTs are walked in global memory
+constexpr uint32_t kSubW = 10;              // slot words per chain: <= 32 codes + 4 + 1 (kEach = 1)
+#else
 constexpr uint32_t kR = 12;                 // root bits of T12
-constexpr uint32_t kRows = 1u << kR;
-constexpr uint32_t kCodes = 4;              // codes per entry
+constexpr uint32_t kRep = 1;
+constexpr uint32_t kEscRows = 0;
 constexpr uint32_t kLutSmem = 8192;
 constexpr uint32_t kSubW = 12;              // slot words per chain: <= 32 codes + overshoot
+#endif
+constexpr uint32_t kRows = 1u << kR;
+constexpr uint32_t kCodes = 4;              // codes per entry
 constexpr uint32_t kWarpReg12 = 16 + 2 * kSubW * 128;   // frame pad + lane-column slots of 2 chains
-constexpr uint32_t kXMask = (1u << 24) - 1u;
+constexpr uint32_t kXMask = 0xFFFFu;           // consumed bits (escape ids sit in bits 16-23)
 
-constexpr uint32_t kOffT = 0;                                       // uint2 [kRows] + null entry
-constexpr uint32_t kOffLut = kOffT + kRows * 8 + 16;
+constexpr uint32_t kOffT = 0;                                       // uint2 [kRows][kRep] + null entry
+constexpr uint32_t kOffEsc = kOffT + kRows * 8 * kRep + 16;         // uint16 [kEscRows][512] + bookkeeping
+constexpr uint32_t kOffLut = kOffEsc + kEscRows * 1024 + 32;
 constexpr uint32_t kOffLen = kOffLut + kLutSmem;                    // CodeLengths[e]
 constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengths[unrot(r)]
 constexpr uint32_t kOffWsum = kOffRLen + 256;                       // [groups][2][warps]
 constexpr uint32_t kOffReg = kOffWsum + kGroups12 * 2 * kWarps12 * 4;
 constexpr uint32_t kOffStage = kOffReg + kGroups12 * kWarps12 * kWarpReg12;
+#ifdef SP12_R9
+constexpr uint32_t kSmCap = 6656;           // PackedSignMantissa bytes of one tile staged in SMEM
+#else
 constexpr uint32_t kSmCap = 7168;           // PackedSignMantissa bytes of one tile staged in SMEM
+#endif
 constexpr uint32_t kOffSm = kOffStage + kGroups12 * kStageBytes;    // [groups][kSmCap]
 constexpr uint32_t kOffCnt = kOffSm + kGroups12 * kSmCap;          // [groups] warps done with the merge
 constexpr uint32_t kOffMbar = kOffCnt + kGroups12 * 8;             // [groups][stage, sign/mantissa]
@@ -160,15 +177,20 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     const uint32_t t = tid % kLanes;
     const uint32_t lane = tid & 31, wig = t >> 5;
     const uint32_t FULL = 0xFFFFFFFFu;
+#ifdef SP12_R9
+#define K_ROW bt.kpow[10]  // 2^9: a >> 23
+#define K_ENT bt.kpow[11]  // 128: row stride (16 replicas of 8 bytes)
+#else
 #define K_ROW bt.kpow[8]   // 2^12: a >> 20
 #define K_ENT bt.kpow[9]   // 8: entry bytes
+#endif
 #define K_S8 bt.kpow[3]    // 2^24: >> 8
 #define K_S16 bt.kpow[4]   // 2^16: >> 16
 #define K_S24 bt.kpow[2]   // 2^8: >> 24
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
-    const uint32_t tab = sbase + kOffT;
-    const uint32_t null_ent = sbase + kOffT + kRows * 8u;   // all-zero entry: advances nothing
+    const uint32_t tab = sbase + kOffT + (lane % kRep) * 8u;   // this lane's replica
+    const uint32_t null_ent = sbase + kOffT + kRows * 8u * kRep;   // all-zero entry: advances nothing
     const uint32_t wreg = kOffReg + (g * kWarps12 + wig) * kWarpReg12;   // this warp's region (byte offset)
     uint32_t *wsum = smem_w + kOffWsum / 4 + g * 2 * kWarps12;
     const uint32_t stage = sbase + kOffStage + g * kStageBytes;
@@ -189,7 +211,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         *mcnt = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < 4) smem_w[(kOffT + kRows * 8u) / 4 + tid] = 0;
+    if (tid < 4) smem_w[(kOffT + kRows * 8u * kRep) / 4 + tid] = 0;
     uint32_t q = 0, parity = 0, qs = 0;
 
     int ti_idx = tensor_of_tile(bt, c_begin);
@@ -217,6 +239,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             return lut_walk_global(w, ts, len);
         };
         bool row_esc_last = false;
+        uint32_t *esc_n = smem_w + (kOffEsc + kEscRows * 1024) / 4, *esc_row = esc_n + 1;
+        if (kEscRows && tid == 0) *esc_n = 0;
+        if (kEscRows) __syncthreads();
         for (uint32_t row = tid; row < kRows; row += kCta12) {
             const uint32_t W = row << (32 - kR);
             uint32_t s = 0, syms = 0, c2 = 0;
@@ -228,8 +253,26 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 syms |= rot8(sym) << (8 * c2);
                 c2++;
             }
-            *reinterpret_cast<uint2 *>(sb + kOffT + row * 8u) = make_uint2(syms, s | (c2 << 27));
+            uint32_t hi = s | (c2 << 27);
+            if (kEscRows && c2 == 0) {               // escape row: second-level table id in hi[16:24)
+                const uint32_t id = atomicAdd(esc_n, 1u);
+                if (id < kEscRows) { esc_row[id] = row; hi = (id + 1) << 16; }
+            }
+#pragma unroll
+            for (uint32_t j = 0; j < kRep; j++)
+                *reinterpret_cast<uint2 *>(sb + kOffT + (row * kRep + j) * 8u) = make_uint2(syms, hi);
             if (row == kRows - 1) row_esc_last = c2 == 0;
+        }
+        if (kEscRows) {
+            __syncthreads();
+            const uint32_t n_esc = min(*esc_n, kEscRows);
+            uint16_t *l2 = reinterpret_cast<uint16_t *>(sb + kOffEsc);
+            for (uint32_t i = tid; i < (n_esc << 9); i += kCta12) {
+                const uint32_t row = esc_row[i >> 9], j = i & 511u;
+                uint32_t len;
+                const uint32_t sym = walk((row << (32 - kR)) | (j << (32 - kR - 9)), len);
+                l2[i] = len <= kR + 9 ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
+            }
         }
         // a 1-bit codeword allows 64 codes per chain: such tensors take the count + direct path
         const bool safe = __syncthreads_or(tid < 256u && sb[kOffLen + tid] == 1) != 0;
@@ -332,19 +375,35 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     if (!__any_sync(FULL, actA || actB)) break;
                     if (!actA) { tA = null_ent; aA = 0; }                      // freeze on the null entry
                     if (!actB) { tB = null_ent; aB = 0; }
-                    const bool escA = actA && hA == 0, escB = actB && hB == 0;
+                    const bool escA = actA && (hA & 0xFFFFu) == 0, escB = actB && (hB & 0xFFFFu) == 0;
                     if (__any_sync(FULL, escA || escB)) {
                         if (escA) {
-                            uint32_t len;
-                            const uint32_t sym = walk(aA, len);
-                            pack(rot8(sym), 8u << 24, accA, fA, wA, K_S24);
+                            uint32_t len, r = 0;
+                            if (kEscRows) {                       // second-level table (next 9 bits)
+                                const uint32_t id = hA >> 16;
+                                if (id != 0) {
+                                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r)
+                                                 : "r"(sbase + kOffEsc + (((id - 1) << 9) | ((aA >> (23 - kR)) & 511u)) * 2));
+                                    len = r >> 8;
+                                }
+                            }
+                            if ((r >> 8) == 0) r = rot8(walk(aA, len));
+                            pack(r & 0xFFu, 8u << 24, accA, fA, wA, K_S24);
                             xA += len;
                             shift96_long_ones(aA, bA, cA, len);
                         }
                         if (escB) {
-                            uint32_t len;
-                            const uint32_t sym = walk(aB, len);
-                            pack(rot8(sym), 8u << 24, accB, fB, wB, K_S24);
+                            uint32_t len, r = 0;
+                            if (kEscRows) {                       // second-level table (next 9 bits)
+                                const uint32_t id = hB >> 16;
+                                if (id != 0) {
+                                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r)
+                                                 : "r"(sbase + kOffEsc + (((id - 1) << 9) | ((aB >> (23 - kR)) & 511u)) * 2));
+                                    len = r >> 8;
+                                }
+                            }
+                            if ((r >> 8) == 0) r = rot8(walk(aB, len));
+                            pack(r & 0xFFu, 8u << 24, accB, fB, wB, K_S24);
                             xB += len;
                             shift96_long_ones(aB, bB, cB, len);
                         }
@@ -384,7 +443,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     while (off < lim) {
                         uint32_t el, eh, len;
                         lds64(madlo(mulhi(a, K_ROW), K_ENT, tab), el, eh);
-                        if (eh != 0) len = ld8(rlenb + (el & 0xFFu));
+                        if ((eh & 0xFFFFu) != 0) len = ld8(rlenb + (el & 0xFFu));
                         else walk(a, len);
                         n++;
                         off += len;
@@ -436,7 +495,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     while (p < pend && off < lim_off) {
                         uint32_t el, eh, len, sym;
                         lds64(madlo(mulhi(a, K_ROW), K_ENT, tab), el, eh);
-                        if (eh != 0) { sym = unrot8(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
+                        if ((eh & 0xFFFFu) != 0) { sym = unrot8(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
                         else sym = walk(a, len);
                         out[p] = compose(sym, __ldg(ts.packed_sign_mantissa + p));
                         p++;
