@@ -114,10 +114,21 @@ df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t coun
 /* ---- end-to-end from host memory --------------------------------------------------------------
  * df11_decompress_host: copies the host arrays of `h` into the caller-provided device staging
  * buffers described by `d` (same sizes as h's arrays), decodes into d->out and copies the BF16
- * result into `host_out` (N words; pinned memory recommended), all enqueued on `stream`.
+ * result into `host_out` (N words; pinned memory recommended; NULL = leave the result in d->out),
+ * all enqueued on `stream`.
  * Returns after enqueueing; synchronise the stream before reading host_out. */
 df11_status df11_decompress_host(const df11_host_tensor *h, const df11_device_tensor *d,
                                  uint16_t *host_out, void *stream);
+
+/* df11_decompress_host_block: df11_decompress_host for `count` tensors (a transformer block),
+ * pipelined over two caller-owned streams: the H2D copies and decode of tensor i+1 run on `stream`
+ * while the BF16 result of tensor i is copied back on `copy_stream` (PCIe is full duplex).  On return
+ * everything is enqueued and `stream` waits for the last copy, so synchronising `stream` suffices.
+ * host_outs[i] may be NULL for an empty tensor; copy_stream == stream degrades to sequential calls.
+ * Errors: as df11_decompress_host; DF11_E_CUDA for stream/event failures. */
+df11_status df11_decompress_host_block(const df11_host_tensor *hs, const df11_device_tensor *ds,
+                                       uint16_t *const *host_outs, uint32_t count, void *stream,
+                                       void *copy_stream);
 
 /* ---- device encoder (format P:97; Table `time` P:471-486) -------
  * The same bytes as df11_encode, produced on the GPU in three steps so that the caller owns every

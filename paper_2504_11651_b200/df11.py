@@ -25,7 +25,7 @@ MAX_BATCH = 64
 
 EXPORTED_SYMBOLS = ("df11_encode", "df11_encode_group", "df11_host_tensor_free", "df11_decompress",
                     "df11_decompress_block", "df11_decompress_block_ex", "df11_decompress_host",
-                    "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
+                    "df11_decompress_host_block", "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
                     "df11_launch_count", "df11_histogram_device", "df11_encode_plan_create",
                     "df11_encode_plan_free", "df11_encode_device")
 
@@ -98,12 +98,15 @@ def lib():
         L.df11_decompress_block.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P]
         L.df11_decompress_block_ex.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P, ctypes.c_int]
         L.df11_decompress_host.argtypes = [ctypes.POINTER(HostTensorC), ctypes.POINTER(DeviceTensorC), P, P]
+        L.df11_decompress_host_block.argtypes = [ctypes.POINTER(HostTensorC), ctypes.POINTER(DeviceTensorC),
+                                                 ctypes.POINTER(P), U32, P, P]
         L.df11_histogram_device.argtypes = [P, U64, P, P]
         L.df11_encode_plan_create.argtypes = [P, P, ctypes.POINTER(EncodeOpts), ctypes.POINTER(EncodePlanC)]
         L.df11_encode_plan_free.argtypes = [ctypes.POINTER(EncodePlanC)]
         L.df11_encode_device.argtypes = [P, ctypes.POINTER(EncodePlanC), ctypes.POINTER(DeviceBuffersC), P, U64, P]
         for f in ("df11_encode", "df11_encode_group", "df11_decompress", "df11_decompress_block",
-                  "df11_decompress_block_ex", "df11_decompress_host", "df11_histogram_device",
+                  "df11_decompress_block_ex", "df11_decompress_host", "df11_decompress_host_block",
+                  "df11_histogram_device",
                   "df11_encode_plan_create", "df11_encode_device"):
             getattr(L, f).restype = ctypes.c_int
         L.df11_status_string.argtypes = [ctypes.c_int]
@@ -364,6 +367,25 @@ def decompress_host(h: HostTensor, dt: DeviceTensor, host_out, stream=None):
     _check(lib().df11_decompress_host(ctypes.byref(h._c), ctypes.byref(c_d),
                                       ctypes.c_void_p(host_out.data_ptr()), _stream_ptr(stream)))
     return host_out
+
+
+def decompress_host_block(hs, dts, host_outs, stream=None, copy_stream=None):
+    """df11_decompress_host_block: the H2D + decode of tensor i+1 on `stream` overlap the D2H of tensor i
+    on `copy_stream`; synchronising `stream` covers the whole block.  `hs` are HostTensor-like objects
+    exposing a `_c` HostTensorC (pinned host arrays recommended)."""
+    import torch
+    n = len(hs)
+    if copy_stream is None:
+        copy_stream = torch.cuda.Stream()
+    H = (HostTensorC * n)()
+    D = (DeviceTensorC * n)()
+    O = (ctypes.c_void_p * n)()
+    for i, (h, dt, o) in enumerate(zip(hs, dts, host_outs)):
+        ctypes.memmove(ctypes.byref(H, i * ctypes.sizeof(HostTensorC)), ctypes.byref(h._c), ctypes.sizeof(HostTensorC))
+        D[i] = dt.descriptor()
+        O[i] = o.data_ptr() if o is not None else None
+    _check(lib().df11_decompress_host_block(H, D, O, n, _stream_ptr(stream), _stream_ptr(copy_stream)))
+    return host_outs
 
 
 # --------------------------------------------------------------------------- device encoder (NEXT-3)

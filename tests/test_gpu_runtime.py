@@ -34,3 +34,25 @@ def test_overlap_runner_bit_exact(prefetch):
     torch.cuda.synchronize()
     assert seen == list(range(5))
     assert torch.equal(y, y_ref)
+
+
+def test_decompress_host_block_pipelined():
+    """df11_decompress_host_block: H2D + decode on one stream, D2H overlapped on a second; the BF16
+    results in host memory equal the originals bit for bit (P:8 lossless), including an empty tensor."""
+    from paper_2504_11651_b200 import df11
+    dev = torch.device("cuda", 0)
+    # "big" has 2 654 format blocks: two chunks of the pipeline
+    shapes = [("q", (512, 1000)), ("empty", (0,)), ("k", (33, 4097)), ("big", (4096, 4096)), ("v", (3000, 700))]
+    ws = [workloads.gaussian_bf16(sh, workloads.seed_for("hb", 0, n)) if sh != (0,) else np.zeros(0, np.uint16)
+          for n, sh in shapes]
+    hs = [df11.encode(w) for w in ws]
+    dts = [df11.DeviceTensor(h, dev) for h in hs]
+    outs = [torch.empty(max(w.size, 1), dtype=torch.bfloat16, pin_memory=True) for w in ws]
+    for rep in range(2):                                  # twice: the staging buffers are reused
+        for o in outs:
+            o.fill_(0)
+        df11.decompress_host_block(hs, dts, outs, copy_stream=torch.cuda.Stream(dev))
+        torch.cuda.current_stream(dev).synchronize()
+        for w, o in zip(ws, outs):
+            got = o[: w.size].view(torch.int16).numpy().view(np.uint16)
+            assert np.array_equal(got, w.reshape(-1))
