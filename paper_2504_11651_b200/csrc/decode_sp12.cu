@@ -228,29 +228,74 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         const bool lut_in_smem = lut_bytes <= kLutSmem;
         if (lut_in_smem)
             for (uint32_t i = tid; i < lut_bytes; i += kCta12) sb[kOffLut + i] = __ldg(ts.luts + i);
+        uint32_t len_t = 0;
         if (tid < 256u) {
-            const uint32_t l = __ldg(ts.code_lengths + tid);
-            sb[kOffLen + tid] = (uint8_t)l;
-            sb[kOffRLen + rot8(tid)] = (uint8_t)(l ? l : 32u);
+            len_t = __ldg(ts.code_lengths + tid);
+            sb[kOffLen + tid] = (uint8_t)len_t;
+            sb[kOffRLen + rot8(tid)] = (uint8_t)(len_t ? len_t : 32u);
         }
-        __syncthreads();
+        // a 1-bit codeword allows 64 codes per chain: such tensors take the count + direct path
+        const bool safe = __syncthreads_or(len_t == 1) != 0;
+
+        const uint32_t N = (uint32_t)ts.num_elements;
+        const bool vec_out = ((reinterpret_cast<uintptr_t>(ts.out) & 15) == 0);
+        const uint4 *__restrict__ psm4 = reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa);
+        uint16_t *__restrict__ out = ts.out;
+        // PackedSignMantissa of a tile, [a0, a1) = its output range widened to 16 bytes, is staged in
+        // SMEM by one TMA bulk copy (issued by the last warp to finish the previous tile's merge) when
+        // it fits kSmCap; otherwise it is prefetched into L2 and read with LDG in the merge.
+        const bool sm_tma = vec_out && !safe && (reinterpret_cast<uintptr_t>(ts.packed_sign_mantissa) & 15) == 0;
+        auto sm_range = [&](uint32_t plo, uint32_t phi, uint32_t &a0, uint32_t &a1) {
+            const uint32_t l = min(plo, N), h = min(max(min(phi, N), l), l + 8 * kN * kT);
+            a0 = l & ~15u;
+            a1 = (h + 15u) & ~15u;
+            return sm_tma && a1 > a0 && a1 - a0 <= kSmCap;
+        };
+        auto stage_sm = [&](uint32_t plo, uint32_t phi) {
+            uint32_t a0, a1;
+            if (sm_range(plo, phi, a0, a1)) {
+                mbar_expect_tx(smbar, a1 - a0);
+                tma_g2s(smb, ts.packed_sign_mantissa + a0, a1 - a0, smbar);
+            } else if (a1 > a0) {
+                prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
+            }
+        };
+        // each group's first tile: its copies are in flight while the table is built
+        uint32_t tile = seg_begin + g;
+        uint32_t nlo = 0, nhi = 0;
+        if (tile < seg_end) {
+            nlo = __ldg(ts.block_output_pos + tile - base_tile);
+            nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
+            if (t == 0) {
+                issue_tile(ts, tile - base_tile, stage, mbar);
+                stage_sm(nlo, nhi);
+            }
+        }
+
         auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
             if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, len);
             return lut_walk_global(w, ts, len);
         };
+        // first code of every kR-bit prefix (rotated exponent | length << 8; 0 = longer than kR bits),
+        // in the idle warp regions; an entry then chains up to kCodes of these: the code starting s bits
+        // into the row is the first code of the zero-padded prefix row << s if it fits in kR - s bits
+        uint16_t *fc = reinterpret_cast<uint16_t *>(sb + kOffReg);
+        for (uint32_t row = tid; row < kRows; row += kCta12) {
+            uint32_t len;
+            const uint32_t sym = walk(row << (32 - kR), len);
+            fc[row] = len <= kR ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
+        }
         bool row_esc_last = false;
         uint32_t *esc_n = smem_w + (kOffEsc + kEscRows * 1024) / 4, *esc_row = esc_n + 1;
         if (kEscRows && tid == 0) *esc_n = 0;
-        if (kEscRows) __syncthreads();
+        __syncthreads();
         for (uint32_t row = tid; row < kRows; row += kCta12) {
-            const uint32_t W = row << (32 - kR);
             uint32_t s = 0, syms = 0, c2 = 0;
             while (s < kR && c2 < kCodes) {
-                uint32_t len;
-                const uint32_t sym = walk(W << s, len);
-                if (len > kR - s) break;
+                const uint32_t v = fc[(row << s) & (kRows - 1u)], len = v >> 8;
+                if (len == 0 || len > kR - s) break;
                 s += len;
-                syms |= rot8(sym) << (8 * c2);
+                syms |= (v & 0xFFu) << (8 * c2);
                 c2++;
             }
             uint32_t hi = s | (c2 << 27);
@@ -274,45 +319,11 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 l2[i] = len <= kR + 9 ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
             }
         }
-        // a 1-bit codeword allows 64 codes per chain: such tensors take the count + direct path
-        const bool safe = __syncthreads_or(tid < 256u && sb[kOffLen + tid] == 1) != 0;
-        // if 12 one-bits hold no complete code (true for canonical codes longer than 12 bits), one-bits
+        // if kR one-bits hold no complete code (true for canonical codes longer than kR bits), one-bits
         // after a chain's last bit stall it exactly there
         const bool long_codes = __syncthreads_or(row_esc_last) != 0;
 
-        const uint32_t N = (uint32_t)ts.num_elements;
-        const bool vec_out = ((reinterpret_cast<uintptr_t>(ts.out) & 15) == 0);
-        const uint4 *__restrict__ psm4 = reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa);
-        uint16_t *__restrict__ out = ts.out;
-
         // =============================== tiles of this group
-        uint32_t tile = seg_begin + g;
-        if (t == 0 && tile < seg_end) issue_tile(ts, tile - base_tile, stage, mbar);
-        uint32_t nlo = 0, nhi = 0;
-        if (tile < seg_end) {
-            nlo = __ldg(ts.block_output_pos + tile - base_tile);
-            nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
-        }
-        // PackedSignMantissa of a tile, [a0, a1) = its output range widened to 16 bytes, is staged in
-        // SMEM by one TMA bulk copy (issued by the last warp to finish the previous tile's merge) when
-        // it fits kSmCap; otherwise it is prefetched into L2 and read with LDG in the merge.
-        const bool sm_tma = vec_out && !safe && (reinterpret_cast<uintptr_t>(ts.packed_sign_mantissa) & 15) == 0;
-        auto sm_range = [&](uint32_t plo, uint32_t phi, uint32_t &a0, uint32_t &a1) {
-            const uint32_t l = min(plo, N), h = min(max(min(phi, N), l), l + 8 * kN * kT);
-            a0 = l & ~15u;
-            a1 = (h + 15u) & ~15u;
-            return sm_tma && a1 > a0 && a1 - a0 <= kSmCap;
-        };
-        auto stage_sm = [&](uint32_t plo, uint32_t phi) {
-            uint32_t a0, a1;
-            if (sm_range(plo, phi, a0, a1)) {
-                mbar_expect_tx(smbar, a1 - a0);
-                tma_g2s(smb, ts.packed_sign_mantissa + a0, a1 - a0, smbar);
-            } else if (a1 > a0) {
-                prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
-            }
-        };
-        if (t == 0 && tile < seg_end) stage_sm(nlo, nhi);
         for (; tile < seg_end; tile += kGroups12, q++) {
             const uint32_t b = tile - base_tile;
             const uint32_t clo = nlo, chi = nhi;
