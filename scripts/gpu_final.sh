@@ -14,7 +14,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/$
 for c in matrix4096 llama70b_block flux_double_block flux_single_block; do
   timeout 600 python bench.py --config $c --steps 100 --warmup 5 --no-cpu-baseline --no-transfer >> gpurun_out/${TAG}_configs.jsonl 2>> gpurun_out/${TAG}_bench.err
 done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 12 --csv --log-file gpurun_out/${TAG}_launches.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline --no-transfer > /dev/null 2>&1
 bash scripts/gpu_prof_only.sh ${TAG}
 cat gpurun_out/${TAG}_tests.log; tail -c 600 gpurun_out/${TAG}_bench.jsonl; tail -c 300 gpurun_out/${TAG}_ref.jsonl
