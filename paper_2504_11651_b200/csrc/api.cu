@@ -5,6 +5,7 @@
 // format parameters the fast kernel does not specialise go through the literal Algorithm 1 kernel
 // (decode_alg1.cu), one launch per distinct T.
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -120,7 +121,11 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
             (ts[i].B < kSmall ? small[nsmall++] : big[nbig++]) = i;
             total += ts[i].B;
         }
-        const uint32_t G = df11::fast_grid(total, num_sms);
+        uint32_t G = df11::fast_grid(total, num_sms);
+        // DF11_MAX_GRID (debug knob, read once): cap the persistent grid, e.g. so that a small input
+        // walks many tiles per group under compute-sanitizer
+        static const int max_grid = [] { const char *v = std::getenv("DF11_MAX_GRID"); return v ? std::atoi(v) : 0; }();
+        if (max_grid > 0) G = std::min<uint32_t>(G, (uint32_t)max_grid);
         auto boundary = [&](uint32_t c) { return (uint32_t)(((uint64_t)total * c) / G); };
         uint32_t pos = 0, bi = 0, boff = 0;
         auto push = [&](uint32_t ti, uint32_t off, uint32_t n) {

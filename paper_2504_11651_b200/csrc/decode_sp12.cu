@@ -594,6 +594,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     for (uint32_t e = ra + lane; e < rb; e += 32)
                         out[e] = compose_r(ebf[e - F], __ldg(ts.packed_sign_mantissa + e));
                 if (t == 0 && has_next) stage_sm(nlo, nhi);
+                __syncwarp();                  // the region's reads are done before the next tile's slots
             }
         }
         seg_begin = seg_end;

@@ -12,7 +12,10 @@ from paper_2504_11651_b200 import df11  # noqa: E402
 
 cases = [workloads.gaussian_bf16((150001,), seed=1), workloads.constant(40000),
          workloads.from_exponent_histogram({e: max(1, int(40000 * 0.72 ** i)) for i, e in enumerate(range(60, 200))}, 3),
-         workloads.all_bf16_patterns()]
+         workloads.all_bf16_patterns(),
+         workloads.from_exponent_histogram({110 + i: 20000 for i in range(4)}, seed=12),      # 2-bit codes
+         workloads.from_exponent_histogram({e: max(1, int(200000 * 0.829 ** i)) for i, e in enumerate(range(90, 130))}, 11)]
+# run with DF11_MAX_GRID=2: every group walks several tiles (stage/sign-mantissa refills, tensor switches)
 kernels = sys.argv[1:] or ["fast", "alg1"]
 for kernel in kernels:
     dts = [df11.to_device(df11.encode(w)) for w in cases]
