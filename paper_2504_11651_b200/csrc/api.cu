@@ -152,6 +152,31 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
         bt.tile_start[bt.count] = pos;
         bt.total_tiles = pos;
         bt.grid = G;
+        // Per-CTA tile ranges of equal work, where an entry (tensor) start inside a CTA's range costs
+        // kSwitchTiles tiles of work (the CTA rebuilds its decode table and restarts its copies there):
+        // CTAs that switch tensors get fewer tiles.  W(x) = x + kSwitchTiles * #{entry starts <= x};
+        // boundary c is the first x with W(x) >= c * W(total) / G, so it snaps to an entry start when
+        // the target falls inside that start's jump.
+        if (G <= (uint32_t)df11::kMaxCta) {
+#ifndef DF11_SWITCH_TILES
+#define DF11_SWITCH_TILES 3
+#endif
+            constexpr uint64_t kSwitchTiles = DF11_SWITCH_TILES;
+            const uint64_t wtot = (uint64_t)total + kSwitchTiles * (bt.count - 1);
+            uint32_t ei = 1;                                // next entry start not yet counted
+            for (uint32_t c = 0; c <= G; c++) {
+                const uint64_t target = wtot * c / G;
+                while (ei < bt.count && (uint64_t)bt.tile_start[ei] + kSwitchTiles * ei <= target) ei++;
+                // entries 1..ei-1 have W(start) <= target; x = target - P*(ei-1), clamped to the
+                // next entry start (inside its jump)
+                uint64_t x = target - kSwitchTiles * (ei - 1);
+                if (ei < bt.count) x = std::min<uint64_t>(x, bt.tile_start[ei]);
+                bt.cta_start[c] = (uint32_t)std::min<uint64_t>(x, total);
+            }
+            bt.cta_start[0] = 0;
+            bt.cta_start[G] = total;
+            bt.cta_ranges = 1;
+        }
         const uint32_t kpow[12] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7,
                                    1u << 12, 8u, 1u << 9, 128u};
         std::memcpy(bt.kpow, kpow, sizeof(kpow));

@@ -11,6 +11,7 @@ namespace df11 {
 // within a transformer block as a single batch").  Passed by value as a __grid_constant__ kernel
 // parameter: no workspace, no H2D copy, graph-capturable.
 constexpr int kMaxEntries = 2 * DF11_MAX_BATCH;   // a tensor may be split into several tile ranges
+constexpr int kMaxCta = 256;                      // persistent grid bound for per-CTA tile ranges
 
 struct Batch {
     df11_device_tensor t[kMaxEntries];
@@ -19,6 +20,8 @@ struct Batch {
     uint32_t count;
     uint32_t total_tiles;
     uint32_t grid;                             // CTAs the launcher will use (fast kernel)
+    uint32_t cta_ranges;                       // 1: CTA c walks tiles [cta_start[c], cta_start[c+1])
+    uint32_t cta_start[kMaxCta + 1];
     // powers of two used as IMAD multipliers (field extraction on the FMA pipe); read from the
     // constant bank so the compiler cannot strength-reduce them into ALU shifts (set by the launcher)
     uint32_t kpow[12];

@@ -202,8 +202,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     const uint32_t rlenb = sbase + kOffRLen;
 
     const uint32_t total = bt.total_tiles;
-    const uint32_t c_begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
-    const uint32_t c_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
+    const uint32_t c_begin = bt.cta_ranges ? bt.cta_start[blockIdx.x]
+                                           : (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
+    const uint32_t c_end = bt.cta_ranges ? bt.cta_start[blockIdx.x + 1]
+                                         : (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
     if (c_begin >= c_end) return;
     if (t == 0) {
         mbar_init(mbar, 1);
