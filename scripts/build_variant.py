@@ -3,6 +3,7 @@
 (select it at run time with DF11_LIB=...).  Test tooling only; the product build is build.py.
 
     python scripts/build_variant.py NAME [-DFOO=1 ...]
+    DF11_SRC_OVERRIDE=decode_sp12.cu=/tmp/x.cu python scripts/build_variant.py NAME   (replace a source)
 """
 import os
 import subprocess
@@ -20,8 +21,10 @@ def main():
     os.makedirs(out_dir, exist_ok=True)
     os.makedirs(obj_dir, exist_ok=True)
     objs = []
+    override = dict(kv.split("=", 1) for kv in os.environ.get("DF11_SRC_OVERRIDE", "").split(",") if kv)
     for src in B._sources():
         obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
+        src = override.get(os.path.basename(src), src)          # e.g. decode_sp12.cu=/tmp/instrumented.cu
         if src.endswith(".cu"):
             cmd = [B.NVCC, *B.NVCC_FLAGS, *defs, "-c", src, "-o", obj]
         else:
