@@ -24,7 +24,8 @@ torch.cuda.synchronize()
 buf = np.zeros((148 * 32, 8), np.uint64)
 rc = df11.lib().df11_debug_sp12_prof(buf.ctypes.data_as(ctypes.c_void_p))
 assert rc == 0, rc
-names = ["merge+tail (prev tile)", "stage wait", "decode", "scan", "barrier", "compaction", "sm wait", "segment end"]
+names = ["merge+tail (prev tile)", "stage wait", "decode", "scan", "barrier", "range + slot loads",
+         "compaction stores+heads", "merge setup + sm wait"]
 tot = buf.astype(np.float64).sum(1)
 act = tot > 0
 print(f"{cfg}: warps {act.sum()}, mean cycles per warp {tot[act].mean():.0f}, max {tot.max():.0f}")
