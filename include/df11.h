@@ -111,6 +111,15 @@ df11_status df11_decompress_block(const df11_device_tensor *ts, uint32_t count, 
 df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream,
                                      int kernel);
 
+/* ---- launcher planning (host; used by df11_decompress_block, exported for tests) ----------------
+ * df11_plan_cta_ranges: tile ranges of the persistent decode grid.  entry_start[0..count] are the
+ * exclusive prefix sums of the batch entries' format-block counts (entry_start[count] = total);
+ * CTA c walks [cta_start[c], cta_start[c+1]) (cta_start has grid + 1 entries, non-decreasing,
+ * cta_start[0] = 0, cta_start[grid] = total).  Ranges have equal work, where an entry start strictly
+ * inside a range costs switch_tiles tiles (the CTA rebuilds its decode table there). */
+void df11_plan_cta_ranges(const uint32_t *entry_start, uint32_t count, uint32_t grid, uint32_t switch_tiles,
+                          uint32_t *cta_start);
+
 /* ---- end-to-end from host memory --------------------------------------------------------------
  * df11_decompress_host: copies the host arrays of `h` into the caller-provided device staging
  * buffers described by `d` (same sizes as h's arrays), decodes into d->out and copies the BF16

@@ -79,6 +79,27 @@ extern "C" df11_status df11_fail(df11_status st, const char *msg) {
     return st;
 }
 
+extern "C" void df11_plan_cta_ranges(const uint32_t *entry_start, uint32_t count, uint32_t grid,
+                                     uint32_t switch_tiles, uint32_t *cta_start) {
+    // W(x) = x + switch_tiles * #{entry starts e, 0 < e <= x}; boundary c is the first x with
+    // W(x) >= c * W(total) / grid, so a boundary snaps to an entry start when its target falls inside
+    // that start's jump, and a CTA whose range holds an entry start gets switch_tiles fewer tiles.
+    if (!grid) return;
+    const uint32_t total = count ? entry_start[count] : 0;
+    const uint64_t P = switch_tiles;
+    const uint64_t wtot = (uint64_t)total + P * (count ? count - 1 : 0);
+    uint32_t ei = 1;                                // next entry start not yet counted
+    for (uint32_t c = 0; c <= grid; c++) {
+        const uint64_t target = wtot * c / grid;
+        while (ei < count && (uint64_t)entry_start[ei] + P * ei <= target) ei++;
+        uint64_t x = target - P * (ei - 1);         // entries 1..ei-1 counted
+        if (ei < count) x = std::min<uint64_t>(x, entry_start[ei]);
+        cta_start[c] = (uint32_t)std::min<uint64_t>(x, total);
+    }
+    cta_start[0] = 0;
+    cta_start[grid] = total;
+}
+
 extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream_v,
                                                 int kernel) {
     if (count > DF11_MAX_BATCH) return df11_fail(DF11_E_INVALID_ARGUMENT, "count > DF11_MAX_BATCH");
@@ -152,31 +173,14 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
         bt.tile_start[bt.count] = pos;
         bt.total_tiles = pos;
         bt.grid = G;
-        // Per-CTA tile ranges of equal work, where an entry (tensor) start inside a CTA's range costs
-        // kSwitchTiles tiles of work (all 8 groups drain the previous segment at a CTA barrier, the
-        // decode table is rebuilt, the copies restart): CTAs that switch tensors get fewer tiles.
-        // kSwitchTiles = 12 measured best (3: +1.3 %, 8: +2.9 %, 12: +3.1 %, 16/24: +2.5 % on the
-        // Llama-8B block vs uniform ranges).  W(x) = x + kSwitchTiles * #{entry starts <= x};
-        // boundary c is the first x with W(x) >= c * W(total) / G, so it snaps to an entry start when
-        // the target falls inside that start's jump.
+        // Per-CTA tile ranges of equal work (df11_plan_cta_ranges): CTAs that switch tensors get fewer
+        // tiles.  A switch costs 12 tiles, measured best (3: +1.3 %, 8: +2.9 %, 12: +3.1 %, 16/24:
+        // +2.5 % on the Llama-8B block vs uniform ranges).
         if (G <= (uint32_t)df11::kMaxCta) {
 #ifndef DF11_SWITCH_TILES
 #define DF11_SWITCH_TILES 12
 #endif
-            constexpr uint64_t kSwitchTiles = DF11_SWITCH_TILES;
-            const uint64_t wtot = (uint64_t)total + kSwitchTiles * (bt.count - 1);
-            uint32_t ei = 1;                                // next entry start not yet counted
-            for (uint32_t c = 0; c <= G; c++) {
-                const uint64_t target = wtot * c / G;
-                while (ei < bt.count && (uint64_t)bt.tile_start[ei] + kSwitchTiles * ei <= target) ei++;
-                // entries 1..ei-1 have W(start) <= target; x = target - P*(ei-1), clamped to the
-                // next entry start (inside its jump)
-                uint64_t x = target - kSwitchTiles * (ei - 1);
-                if (ei < bt.count) x = std::min<uint64_t>(x, bt.tile_start[ei]);
-                bt.cta_start[c] = (uint32_t)std::min<uint64_t>(x, total);
-            }
-            bt.cta_start[0] = 0;
-            bt.cta_start[G] = total;
+            df11_plan_cta_ranges(bt.tile_start, bt.count, G, DF11_SWITCH_TILES, bt.cta_start);
             bt.cta_ranges = 1;
         }
         const uint32_t kpow[12] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7,

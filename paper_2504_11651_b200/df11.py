@@ -25,7 +25,7 @@ MAX_BATCH = 64
 
 EXPORTED_SYMBOLS = ("df11_encode", "df11_encode_group", "df11_host_tensor_free", "df11_decompress",
                     "df11_decompress_block", "df11_decompress_block_ex", "df11_decompress_host",
-                    "df11_decompress_host_block", "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
+                    "df11_decompress_host_block", "df11_plan_cta_ranges", "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
                     "df11_launch_count", "df11_histogram_device", "df11_encode_plan_create",
                     "df11_encode_plan_free", "df11_encode_device")
 
@@ -98,6 +98,8 @@ def lib():
         L.df11_decompress_block.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P]
         L.df11_decompress_block_ex.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P, ctypes.c_int]
         L.df11_decompress_host.argtypes = [ctypes.POINTER(HostTensorC), ctypes.POINTER(DeviceTensorC), P, P]
+        L.df11_plan_cta_ranges.argtypes = [P, U32, U32, U32, P]
+        L.df11_plan_cta_ranges.restype = None
         L.df11_decompress_host_block.argtypes = [ctypes.POINTER(HostTensorC), ctypes.POINTER(DeviceTensorC),
                                                  ctypes.POINTER(P), U32, P, P]
         L.df11_histogram_device.argtypes = [P, U64, P, P]

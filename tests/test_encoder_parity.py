@@ -132,3 +132,35 @@ def test_encoder_speed_8b_block():
     dt = time.perf_counter() - t
     assert h.num_elements == w.size
     assert w.size / dt > 50e6, w.size / dt
+
+
+def test_plan_cta_ranges_cover_and_balance():
+    """Launcher planning (row a9): the per-CTA tile ranges are non-decreasing, cover every tile
+    exactly once, and a CTA whose range holds a tensor start gets about `switch_tiles` fewer tiles."""
+    import ctypes
+    from paper_2504_11651_b200 import df11
+    rng = np.random.default_rng(3)
+    L = df11.lib()
+    for trial in range(200):
+        count = int(rng.integers(1, 20))
+        sizes = rng.integers(1, 5000, size=count)
+        if trial % 3 == 0:
+            sizes[rng.integers(0, count)] = int(rng.integers(1, 16))          # a small tensor
+        starts = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint32)
+        total = int(starts[-1])
+        grid = int(rng.integers(1, 200))
+        for P in (0, 12):
+            out = np.zeros(grid + 1, np.uint32)
+            L.df11_plan_cta_ranges(starts.ctypes.data_as(ctypes.c_void_p), count, grid, P,
+                                   out.ctypes.data_as(ctypes.c_void_p))
+            assert out[0] == 0 and out[-1] == total
+            assert np.all(np.diff(out.astype(np.int64)) >= 0)
+            if P == 0:          # plain equal split (rounding down)
+                assert np.array_equal(out, (np.arange(grid + 1, dtype=np.uint64) * total // grid).astype(np.uint32))
+            # work per CTA (tiles + P per interior entry start) differs by at most P + 1 across CTAs
+            work = []
+            for c in range(grid):
+                inner = int(np.sum((starts[1:-1] > out[c]) & (starts[1:-1] < out[c + 1])))
+                work.append(int(out[c + 1]) - int(out[c]) + P * inner)
+            if total >= grid * (P + 2):
+                assert max(work) - min(work) <= 2 * P + 2, (work, P)
