@@ -1,9 +1,10 @@
 // api.cu — the C ABI (include/df11.h): validation, kernel selection, launches, diagnostics.
 //
 // df11_decompress_block: all tensors of a transformer block are described in ONE
-// __grid_constant__ Batch and decoded by ONE launch of the fast kernel (decode_fast.cu).  Tensors whose
-// format parameters the fast kernel does not specialise go through the literal Algorithm 1 kernel
-// (decode_alg1.cu), one launch per distinct T.
+// __grid_constant__ Batch and decoded by ONE launch of the product kernel (decode_sp12.cu; the earlier
+// decode_fast.cu / decode_sp.cu kernels are selected only by A/B builds with -DDF11_TWO_PASS /
+// -DDF11_SP9).  Tensors whose format parameters it does not specialise (T = 256, n = 8) go through the
+// literal Algorithm 1 kernel (decode_alg1.cu), one launch per distinct T.
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>

@@ -7,7 +7,7 @@
 // What differs is the decode table and the byte format of the exponents between decode and merge:
 //
 //  * T12: 4096 entries of 8 bytes indexed by the next 12 bits of the stream.  An entry holds up to 4
-//    complete codes: lo = their exponents (one byte each), hi = consumed bits | count << 29.  12 bits
+//    complete codes: lo = their exponents (one byte each), hi = consumed bits | 8*count << 24.  12 bits
 //    decode 3.8 codes per lookup on LLM-like exponents vs 2.8 for a 9-bit, 3-code table, and codes
 //    longer than 12 bits (resolved by the paper's LUT walk) are 8x rarer.  The table is not
 //    lane-replicated (32 KB); its LDS.64 bank conflicts are the price of 1.35x fewer lookups.
@@ -18,8 +18,10 @@
 //    (funnel shifts use the low 5 bits), and the exponents are appended to the chain's slot through a
 //    pending word: m = acc | lo << fb is stored with ONE 32-bit STS, and the word pointer advances when
 //    the word is full.  Slots are lane-column-major (word k of lane l at k*128 + 4l), so every slot
-//    access of a warp hits 32 distinct banks.  hi = consumed | (8*count) << 24; x accumulates the
-//    consumed bits in its low 24 bits (the count garbage sits above).
+//    access of a warp hits 32 distinct banks.  x += hi accumulates the consumed bits in its low 16 bits
+//    (the count, and in the SP12_R9 variant an escape id in bits 16-23, sit above).
+//  * A tile's PackedSignMantissa range is staged in SMEM by one TMA bulk copy; the first tile's copies
+//    are issued before the table build; per-CTA tile ranges come from df11_plan_cta_ranges (api.cu).
 #include "fast_helpers.cuh"
 
 namespace df11 {
