@@ -542,8 +542,26 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 compact_words(dA, wa, cntA);
                 compact_words(dB, wb, cntB);
                 __syncwarp();
-                compact_head(dA, wa[0], cntA);
-                compact_head(dB, wb[0], cntB);
+#ifndef SP12_BYTE_HEADS
+                // first partial word of a chain: its low bytes already hold the previous chain's tail
+                // (that chain's last word, written above), so one read-modify-write completes it when
+                // every chain of the warp has >= 4 codes (then no word holds bytes of 3 chains)
+                if (!__any_sync(FULL, cntA < 4u || cntB < 4u)) {
+                    const uint32_t rA = dA & 3u, rB = dB & 3u;
+                    if (rA) {
+                        const uint32_t o = lds32(dA - rA);
+                        sts32(dA - rA, (o & ((1u << (8 * rA)) - 1u)) | (wa[0] << (8 * rA)));
+                    }
+                    if (rB) {
+                        const uint32_t o = lds32(dB - rB);
+                        sts32(dB - rB, (o & ((1u << (8 * rB)) - 1u)) | (wb[0] << (8 * rB)));
+                    }
+                } else
+#endif
+                {
+                    compact_head(dA, wa[0], cntA);
+                    compact_head(dB, wb[0], cntB);
+                }
             }
             __syncwarp();
 
