@@ -28,7 +28,7 @@ def main():
         if src.endswith(".cu"):
             cmd = [B.NVCC, *B.NVCC_FLAGS, *defs, "-c", src, "-o", obj]
         else:
-            cmd = ["g++", *B.CXX_FLAGS, *defs, "-c", src, "-o", obj]
+            cmd = ["g++", *B.CXX_FLAGS, *[d for d in defs if d.startswith("-D")], "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise SystemExit(r.stdout + r.stderr)
