@@ -271,7 +271,11 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(args.config, kernel_used), "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": algo_bytes,
-                "note": "achieved = (DF11 bytes read + BF16 bytes written) / mean launch time (CUDA events)"}
+                "frac_of_nominal_8tbs": achieved / 8000.0,
+                "launch_us": {"mean": avg_launch_ms * 1e3, "median": float(np.median(launch_ms)) * 1e3,
+                              "min": float(np.min(launch_ms)) * 1e3, "p90": float(np.percentile(launch_ms, 90)) * 1e3},
+                "note": "achieved = (DF11 bytes read + BF16 bytes written) / mean launch time (CUDA events); "
+                        "launch_us: this rank's per-launch CUDA-event times"}
 
     # ---- e2e: through the C ABI with host buffers (pinned H2D of the DF11 arrays, decode, D2H of BF16)
     e2e = None
