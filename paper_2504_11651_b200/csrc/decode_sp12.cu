@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         // PackedSignMantissa of a tile, [a0, a1) = its output range widened to 16 bytes, is staged in
         // SMEM by one TMA bulk copy (issued by the last warp to finish the previous tile's merge) when
         // it fits kSmCap; otherwise it is prefetched into L2 and read with LDG in the merge.
-        const bool sm_tma = vec_out && !safe && (reinterpret_cast<uintptr_t>(ts.packed_sign_mantissa) & 15) == 0;
+        const bool psm_al = (reinterpret_cast<uintptr_t>(ts.packed_sign_mantissa) & 15) == 0;   // bulk copies
+        const bool sm_tma = vec_out && !safe && psm_al;
         auto sm_range = [&](uint32_t plo, uint32_t phi, uint32_t &a0, uint32_t &a1) {
             const uint32_t l = min(plo, N), h = min(max(min(phi, N), l), l + 8 * kN * kT);
             a0 = l & ~15u;
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             if (sm_range(plo, phi, a0, a1)) {
                 mbar_expect_tx(smbar, a1 - a0);
                 tma_g2s(smb, ts.packed_sign_mantissa + a0, a1 - a0, smbar);
-            } else if (a1 > a0) {
+            } else if (a1 > a0 && psm_al) {
                 prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
             }
         };

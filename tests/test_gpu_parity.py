@@ -239,3 +239,23 @@ def test_full_size_llama8b_block(df11, oracle_mod, kernel):
     a = hs[-1].arrays()
     for key in ("code_lengths", "luts", "encoded_exponent", "packed_sign_mantissa", "gaps", "block_output_pos"):
         assert np.array_equal(a[key], fmt[key]), key
+
+
+def test_unaligned_sign_mantissa_buffer(df11):
+    """PackedSignMantissa at an odd device address (a view into a larger buffer): the fast kernel
+    needs 16-byte aligned streams (TMA bulk copies, 128-bit loads), so `auto` routes the tensor to the
+    Algorithm 1 kernel and an explicit `fast` request is refused; the auto result is still the
+    original tensor bit for bit (P:8)."""
+    w = workloads.gaussian_bf16((700001,), seed=21)
+    dt = df11.to_device(df11.encode(w))
+    psm = dt.packed_sign_mantissa
+    big = torch.zeros(psm.numel() + 16, dtype=torch.uint8, device=psm.device)
+    big[1:1 + psm.numel()].copy_(psm)
+    dt.packed_sign_mantissa = big[1:1 + psm.numel()]                  # data_ptr() % 16 == 1
+    assert dt.packed_sign_mantissa.data_ptr() % 16 == 1
+    with pytest.raises(df11.Df11Error):
+        df11.decompress(dt, kernel="fast")
+    out = df11.decompress(dt, kernel="auto")
+    torch.cuda.synchronize()
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1)
+    assert np.array_equal(got, w.reshape(-1))
