@@ -38,6 +38,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default=workloads.BASELINE_CONFIGS[1])
     p.add_argument("--kernel", choices=["auto", "alg1", "fast"], default="auto")
+    p.add_argument("--dist", choices=["gauss", "t5", "sigma-lu"], default="gauss",
+                   help="weight distribution: gauss = the headline recipe; t5 / sigma-lu = realism variants")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
@@ -209,7 +211,7 @@ def main():
         return
 
     # ---- this rank's shard: one transformer block (seeded by rank -> distinct weights per GPU)
-    tensors = workloads.config_tensors(args.config, layer=rank)
+    tensors = workloads.config_tensors(args.config, layer=rank, dist=args.dist)
     hs = [df11.encode(w) for _, w in tensors]
     N = sum(h.num_elements for h in hs)
     scratch = torch.empty(N + 64, dtype=torch.bfloat16, device=dev)        # reused BF16 scratch
@@ -301,7 +303,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": args.config, "tensors": len(hs), "elements_per_gpu": N,
+            "config": {"workload": args.config, "dist": args.dist, "tensors": len(hs), "elements_per_gpu": N,
                        "bf16_bytes_per_gpu": bf16_bytes, "df11_bytes_per_gpu": algo_bytes - bf16_bytes,
                        "bits_per_weight": 8 * (algo_bytes - bf16_bytes) / N, "T": hs[0].T, "n": hs[0].n,
                        "kernel": kernel_used, "parallelism": f"shard{world} (one block per GPU, no collective)",

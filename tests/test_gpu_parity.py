@@ -54,7 +54,8 @@ def _check_oracle_format(df11, oracle_mod, w, kernel, **kw):
 @pytest.mark.parametrize("case", ["gauss_1m", "gauss_ragged", "constant_1bit", "two_symbol", "all_patterns_wide",
                                   "overflow_wide", "fibonacci_32bit", "one_element", "tiny_17", "sigma_large",
                                   "random_bits", "escape_heavy", "escape_deep", "uniform8_short_codes",
-                                  "one_bit_with_tail", "maxlen_12", "maxlen_13", "four_symbol_2bit"])
+                                  "one_bit_with_tail", "maxlen_12", "maxlen_13", "four_symbol_2bit",
+                                  "student_t5", "sigma_loguniform"])
 def test_parity_cases(df11, oracle_mod, kernel, case):
     if case == "gauss_1m":
         w = workloads.gaussian_bf16((1 << 20,), seed=1)
@@ -114,6 +115,13 @@ def test_parity_cases(df11, oracle_mod, kernel, case):
         # four equally likely exponents: 2-bit codes, 8192 outputs per format block, more than the
         # kernel stages in SMEM per tile (its PackedSignMantissa is read from global memory instead)
         w = workloads.from_exponent_histogram({110 + i: 60000 for i in range(4)}, seed=12)
+    elif case == "student_t5":
+        # heavy-tailed realism variant: more exponents, longer codes, more escapes
+        w = workloads.student_t_bf16((3 * 16384 * 5 + 999,), seed=13)
+    elif case == "sigma_loguniform":
+        # per-tensor sigma drawn log-uniform in [0.01, 0.04]; here the extremes
+        w = np.concatenate([workloads.gaussian_bf16((200003,), seed=14, sigma=0.01),
+                            workloads.gaussian_bf16((200003,), seed=15, sigma=0.04)])
     elif case == "escape_deep":
         # geometric tail: codes up to ~26 bits, some beyond the second level (walk path)
         counts = {e: max(1, int(400000 * 0.72 ** i)) for i, e in enumerate(range(60, 200))}

@@ -82,6 +82,14 @@ def gaussian_bf16(shape, seed: int, sigma: float = SIGMA) -> np.ndarray:
     return f32_to_bf16_bits(x).reshape(shape)
 
 
+def student_t_bf16(shape, seed: int, nu: float = 5.0, scale: float = SIGMA) -> np.ndarray:
+    """Heavy-tailed realism variant: BF16(scale * Student-t(nu)) as uint16, PCG64."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = rng.standard_t(nu, size=int(np.prod(shape))).astype(np.float32)
+    x *= np.float32(scale)
+    return f32_to_bf16_bits(x).reshape(shape)
+
+
 def gaussian_bf16_torch(shape, seed: int, device, sigma: float = SIGMA):
     """BF16(N(0, sigma^2)) generated on `device` with torch's Philox (fast, for the multi-GB model
     configs); returned as a host uint16 array (the host encoder's input)."""
@@ -98,10 +106,21 @@ MODELS = {
 }
 
 
-def config_tensors(config: str, layer: int = 0, base_seed: int = 0, sigma: float = SIGMA):
-    """[(name, uint16 array)] for one unit of `config`."""
-    return [(name, gaussian_bf16(shape, seed_for(config, layer, name, base_seed), sigma))
-            for name, shape in CONFIGS[config]]
+def config_tensors(config: str, layer: int = 0, base_seed: int = 0, sigma: float = SIGMA, dist: str = "gauss"):
+    """[(name, uint16 array)] for one unit of `config`.  dist: "gauss" (the headline recipe), or the
+    realism variants of SURVEY 8(d), reported separately: "t5" (scale * Student-t(5)) and "sigma-lu"
+    (per-tensor sigma log-uniform in [0.01, 0.04], drawn from the tensor's seed)."""
+    out = []
+    for name, shape in CONFIGS[config]:
+        seed = seed_for(config, layer, name, base_seed)
+        if dist == "t5":
+            out.append((name, student_t_bf16(shape, seed, 5.0, sigma)))
+        elif dist == "sigma-lu":
+            s = float(np.exp(np.random.Generator(np.random.PCG64(seed ^ 0x5F5F)).uniform(np.log(0.01), np.log(0.04))))
+            out.append((name, gaussian_bf16(shape, seed, s)))
+        else:
+            out.append((name, gaussian_bf16(shape, seed, sigma)))
+    return out
 
 
 def config_numel(config: str) -> int:
