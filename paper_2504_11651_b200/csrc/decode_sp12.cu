@@ -227,11 +227,26 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 
         // =============================== T12 for this tensor (CTA-wide)
         __syncthreads();
+        // each group's first tile: its BlockOutputPos reads and stream copies go out first, so that
+        // their latency overlaps the table build
+        uint32_t tile = seg_begin + g;
+        uint32_t nlo = 0, nhi = 0;
+        if (tile < seg_end) {
+            nlo = __ldg(ts.block_output_pos + tile - base_tile);
+            nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
+            if (t == 0) issue_tile(ts, tile - base_tile, stage, mbar);
+        }
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
         const uint32_t lut_bytes = kk * 256u * eb_bytes;
         const bool lut_in_smem = lut_bytes <= kLutSmem;
-        if (lut_in_smem)
-            for (uint32_t i = tid; i < lut_bytes; i += kCta12) sb[kOffLut + i] = __ldg(ts.luts + i);
+        if (lut_in_smem) {
+            if ((reinterpret_cast<uintptr_t>(ts.luts) & 15) == 0) {       // 16-byte loads (k*256*eb bytes)
+                for (uint32_t i = tid; i < lut_bytes / 16; i += kCta12)
+                    reinterpret_cast<uint4 *>(sb + kOffLut)[i] = __ldg(reinterpret_cast<const uint4 *>(ts.luts) + i);
+            } else {
+                for (uint32_t i = tid; i < lut_bytes; i += kCta12) sb[kOffLut + i] = __ldg(ts.luts + i);
+            }
+        }
         uint32_t len_t = 0;
         if (tid < 256u) {
             len_t = __ldg(ts.code_lengths + tid);
@@ -265,17 +280,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
             }
         };
-        // each group's first tile: its copies are in flight while the table is built
-        uint32_t tile = seg_begin + g;
-        uint32_t nlo = 0, nhi = 0;
-        if (tile < seg_end) {
-            nlo = __ldg(ts.block_output_pos + tile - base_tile);
-            nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
-            if (t == 0) {
-                issue_tile(ts, tile - base_tile, stage, mbar);
-                stage_sm(nlo, nhi);
-            }
-        }
+        if (t == 0 && tile < seg_end) stage_sm(nlo, nhi);
 
         auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
             if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, len);
@@ -285,33 +290,78 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         // in the idle warp regions; an entry then chains up to kCodes of these: the code starting s bits
         // into the row is the first code of the zero-padded prefix row << s if it fits in kR - s bits
         uint16_t *fc = reinterpret_cast<uint16_t *>(sb + kOffReg);
-        for (uint32_t row = tid; row < kRows; row += kCta12) {
-            uint32_t len;
-            const uint32_t sym = walk(row << (32 - kR), len);
-            fc[row] = len <= kR ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
-        }
         bool row_esc_last = false;
         uint32_t *esc_n = smem_w + (kOffEsc + kEscRows * 1024) / 4, *esc_row = esc_n + 1;
         if (kEscRows && tid == 0) *esc_n = 0;
-        __syncthreads();
-        for (uint32_t row = tid; row < kRows; row += kCta12) {
-            uint32_t s = 0, syms = 0, c2 = 0;
-            while (s < kR && c2 < kCodes) {
-                const uint32_t v = fc[(row << s) & (kRows - 1u)], len = v >> 8;
-                if (len == 0 || len > kR - s) break;
-                s += len;
-                syms |= (v & 0xFFu) << (8 * c2);
-                c2++;
-            }
-            uint32_t hi = s | (c2 << 27);
-            if (kEscRows && c2 == 0) {               // escape row: second-level table id in hi[16:24)
-                const uint32_t id = atomicAdd(esc_n, 1u);
-                if (id < kEscRows) { esc_row[id] = row; hi = (id + 1) << 16; }
-            }
+        constexpr bool kFastBuild = kR == 12 && kRep == 1 && kEscRows == 0 && kRows == 4 * kCta12;
+        if (kFastBuild && lut_in_smem) {
+            // 12-bit prefix r: its first 8 bits index the root LUT; a code of 9..12 bits is
+            // resolved by the second-level LUT from the last 4 bits (zero-padded).  Four rows per
+            // thread, unrolled for ILP; then up to 4 chained first-code lookups per row.
+            const uint32_t thr = eb_bytes == 1 ? 240u : 256u;
+            auto lut = [&](uint32_t idx) -> uint32_t {
+                return eb_bytes == 1 ? (uint32_t)sb[kOffLut + idx]
+                                     : (uint32_t)reinterpret_cast<const uint16_t *>(sb + kOffLut)[idx];
+            };
+            uint32_t v[4];
 #pragma unroll
-            for (uint32_t j = 0; j < kRep; j++)
-                *reinterpret_cast<uint2 *>(sb + kOffT + (row * kRep + j) * 8u) = make_uint2(syms, hi);
-            if (row == kRows - 1) row_esc_last = c2 == 0;
+            for (int u = 0; u < 4; u++) {
+                const uint32_t r = tid + u * kCta12;
+                uint32_t e = lut(r >> 4), ok = 1;
+                if (e >= thr) {
+                    const uint32_t j = eb_bytes == 1 ? 256u - e : e - 256u;
+                    ok = j < kk;
+                    e = ok ? lut(j * 256u + ((r & 15u) << 4)) : 0u;
+                    ok = ok && e < thr;
+                }
+                const uint32_t len = ok ? (uint32_t)sb[kOffLen + (e & 0xFFu)] : 0u;
+                v[u] = (len != 0 && len <= kR) ? (rot8(e & 0xFFu) | (len << 8)) : 0u;
+                fc[r] = (uint16_t)v[u];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t r = tid + u * kCta12;
+                uint32_t w = v[u], st = 0, syms = 0, c2 = 0;
+#pragma unroll
+                for (int k2 = 0; k2 < (int)kCodes; k2++) {
+                    const uint32_t len = w >> 8;
+                    if (len == 0 || len > kR - st) break;
+                    syms |= (w & 0xFFu) << (8 * c2);
+                    st += len;
+                    c2++;
+                    if (st < kR) w = fc[(r << st) & (kRows - 1u)];
+                    else w = 0;
+                }
+                *reinterpret_cast<uint2 *>(sb + kOffT + r * 8u) = make_uint2(syms, st | (c2 << 27));
+                if (r == kRows - 1) row_esc_last = c2 == 0;
+            }
+        } else {
+            for (uint32_t row = tid; row < kRows; row += kCta12) {
+                uint32_t len;
+                const uint32_t sym = walk(row << (32 - kR), len);
+                fc[row] = len <= kR ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
+            }
+            __syncthreads();
+            for (uint32_t row = tid; row < kRows; row += kCta12) {
+                uint32_t st = 0, syms = 0, c2 = 0;
+                while (st < kR && c2 < kCodes) {
+                    const uint32_t v = fc[(row << st) & (kRows - 1u)], len = v >> 8;
+                    if (len == 0 || len > kR - st) break;
+                    st += len;
+                    syms |= (v & 0xFFu) << (8 * c2);
+                    c2++;
+                }
+                uint32_t hi = st | (c2 << 27);
+                if (kEscRows && c2 == 0) {               // escape row: second-level table id in hi[16:24)
+                    const uint32_t id = atomicAdd(esc_n, 1u);
+                    if (id < kEscRows) { esc_row[id] = row; hi = (id + 1) << 16; }
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < kRep; j++)
+                    *reinterpret_cast<uint2 *>(sb + kOffT + (row * kRep + j) * 8u) = make_uint2(syms, hi);
+                if (row == kRows - 1) row_esc_last = c2 == 0;
+            }
         }
         if (kEscRows) {
             __syncthreads();

@@ -1,0 +1,77 @@
+#!/usr/bin/env python
+"""Size sweep (SURVEY 8(d) extra; the paper's transfer-vs-decompression figure): DF11 decode
+throughput of one tensor of 2^16 .. 2^28 elements (Llama-style LM-head slices, N(0, 0.02)) vs a
+pinned host-to-device copy of the same BF16 bytes.  One JSON line per size.
+
+    python scripts/bench_size_sweep.py [--min-log2 16] [--max-log2 28]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--min-log2", type=int, default=16)
+    ap.add_argument("--max-log2", type=int, default=28)
+    args = ap.parse_args()
+    import torch
+
+    from paper_2504_11651_b200 import df11
+    dev = torch.device("cuda", 0)
+    hidden = 4096
+    for lg in range(args.min_log2, args.max_log2 + 1, 2):
+        n = 1 << lg
+        shape = (max(n // hidden, 1), min(hidden, n))
+        w = workloads.gaussian_bf16(shape, workloads.seed_for("sweep", lg, "lm_head"))
+        dt = df11.to_device(df11.encode(w), dev)
+        out = df11.decompress(dt)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16).cpu().view(-1),
+                           torch.from_numpy(w.reshape(-1).view(np.int16))), lg
+        reps = max(5, min(200, (1 << 30) // (2 * n)))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(3):
+            df11.decompress(dt, out=out)
+        torch.cuda.synchronize()
+        # the decode calls are captured in a CUDA graph (the ABI is capturable): small tensors are
+        # otherwise bound by the ~15 us of Python + ctypes per call, not by the GPU
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                df11.decompress(dt, out=out)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        dec_us = a.elapsed_time(b) * 1e3 / reps
+        host = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+        dst = torch.empty(n, dtype=torch.bfloat16, device=dev)
+        dst.copy_(host, non_blocking=True)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(reps):
+            dst.copy_(host, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        h2d_us = a.elapsed_time(b) * 1e3 / reps
+        print(json.dumps({"elements": n, "log2": lg, "decode_us": dec_us, "decode_gbs": 2 * n / dec_us / 1e3,
+                          "h2d_us": h2d_us, "h2d_gbs": 2 * n / h2d_us / 1e3, "decode_over_h2d": h2d_us / dec_us,
+                          "reps": reps, "bit_exact": True, "decode_timing": "CUDA graph of reps launches"}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
