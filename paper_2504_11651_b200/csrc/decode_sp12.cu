@@ -290,6 +290,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         // in the idle warp regions; an entry then chains up to kCodes of these: the code starting s bits
         // into the row is the first code of the zero-padded prefix row << s if it fits in kR - s bits
         uint16_t *fc = reinterpret_cast<uint16_t *>(sb + kOffReg);
+        // lookups at row << s hit indices with s zero low bits: XOR-swizzle the bank bits with bits 6..10
+        // so that they spread over the banks instead of piling into one
+        auto fci = [](uint32_t i) { return i ^ (((i >> 6) & 31u) << 1); };
         bool row_esc_last = false;
         uint32_t *esc_n = smem_w + (kOffEsc + kEscRows * 1024) / 4, *esc_row = esc_n + 1;
         if (kEscRows && tid == 0) *esc_n = 0;
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 }
                 const uint32_t len = ok ? (uint32_t)sb[kOffLen + (e & 0xFFu)] : 0u;
                 v[u] = (len != 0 && len <= kR) ? (rot8(e & 0xFFu) | (len << 8)) : 0u;
-                fc[r] = (uint16_t)v[u];
+                fc[fci(r)] = (uint16_t)v[u];
             }
             __syncthreads();
 #pragma unroll
@@ -330,7 +333,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     syms |= (w & 0xFFu) << (8 * c2);
                     st += len;
                     c2++;
-                    if (st < kR) w = fc[(r << st) & (kRows - 1u)];
+                    if (st < kR) w = fc[fci((r << st) & (kRows - 1u))];
                     else w = 0;
                 }
                 *reinterpret_cast<uint2 *>(sb + kOffT + r * 8u) = make_uint2(syms, st | (c2 << 27));
@@ -340,13 +343,13 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             for (uint32_t row = tid; row < kRows; row += kCta12) {
                 uint32_t len;
                 const uint32_t sym = walk(row << (32 - kR), len);
-                fc[row] = len <= kR ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
+                fc[fci(row)] = len <= kR ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
             }
             __syncthreads();
             for (uint32_t row = tid; row < kRows; row += kCta12) {
                 uint32_t st = 0, syms = 0, c2 = 0;
                 while (st < kR && c2 < kCodes) {
-                    const uint32_t v = fc[(row << st) & (kRows - 1u)], len = v >> 8;
+                    const uint32_t v = fc[fci((row << st) & (kRows - 1u))], len = v >> 8;
                     if (len == 0 || len > kR - st) break;
                     st += len;
                     syms |= (v & 0xFFu) << (8 * c2);
