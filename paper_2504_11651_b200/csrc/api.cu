@@ -175,11 +175,11 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
         bt.total_tiles = pos;
         bt.grid = G;
         // Per-CTA tile ranges of equal work (df11_plan_cta_ranges): CTAs that switch tensors get fewer
-        // tiles.  A switch costs 12 tiles, measured best (3: +1.3 %, 8: +2.9 %, 12: +3.1 %, 16/24:
-        // +2.5 % on the Llama-8B block vs uniform ranges).
+        // tiles.  A switch costs 9 tiles (with the original table build 12 measured best: 3: +1.3 %,
+        // 8: +2.9 %, 12: +3.1 % on the Llama-8B block vs uniform ranges; after the faster build, 9).
         if (G <= (uint32_t)df11::kMaxCta) {
 #ifndef DF11_SWITCH_TILES
-#define DF11_SWITCH_TILES 12
+#define DF11_SWITCH_TILES 9
 #endif
             df11_plan_cta_ranges(bt.tile_start, bt.count, G, DF11_SWITCH_TILES, bt.cta_start);
             bt.cta_ranges = 1;
