@@ -56,3 +56,28 @@ def test_decompress_host_block_pipelined():
         for w, o in zip(ws, outs):
             got = o[: w.size].view(torch.int16).numpy().view(np.uint16)
             assert np.array_equal(got, w.reshape(-1))
+
+
+@pytest.mark.parametrize("max_grid", [1, 3])
+def test_capped_grid_many_tiles_and_switches(max_grid):
+    """DF11_MAX_GRID caps the persistent grid (read once per process, so a subprocess): one or three
+    CTAs then walk every tile of a mixed block — long tile loops per group, stage and sign/mantissa
+    refills, decode-table rebuilds at every tensor switch — and the result stays bit-exact."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, workloads\n"
+        "from paper_2504_11651_b200 import df11\n"
+        "ts = [workloads.gaussian_bf16((n,), seed=n) for n in (300001, 17, 123457, 64000, 5)]\n"
+        "ts.append(workloads.student_t_bf16((200003,), seed=2))\n"
+        "dts = [df11.to_device(df11.encode(w)) for w in ts]\n"
+        "outs = df11.decompress_block(dts, kernel='fast')\n"
+        "torch.cuda.synchronize()\n"
+        "for w, o in zip(ts, outs):\n"
+        "    assert np.array_equal(o.view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1), w.reshape(-1))\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DF11_MAX_GRID=str(max_grid), PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
