@@ -212,7 +212,9 @@ def main():
 
     # ---- this rank's shard: one transformer block (seeded by rank -> distinct weights per GPU)
     tensors = workloads.config_tensors(args.config, layer=rank, dist=args.dist)
-    hs = [df11.encode(w) for _, w in tensors]
+    # host encoder threads: share the host's cores among the ranks of this node
+    enc_threads = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", str(world))))
+    hs = [df11.encode(w, num_threads=enc_threads) for _, w in tensors]
     N = sum(h.num_elements for h in hs)
     scratch = torch.empty(N + 64, dtype=torch.bfloat16, device=dev)        # reused BF16 scratch
     outs, o = [], 0
