@@ -390,7 +390,8 @@ def run_model(args, df11, dev, rank, world, local, barrier):
         else:
             ts = [(kind, workloads.gaussian_bf16_torch((m["vocab"], m["hidden"]),
                                                         workloads.seed_for(args.config, idx, kind), dev))]
-        hs = [df11.encode(w) for _, w in ts]
+        threads = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", str(world))))
+        hs = [df11.encode(w, num_threads=threads) for _, w in ts]
         dts = [df11.to_device(h, dev) for h in hs]
         return ts, hs, dts
 
