@@ -107,7 +107,10 @@ void df11_host_tensor_free(df11_host_tensor *t);
 df11_status df11_decompress(const df11_device_tensor *t, void *stream);
 df11_status df11_decompress_block(const df11_device_tensor *ts, uint32_t count, void *stream);
 /* Same with an explicit kernel: DF11_KERNEL_ALG1 (literal Alg. 1, any valid T/n) or DF11_KERNEL_FAST
- * (persistent sm_100a kernel; DF11_E_UNSUPPORTED if a tensor is outside its parameter range). */
+ * (persistent sm_100a kernel; DF11_E_UNSUPPORTED if a tensor is outside its parameter range: T = 256,
+ * n = 8, encoded_exponent / gaps / packed_sign_mantissa 16-byte aligned, out 2-byte aligned).  With
+ * DF11_KERNEL_AUTO the batch is split: tensors in that range take ONE product-kernel launch, the rest
+ * the Alg. 1 kernel (one launch per distinct T); df11_last_kernel_mask() says which ran. */
 df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream,
                                      int kernel);
 
@@ -202,6 +205,9 @@ const char *df11_last_error_message(void);         /* thread-local, human readab
 const char *df11_version(void);
 /* Number of kernel launches enqueued by this thread since the last reset (for bench accounting). */
 uint64_t    df11_launch_count(int reset);
+/* Kernels the calling thread's last df11_decompress* call launched: bit 0 = Alg. 1 kernel, bit 1 =
+ * product kernel (0 = nothing launched, e.g. an empty batch or a validation error). */
+uint32_t    df11_last_kernel_mask(void);
 
 #ifdef __cplusplus
 }

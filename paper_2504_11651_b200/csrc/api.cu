@@ -1,10 +1,10 @@
 // api.cu — the C ABI (include/df11.h): validation, kernel selection, launches, diagnostics.
 //
 // df11_decompress_block: all tensors of a transformer block are described in ONE
-// __grid_constant__ Batch and decoded by ONE launch of the product kernel (decode_sp12.cu; the earlier
-// decode_fast.cu / decode_sp.cu kernels are selected only by A/B builds with -DDF11_TWO_PASS /
-// -DDF11_SP9).  Tensors whose format parameters it does not specialise (T = 256, n = 8) go through the
-// literal Algorithm 1 kernel (decode_alg1.cu), one launch per distinct T.
+// __grid_constant__ Batch and decoded by ONE launch of the product kernel (decode_sp12.cu).  Tensors it
+// does not specialise (format parameters other than T = 256, n = 8, or buffers not 16-byte aligned) go
+// through the literal Algorithm 1 kernel (decode_alg1.cu), one launch per distinct T; the eligible rest
+// of the batch still takes the product kernel (df11_last_kernel_mask reports which kernels ran).
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -16,9 +16,8 @@
 
 namespace df11 {
 cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream_t stream, uint64_t *launches);
-cudaError_t launch_fast(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
-cudaError_t launch_sp(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
+cudaError_t launch_wt(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 bool fast_supports(const df11_device_tensor &t);
 uint32_t fast_grid(uint32_t total_tiles, int num_sms);
 }  // namespace df11
@@ -27,6 +26,7 @@ namespace {
 thread_local char g_msg[512] = "";
 thread_local int g_cuda_err = 0;
 thread_local uint64_t g_launches = 0;
+thread_local uint32_t g_kernel_mask = 0;   // bit 0: Algorithm 1 kernel ran, bit 1: product kernel ran
 
 int g_max_smem[64];
 int g_num_sms[64];
@@ -101,112 +101,100 @@ extern "C" void df11_plan_cta_ranges(const uint32_t *entry_start, uint32_t count
     cta_start[grid] = total;
 }
 
-extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream_v,
-                                                int kernel) {
-    if (count > DF11_MAX_BATCH) return df11_fail(DF11_E_INVALID_ARGUMENT, "count > DF11_MAX_BATCH");
-    if (count && !ts) return df11_fail(DF11_E_INVALID_ARGUMENT, "descriptor array is NULL");
-    if (kernel < DF11_KERNEL_AUTO || kernel > DF11_KERNEL_FAST) return df11_fail(DF11_E_INVALID_ARGUMENT, "bad kernel");
-    bool all_fast = true;
-    uint64_t total = 0;
-    for (uint32_t i = 0; i < count; i++) {
-        df11_status st = validate(ts[i], i);
-        if (st != DF11_OK) return st;
-        if (ts[i].num_elements) {
-            total += ts[i].B;
-            if (!df11::fast_supports(ts[i])) all_fast = false;
-        }
+namespace {
+// Product-kernel launch for tensors ts[idx[0..n)] (all fast_supports, non-empty).
+df11_status launch_fast_batch(const df11_device_tensor *ts, const uint32_t *idx, uint32_t n, int num_sms,
+                              int dev, cudaStream_t stream) {
+    static thread_local df11::Batch bt;   // ~12 KB: keep it off the stack
+    // Tile schedule (the block-batched launcher).  CTA c of the persistent kernel walks a
+    // contiguous global tile range and rebuilds its SMEM decode tables at every tensor boundary inside
+    // it.  Small tensors (biases, norm scales) would pile up in a few CTAs and turn them into
+    // stragglers, so each small tensor is placed exactly at a CTA range boundary (big tensors are split
+    // there), spreading them over distinct CTAs.
+    std::memset(&bt, 0, sizeof(bt));
+    constexpr uint32_t kSmall = 16;                     // tiles
+    uint32_t big[DF11_MAX_BATCH], small[DF11_MAX_BATCH], nbig = 0, nsmall = 0, total = 0;
+    for (uint32_t k = 0; k < n; k++) {
+        const uint32_t i = idx[k];
+        (ts[i].B < kSmall ? small[nsmall++] : big[nbig++]) = i;
+        total += ts[i].B;
     }
-    if (total == 0) return DF11_OK;
-    if (total >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "batch has >= 2^32 format blocks");
-    if (kernel == DF11_KERNEL_FAST && !all_fast)
-        return df11_fail(DF11_E_UNSUPPORTED, "fast kernel: a tensor is outside its parameter range (T=256, n=8)");
-    cudaStream_t stream = (cudaStream_t)stream_v;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    int max_smem = 0, num_sms = 0;
-    device_attrs(dev, max_smem, num_sms);
-
-    static thread_local df11::Batch bt;   // ~6 KB: keep it off the stack
-    bool use_fast = all_fast && kernel != DF11_KERNEL_ALG1;
-    if (use_fast) {
-        // Tile schedule (the block-batched launcher).  CTA c of the persistent kernel walks the
-        // contiguous global tile range [c*total/G, (c+1)*total/G) and rebuilds its SMEM decode tables at
-        // every tensor boundary inside it.  Small tensors (biases, norm scales) would pile up in a few
-        // CTAs and turn them into stragglers, so each small tensor is placed exactly at a CTA range
-        // boundary (big tensors are split there), spreading them over distinct CTAs.
-        std::memset(&bt, 0, sizeof(bt));
-        constexpr uint32_t kSmall = 16;                     // tiles
-        uint32_t big[DF11_MAX_BATCH], small[DF11_MAX_BATCH], nbig = 0, nsmall = 0, total = 0;
-        for (uint32_t i = 0; i < count; i++) {
-            if (!ts[i].num_elements) continue;
-            (ts[i].B < kSmall ? small[nsmall++] : big[nbig++]) = i;
-            total += ts[i].B;
-        }
-        uint32_t G = df11::fast_grid(total, num_sms);
-        // DF11_MAX_GRID (debug knob, read once): cap the persistent grid, e.g. so that a small input
-        // walks many tiles per group under compute-sanitizer
-        static const int max_grid = [] { const char *v = std::getenv("DF11_MAX_GRID"); return v ? std::atoi(v) : 0; }();
-        if (max_grid > 0) G = std::min<uint32_t>(G, (uint32_t)max_grid);
-        auto boundary = [&](uint32_t c) { return (uint32_t)(((uint64_t)total * c) / G); };
-        uint32_t pos = 0, bi = 0, boff = 0;
-        auto push = [&](uint32_t ti, uint32_t off, uint32_t n) {
-            bt.t[bt.count] = ts[ti];
-            bt.tile_start[bt.count] = pos;
-            bt.tile_off[bt.count] = off;
-            bt.count++;
-            pos += n;
-        };
-        auto fill_big_until = [&](uint32_t target) {
-            while (pos < target && bi < nbig) {
-                const uint32_t left = ts[big[bi]].B - boff, take = std::min(left, target - pos);
-                push(big[bi], boff, take);
-                boff += take;
-                if (boff == ts[big[bi]].B) { bi++; boff = 0; }
-            }
-        };
-        for (uint32_t k = 0; k < nsmall; k++) {
-            const uint32_t c = (uint32_t)(((uint64_t)(2 * k + 1) * G) / (2 * nsmall));
-            fill_big_until(boundary(c));
-            push(small[k], 0, ts[small[k]].B);
-        }
-        fill_big_until(total);
+#ifdef DF11_WT
+    uint32_t G = std::min<uint32_t>((uint32_t)num_sms, (total + 31) / 32);
+#else
+    uint32_t G = df11::fast_grid(total, num_sms);
+#endif
+    // DF11_MAX_GRID (debug knob, read once): cap the persistent grid, e.g. so that a small input walks
+    // many tiles per group under compute-sanitizer
+    static const int max_grid = [] { const char *v = std::getenv("DF11_MAX_GRID"); return v ? std::atoi(v) : 0; }();
+    if (max_grid > 0) G = std::min<uint32_t>(G, (uint32_t)max_grid);
+    auto boundary = [&](uint32_t c) { return (uint32_t)(((uint64_t)total * c) / G); };
+    uint32_t pos = 0, bi = 0, boff = 0;
+    auto push = [&](uint32_t ti, uint32_t off, uint32_t cnt) {
+        bt.t[bt.count] = ts[ti];
         bt.tile_start[bt.count] = pos;
-        bt.total_tiles = pos;
-        bt.grid = G;
-        // Per-CTA tile ranges of equal work (df11_plan_cta_ranges): CTAs that switch tensors get fewer
-        // tiles.  A switch costs 9 tiles (with the original table build 12 measured best: 3: +1.3 %,
-        // 8: +2.9 %, 12: +3.1 % on the Llama-8B block vs uniform ranges; after the faster build, 9).
-        if (G <= (uint32_t)df11::kMaxCta) {
+        bt.tile_off[bt.count] = off;
+        bt.count++;
+        pos += cnt;
+    };
+    auto fill_big_until = [&](uint32_t target) {
+        while (pos < target && bi < nbig) {
+            const uint32_t left = ts[big[bi]].B - boff, take = std::min(left, target - pos);
+            push(big[bi], boff, take);
+            boff += take;
+            if (boff == ts[big[bi]].B) { bi++; boff = 0; }
+        }
+    };
+    for (uint32_t k = 0; k < nsmall; k++) {
+        const uint32_t c = (uint32_t)(((uint64_t)(2 * k + 1) * G) / (2 * nsmall));
+        fill_big_until(boundary(c));
+        push(small[k], 0, ts[small[k]].B);
+    }
+    fill_big_until(total);
+    bt.tile_start[bt.count] = pos;
+    bt.total_tiles = pos;
+    bt.grid = G;
+    // Per-CTA tile ranges of equal work (df11_plan_cta_ranges): CTAs that switch tensors get fewer
+    // tiles.  A switch costs 9 tiles (with the original table build 12 measured best: 3: +1.3 %, 8:
+    // +2.9 %, 12: +3.1 % on the Llama-8B block vs uniform ranges; after the faster build, 9).
+    if (G <= (uint32_t)df11::kMaxCta) {
 #ifndef DF11_SWITCH_TILES
 #define DF11_SWITCH_TILES 9
 #endif
-            df11_plan_cta_ranges(bt.tile_start, bt.count, G, DF11_SWITCH_TILES, bt.cta_start);
-            bt.cta_ranges = 1;
-        }
-        const uint32_t kpow[12] = {1u << 9, 1u << 7, 1u << 8, 1u << 24, 1u << 16, 1u << 3, 1u << 31, 1u << 7,
-                                   1u << 12, 8u, 1u << 9, 128u};
-        std::memcpy(bt.kpow, kpow, sizeof(kpow));
-#ifdef DF11_TWO_PASS
-        e = df11::launch_fast(bt, dev, stream, &g_launches);    // two decode passes (decode_fast.cu)
-#elif defined(DF11_SP9)
-        e = df11::launch_sp(bt, dev, stream, &g_launches);      // single pass, 9-bit table (decode_sp.cu)
-#else
-        e = df11::launch_sp12(bt, dev, stream, &g_launches);    // single pass, 12-bit table (decode_sp12.cu)
-#endif
-        if (e != cudaSuccess) return cuda_fail(e, "fast decode launch");
-        return DF11_OK;
+        // DF11_SWITCH_TILES_ENV (A/B knob, read once) overrides the compiled switch cost
+        static const uint32_t sw = [] {
+            const char *v = std::getenv("DF11_SWITCH_TILES_ENV");
+            return v ? (uint32_t)std::atoi(v) : (uint32_t)DF11_SWITCH_TILES;
+        }();
+        df11_plan_cta_ranges(bt.tile_start, bt.count, G, sw, bt.cta_start);
+        bt.cta_ranges = 1;
     }
-    // Algorithm 1: one launch per distinct T
+    const uint32_t kpow[12] = {1u << 12, 1u << 4, 1u << 8, 8u, 0, 0, 0, 0, 0, 0, 0, 0};
+    std::memcpy(bt.kpow, kpow, sizeof(kpow));
+#ifdef DF11_WT
+    cudaError_t e = df11::launch_wt(bt, dev, stream, &g_launches);
+#else
+    cudaError_t e = df11::launch_sp12(bt, dev, stream, &g_launches);
+#endif
+    if (e != cudaSuccess) return cuda_fail(e, "fast decode launch");
+    g_kernel_mask |= 2u;
+    return DF11_OK;
+}
+
+// Algorithm 1 launches (one per distinct T) for tensors ts[idx[0..n)].
+df11_status launch_alg1_batch(const df11_device_tensor *ts, const uint32_t *idx, uint32_t n, size_t max_smem,
+                              cudaStream_t stream) {
+    static thread_local df11::Batch bt;
     bool done[DF11_MAX_BATCH] = {};
-    for (uint32_t i = 0; i < count; i++) {
-        if (done[i] || !ts[i].num_elements) continue;
-        const uint32_t T = ts[i].T;
+    for (uint32_t a = 0; a < n; a++) {
+        if (done[a]) continue;
+        const uint32_t T = ts[idx[a]].T;
         std::memset(&bt, 0, sizeof(bt));
         uint32_t acc = 0;
-        for (uint32_t j = i; j < count; j++) {
-            if (done[j] || !ts[j].num_elements || ts[j].T != T) continue;
-            done[j] = true;
+        for (uint32_t b = a; b < n; b++) {
+            const uint32_t j = idx[b];
+            if (done[b] || ts[j].T != T) continue;
+            done[b] = true;
             bt.t[bt.count] = ts[j];
             bt.tile_start[bt.count] = acc;
             acc += ts[j].B;
@@ -214,9 +202,46 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
         }
         bt.tile_start[bt.count] = acc;
         bt.total_tiles = acc;
-        e = df11::launch_alg1(bt, T, (size_t)max_smem, stream, &g_launches);
+        cudaError_t e = df11::launch_alg1(bt, T, max_smem, stream, &g_launches);
         if (e != cudaSuccess) return cuda_fail(e, "Alg. 1 decode launch");
+        g_kernel_mask |= 1u;
     }
+    return DF11_OK;
+}
+}  // namespace
+
+extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream_v,
+                                                int kernel) {
+    if (count > DF11_MAX_BATCH) return df11_fail(DF11_E_INVALID_ARGUMENT, "count > DF11_MAX_BATCH");
+    if (count && !ts) return df11_fail(DF11_E_INVALID_ARGUMENT, "descriptor array is NULL");
+    if (kernel < DF11_KERNEL_AUTO || kernel > DF11_KERNEL_FAST) return df11_fail(DF11_E_INVALID_ARGUMENT, "bad kernel");
+    g_kernel_mask = 0;
+    uint32_t fast_idx[DF11_MAX_BATCH], slow_idx[DF11_MAX_BATCH], nfast = 0, nslow = 0;
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        df11_status st = validate(ts[i], i);
+        if (st != DF11_OK) return st;
+        if (!ts[i].num_elements) continue;
+        total += ts[i].B;
+        if (kernel != DF11_KERNEL_ALG1 && df11::fast_supports(ts[i])) fast_idx[nfast++] = i;
+        else slow_idx[nslow++] = i;
+    }
+    if (total == 0) return DF11_OK;
+    if (total >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "batch has >= 2^32 format blocks");
+    if (kernel == DF11_KERNEL_FAST && nslow)
+        return df11_fail(DF11_E_UNSUPPORTED,
+                         "fast kernel: a tensor is outside its parameter range (T=256, n=8, 16-byte aligned buffers)");
+    cudaStream_t stream = (cudaStream_t)stream_v;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int max_smem = 0, num_sms = 0;
+    device_attrs(dev, max_smem, num_sms);
+    if (nfast) {
+        df11_status st = launch_fast_batch(ts, fast_idx, nfast, num_sms, dev, stream);
+        if (st != DF11_OK) return st;
+    }
+    if (nslow) return launch_alg1_batch(ts, slow_idx, nslow, (size_t)max_smem, stream);
     return DF11_OK;
 }
 
@@ -315,6 +340,7 @@ extern "C" void df11_count_launches(uint64_t k) { g_launches += k; }
 extern "C" int df11_last_cuda_error(void) { return g_cuda_err; }
 extern "C" const char *df11_last_error_message(void) { return g_msg; }
 extern "C" const char *df11_version(void) { return "df11-b200 0.1 (sm_100a)"; }
+extern "C" uint32_t df11_last_kernel_mask(void) { return g_kernel_mask; }
 extern "C" uint64_t df11_launch_count(int reset) {
     uint64_t v = g_launches;
     if (reset) g_launches = 0;

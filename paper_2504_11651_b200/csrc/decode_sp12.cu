@@ -1,16 +1,20 @@
-// decode_sp12.cu — single-pass persistent sm_100a DF11 decode kernel with a 12-bit multi-code table.
+// decode_sp12.cu — the product kernel: single-pass persistent sm_100a DF11 decode with a 12-bit
+// multi-code table.
 //
-// Same schedule and result as decode_sp.cu: persistent 1024-thread CTAs of 8 groups, a
-// group owns one format block ("tile") at a time, each lane decodes two chunks as two interleaved
-// chains into private SMEM slots, a group scan gives the output positions (Alg. 1), the
-// slots are compacted per warp and merged with PackedSignMantissa into coalesced BF16 stores.
-// What differs is the decode table and the byte format of the exponents between decode and merge:
+// Persistent 1024-thread CTAs of 8 groups; a group owns one format block ("tile") at a time, each
+// lane decodes two chunks as two interleaved chains into private SMEM slots, a group scan gives the
+// output positions (Alg. 1), the slots are compacted per warp and merged with
+// PackedSignMantissa into coalesced BF16 stores.  (The earlier two-pass and 9-bit kernels it
+// replaced are kept under scripts/variants/ for A/B history; they are not part of libdf11.so.)
 //
 //  * T12: 4096 entries of 8 bytes indexed by the next 12 bits of the stream.  An entry holds up to 4
 //    complete codes: lo = their exponents (one byte each), hi = consumed bits | 8*count << 24.  12 bits
 //    decode 3.8 codes per lookup on LLM-like exponents vs 2.8 for a 9-bit, 3-code table, and codes
 //    longer than 12 bits (resolved by the paper's LUT walk) are 8x rarer.  The table is not
-//    lane-replicated (32 KB); its LDS.64 bank conflicts are the price of 1.35x fewer lookups.
+//    lane-replicated (32 KB); its LDS.64 bank conflicts are the price of 1.35x fewer lookups.  Row r is
+//    stored at index r ^ (r >> 8): chains near their end look up rows whose low bits are the one-bit
+//    padding (below), which would otherwise all fall into one bank pair (measured 10.5 wavefronts per
+//    LDS.64 in the decode loop; the XOR spreads them by the row's top 4 bits).
 //  * Exponents are stored rotated right by one bit, r = (e >> 1) | (e & 1) << 7: the BF16 high byte is
 //    then sign | (r & 0x7F) and the low byte (r & 0x80) | mantissa, two bit-selects per 4
 //    elements in the merge instead of a shift, a multiply and two bit-selects.
@@ -19,10 +23,12 @@
 //    pending word: m = acc | lo << fb is stored with ONE 32-bit STS, and the word pointer advances when
 //    the word is full.  Slots are lane-column-major (word k of lane l at k*128 + 4l), so every slot
 //    access of a warp hits 32 distinct banks.  x += hi accumulates the consumed bits in its low 16 bits
-//    (the count, and in the SP12_R9 variant an escape id in bits 16-23, sit above).
+//    (the count sits above).
+//  * The merge stores one 8-element unit (16 bytes) per lane and STG.128, so a warp instruction writes
+//    512 contiguous bytes (4 L1 wavefronts; two 16-byte halves per lane 32 bytes apart took 8).
 //  * A tile's PackedSignMantissa range is staged in SMEM by one TMA bulk copy; the first tile's copies
 //    are issued before the table build; per-CTA tile ranges come from df11_plan_cta_ranges (api.cu).
-#include "fast_helpers.cuh"
+#include "t12_common.cuh"
 
 namespace df11 {
 namespace {
@@ -41,39 +47,17 @@ constexpr int kEach = SP12_EACH;            // decode steps between later warp c
 constexpr uint32_t kGroups12 = SP12_GROUPS;
 constexpr uint32_t kCta12 = kLanes * kGroups12;
 constexpr uint32_t kWarps12 = kLanes / 32;
-#ifdef SP12_R9
-// 9-bit table replicated 16x: replica j lives in bank pair j, lane l reads replica l % 16, so the two
-// half-warp passes of an LDS.64 are conflict-free (2 wavefronts); 3.1 codes per lookup
-constexpr uint32_t kR = 9;
-constexpr uint32_t kRep = 16;
-constexpr uint32_t kEscRows = 4;            // escape rows with a second-level table (next 9 bits)
-constexpr uint32_t kLutSmem = 0;            // the format LUTs are walked in global memory
-constexpr uint32_t kSubW = 10;              // slot words per chain: <= 32 codes + 4 + 1 (kEach = 1)
-#else
-constexpr uint32_t kR = 12;                 // root bits of T12
-constexpr uint32_t kRep = 1;
-constexpr uint32_t kEscRows = 0;
-constexpr uint32_t kLutSmem = 8192;
 constexpr uint32_t kSubW = 12;              // slot words per chain: <= 32 codes + overshoot
-#endif
-constexpr uint32_t kRows = 1u << kR;
-constexpr uint32_t kCodes = 4;              // codes per entry
 constexpr uint32_t kWarpReg12 = 16 + 2 * kSubW * 128;   // frame pad + lane-column slots of 2 chains
-constexpr uint32_t kXMask = 0xFFFFu;           // consumed bits (escape ids sit in bits 16-23)
 
-constexpr uint32_t kOffT = 0;                                       // uint2 [kRows][kRep] + null entry
-constexpr uint32_t kOffEsc = kOffT + kRows * 8 * kRep + 16;         // uint16 [kEscRows][512] + bookkeeping
-constexpr uint32_t kOffLut = kOffEsc + kEscRows * 1024 + 32;
+constexpr uint32_t kOffT = 0;                                       // uint2 [kRows] + null entry
+constexpr uint32_t kOffLut = kOffT + kT12Bytes;
 constexpr uint32_t kOffLen = kOffLut + kLutSmem;                    // CodeLengths[e]
 constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengths[unrot(r)]
 constexpr uint32_t kOffWsum = kOffRLen + 256;                       // [groups][2][warps]
 constexpr uint32_t kOffReg = kOffWsum + kGroups12 * 2 * kWarps12 * 4;
 constexpr uint32_t kOffStage = kOffReg + kGroups12 * kWarps12 * kWarpReg12;
-#ifdef SP12_R9
-constexpr uint32_t kSmCap = 6656;           // PackedSignMantissa bytes of one tile staged in SMEM
-#else
 constexpr uint32_t kSmCap = 7168;           // PackedSignMantissa bytes of one tile staged in SMEM
-#endif
 constexpr uint32_t kOffSm = kOffStage + kGroups12 * kStageBytes;    // [groups][kSmCap]
 constexpr uint32_t kOffCnt = kOffSm + kGroups12 * kSmCap;          // [groups] warps done with the merge
 constexpr uint32_t kOffMbar = kOffCnt + kGroups12 * 8;             // [groups][stage, sign/mantissa]
@@ -83,116 +67,20 @@ static_assert(kOffReg % 16 == 0 && kWarpReg12 % 16 == 0 && kOffStage % 16 == 0 &
               "alignment");
 static_assert(kSmem12 <= 232448, "SMEM budget");
 
-__device__ __forceinline__ uint32_t rot8(uint32_t e) { return ((e >> 1) | (e << 7)) & 0xFFu; }
-__device__ __forceinline__ uint32_t unrot8(uint32_t r) { return ((r << 1) | (r >> 7)) & 0xFFu; }
-
-__device__ __forceinline__ void st8(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-template <int k>
-__device__ __forceinline__ void st8k(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u8 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(k) : "memory");
-}
-__device__ __forceinline__ uint32_t ld8(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ void lds64(uint32_t addr, uint32_t &lo, uint32_t &hi) {
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(addr));
-}
-__device__ __forceinline__ void lds128(uint32_t addr, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
-}
-__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-// Append the n <= 4 bytes of lo (n*8 = hi >> 24) to a lane-column slot through the pending word acc
-// (fb valid bits, < 32) at word address wp.  The partial word is stored every time; it is completed
-// (and rewritten) by later appends.
-__device__ __forceinline__ void pack(uint32_t lo, uint32_t hi, uint32_t &acc, uint32_t &fb, uint32_t &wp,
-                                     uint32_t k_s24) {
-    const uint32_t m = acc | (lo << fb);
-    const uint32_t sp = __funnelshift_l(lo, 0u, fb);        // bytes that spill into the next word
-    sts32(wp, m);
-    fb = madhi(hi, k_s24, fb);
-    const bool full = fb >= 32u;
-    wp = full ? wp + 128u : wp;
-    acc = full ? sp : m;
-    fb &= 31u;
-}
-
-// 96-bit bit buffer shifts that pull in one-bits (the chain-end sentinel, see the kernel)
-__device__ __forceinline__ void shift96_ones(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
-    a = __funnelshift_l(b, a, s);
-    b = __funnelshift_l(c, b, s);
-    c = __funnelshift_l(0xFFFFFFFFu, c, s);
-}
-__device__ __forceinline__ void shift96_long_ones(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t s) {
-    const bool w = s >= 32;
-    a = w ? b : a;
-    b = w ? c : b;
-    c = w ? 0xFFFFFFFFu : c;
-    shift96_ones(a, b, c, s);
-}
-__device__ __forceinline__ void sts32_if(uint32_t addr, uint32_t v, bool p) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
-                 ::"r"(addr), "r"(v), "r"((uint32_t)p) : "memory");
-}
-
-// Copy n (<= 32) bytes held in w[0..7] (little-endian byte stream) to SMEM byte address d.  Phase A:
-// the whole words of the destination (the last may carry garbage past the end: the next chain's phase B
-// rewrites those bytes).  Phase B (after a __syncwarp): the first, partial word.
-__device__ __forceinline__ void compact_words(uint32_t d, const uint32_t (&w)[8], uint32_t n) {
-    const uint32_t r = d & 3u, db = d - r, sh = r * 8u;
-    const uint32_t nw = (r + n + 3u) >> 2;                 // <= 9
-#pragma unroll
-    for (int k = 0; k < 9; k++) {
-        const uint32_t v = k == 0 ? w[0] : __funnelshift_l(w[k - 1], k < 8 ? w[k] : 0u, sh);
-        sts32_if(db + 4u * k, v, (uint32_t)k < nw && (k > 0 || r == 0));
-    }
-}
-__device__ __forceinline__ void compact_head(uint32_t d, uint32_t w0, uint32_t n) {
-    const uint32_t r = d & 3u, db = d - r;
-    if (r == 0) return;
-    const uint32_t v0 = w0 << (r * 8u);
-#pragma unroll
-    for (uint32_t i = 1; i < 4; i++)
-        if (i >= r && i < r + n) st8(db + i, v0 >> (8u * i));
-}
-
-// Four BF16 from 4 rotated exponents R and 4 sign/mantissa bytes S (byte planes):
-// high byte = sign | (R & 0x7F), low byte = (R & 0x80) | mantissa; PRMT interleaves them.
-__device__ __forceinline__ void compose4r(uint32_t R, uint32_t S, uint32_t &lo2, uint32_t &hi2) {
-    const uint32_t H = bitsel<0x80808080u>(R, S);
-    const uint32_t L = bitsel<0x7F7F7F7Fu>(R, S);
-    lo2 = prmt(L, H, 0x5140u);
-    hi2 = prmt(L, H, 0x7362u);
-}
-__device__ __forceinline__ uint16_t compose_r(uint32_t r, uint32_t psm) {
-    return (uint16_t)(((psm & 0x80u) << 8) | ((r & 0x7Fu) << 8) | (r & 0x80u) | (psm & 0x7Fu));
-}
-
 __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__ Batch bt) {
     const uint32_t tid = threadIdx.x;
     const uint32_t g = tid / kLanes;
     const uint32_t t = tid % kLanes;
     const uint32_t lane = tid & 31, wig = t >> 5;
     const uint32_t FULL = 0xFFFFFFFFu;
-#ifdef SP12_R9
-#define K_ROW bt.kpow[10]  // 2^9: a >> 23
-#define K_ENT bt.kpow[11]  // 128: row stride (16 replicas of 8 bytes)
-#else
-#define K_ROW bt.kpow[8]   // 2^12: a >> 20
-#define K_ENT bt.kpow[9]   // 8: entry bytes
-#endif
-#define K_S8 bt.kpow[3]    // 2^24: >> 8
-#define K_S16 bt.kpow[4]   // 2^16: >> 16
+#define K_ROW bt.kpow[0]   // 2^12: a >> 20
+#define K_TOP bt.kpow[1]   // 2^4: a >> 28 (the row's top 4 bits: bank swizzle)
 #define K_S24 bt.kpow[2]   // 2^8: >> 24
+#define K_ENT bt.kpow[3]   // 8: entry bytes
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
-    const uint32_t tab = sbase + kOffT + (lane % kRep) * 8u;   // this lane's replica
-    const uint32_t null_ent = sbase + kOffT + kRows * 8u * kRep;   // all-zero entry: advances nothing
+    const uint32_t tab = sbase + kOffT;
+    const uint32_t null_ent = sbase + kOffT + kRows * 8u;      // all-zero entry: advances nothing
     const uint32_t wreg = kOffReg + (g * kWarps12 + wig) * kWarpReg12;   // this warp's region (byte offset)
     uint32_t *wsum = smem_w + kOffWsum / 4 + g * 2 * kWarps12;
     const uint32_t stage = sbase + kOffStage + g * kStageBytes;
@@ -215,7 +103,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         *mcnt = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < 4) smem_w[(kOffT + kRows * 8u * kRep) / 4 + tid] = 0;
+    if (tid < 4) smem_w[(kOffT + kRows * 8u) / 4 + tid] = 0;
     uint32_t q = 0, parity = 0, qs = 0;
 
     int ti_idx = tensor_of_tile(bt, c_begin);
@@ -236,29 +124,14 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
             if (t == 0) issue_tile(ts, tile - base_tile, stage, mbar);
         }
+        bool safe, lut_in_smem;
+        const bool long_codes = build_t12<kCta12>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen, kOffReg, tid,
+                                                  safe, lut_in_smem);
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
-        const uint32_t lut_bytes = kk * 256u * eb_bytes;
-        const bool lut_in_smem = lut_bytes <= kLutSmem;
-        if (lut_in_smem) {
-            if ((reinterpret_cast<uintptr_t>(ts.luts) & 15) == 0) {       // 16-byte loads (k*256*eb bytes)
-                for (uint32_t i = tid; i < lut_bytes / 16; i += kCta12)
-                    reinterpret_cast<uint4 *>(sb + kOffLut)[i] = __ldg(reinterpret_cast<const uint4 *>(ts.luts) + i);
-            } else {
-                for (uint32_t i = tid; i < lut_bytes; i += kCta12) sb[kOffLut + i] = __ldg(ts.luts + i);
-            }
-        }
-        uint32_t len_t = 0;
-        if (tid < 256u) {
-            len_t = __ldg(ts.code_lengths + tid);
-            sb[kOffLen + tid] = (uint8_t)len_t;
-            sb[kOffRLen + rot8(tid)] = (uint8_t)(len_t ? len_t : 32u);
-        }
-        // a 1-bit codeword allows 64 codes per chain: such tensors take the count + direct path
-        const bool safe = __syncthreads_or(len_t == 1) != 0;
 
         const uint32_t N = (uint32_t)ts.num_elements;
         const bool vec_out = ((reinterpret_cast<uintptr_t>(ts.out) & 15) == 0);
-        const uint4 *__restrict__ psm4 = reinterpret_cast<const uint4 *>(ts.packed_sign_mantissa);
+        const uint2 *__restrict__ psm2 = reinterpret_cast<const uint2 *>(ts.packed_sign_mantissa);
         uint16_t *__restrict__ out = ts.out;
         // PackedSignMantissa of a tile, [a0, a1) = its output range widened to 16 bytes, is staged in
         // SMEM by one TMA bulk copy (issued by the last warp to finish the previous tile's merge) when
@@ -286,100 +159,6 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, len);
             return lut_walk_global(w, ts, len);
         };
-        // first code of every kR-bit prefix (rotated exponent | length << 8; 0 = longer than kR bits),
-        // in the idle warp regions; an entry then chains up to kCodes of these: the code starting s bits
-        // into the row is the first code of the zero-padded prefix row << s if it fits in kR - s bits
-        uint16_t *fc = reinterpret_cast<uint16_t *>(sb + kOffReg);
-        // lookups at row << s hit indices with s zero low bits: XOR-swizzle the bank bits with bits 6..10
-        // so that they spread over the banks instead of piling into one
-        auto fci = [](uint32_t i) { return i ^ (((i >> 6) & 31u) << 1); };
-        bool row_esc_last = false;
-        uint32_t *esc_n = smem_w + (kOffEsc + kEscRows * 1024) / 4, *esc_row = esc_n + 1;
-        if (kEscRows && tid == 0) *esc_n = 0;
-        constexpr bool kFastBuild = kR == 12 && kRep == 1 && kEscRows == 0 && kRows == 4 * kCta12;
-        if (kFastBuild && lut_in_smem) {
-            // 12-bit prefix r: its first 8 bits index the root LUT; a code of 9..12 bits is
-            // resolved by the second-level LUT from the last 4 bits (zero-padded).  Four rows per
-            // thread, unrolled for ILP; then up to 4 chained first-code lookups per row.
-            const uint32_t thr = eb_bytes == 1 ? 240u : 256u;
-            auto lut = [&](uint32_t idx) -> uint32_t {
-                return eb_bytes == 1 ? (uint32_t)sb[kOffLut + idx]
-                                     : (uint32_t)reinterpret_cast<const uint16_t *>(sb + kOffLut)[idx];
-            };
-            uint32_t v[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint32_t r = tid + u * kCta12;
-                uint32_t e = lut(r >> 4), ok = 1;
-                if (e >= thr) {
-                    const uint32_t j = eb_bytes == 1 ? 256u - e : e - 256u;
-                    ok = j < kk;
-                    e = ok ? lut(j * 256u + ((r & 15u) << 4)) : 0u;
-                    ok = ok && e < thr;
-                }
-                const uint32_t len = ok ? (uint32_t)sb[kOffLen + (e & 0xFFu)] : 0u;
-                v[u] = (len != 0 && len <= kR) ? (rot8(e & 0xFFu) | (len << 8)) : 0u;
-                fc[fci(r)] = (uint16_t)v[u];
-            }
-            __syncthreads();
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint32_t r = tid + u * kCta12;
-                uint32_t w = v[u], st = 0, syms = 0, c2 = 0;
-#pragma unroll
-                for (int k2 = 0; k2 < (int)kCodes; k2++) {
-                    const uint32_t len = w >> 8;
-                    if (len == 0 || len > kR - st) break;
-                    syms |= (w & 0xFFu) << (8 * c2);
-                    st += len;
-                    c2++;
-                    if (st < kR) w = fc[fci((r << st) & (kRows - 1u))];
-                    else w = 0;
-                }
-                *reinterpret_cast<uint2 *>(sb + kOffT + r * 8u) = make_uint2(syms, st | (c2 << 27));
-                if (r == kRows - 1) row_esc_last = c2 == 0;
-            }
-        } else {
-            for (uint32_t row = tid; row < kRows; row += kCta12) {
-                uint32_t len;
-                const uint32_t sym = walk(row << (32 - kR), len);
-                fc[fci(row)] = len <= kR ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
-            }
-            __syncthreads();
-            for (uint32_t row = tid; row < kRows; row += kCta12) {
-                uint32_t st = 0, syms = 0, c2 = 0;
-                while (st < kR && c2 < kCodes) {
-                    const uint32_t v = fc[fci((row << st) & (kRows - 1u))], len = v >> 8;
-                    if (len == 0 || len > kR - st) break;
-                    st += len;
-                    syms |= (v & 0xFFu) << (8 * c2);
-                    c2++;
-                }
-                uint32_t hi = st | (c2 << 27);
-                if (kEscRows && c2 == 0) {               // escape row: second-level table id in hi[16:24)
-                    const uint32_t id = atomicAdd(esc_n, 1u);
-                    if (id < kEscRows) { esc_row[id] = row; hi = (id + 1) << 16; }
-                }
-#pragma unroll
-                for (uint32_t j = 0; j < kRep; j++)
-                    *reinterpret_cast<uint2 *>(sb + kOffT + (row * kRep + j) * 8u) = make_uint2(syms, hi);
-                if (row == kRows - 1) row_esc_last = c2 == 0;
-            }
-        }
-        if (kEscRows) {
-            __syncthreads();
-            const uint32_t n_esc = min(*esc_n, kEscRows);
-            uint16_t *l2 = reinterpret_cast<uint16_t *>(sb + kOffEsc);
-            for (uint32_t i = tid; i < (n_esc << 9); i += kCta12) {
-                const uint32_t row = esc_row[i >> 9], j = i & 511u;
-                uint32_t len;
-                const uint32_t sym = walk((row << (32 - kR)) | (j << (32 - kR - 9)), len);
-                l2[i] = len <= kR + 9 ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
-            }
-        }
-        // if kR one-bits hold no complete code (true for canonical codes longer than kR bits), one-bits
-        // after a chain's last bit stall it exactly there
-        const bool long_codes = __syncthreads_or(row_esc_last) != 0;
 
         // =============================== tiles of this group
         for (; tile < seg_end; tile += kGroups12, q++) {
@@ -423,15 +202,17 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 uint32_t aB = W2, bB = W3, cB = exact ? W4 | (0xFFFFFFFFu >> gapC) : W4;
                 shift96_ones(aA, bA, cA, gapA);
                 shift96_ones(aB, bB, cB, gapB);
-                uint32_t wA = slotA, wB = slotB, xA = 0, xB = 0, tA = tab, tB = tab;
-                uint32_t accA = 0, accB = 0, fA = 0, fB = 0;
-                uint32_t hA = 1, hB = 1;
+                uint32_t xA = 0, xB = 0, tA = tab, tB = tab;
+                Slot oA, oB;
+                slot_init(oA, slotA);
+                slot_init(oB, slotB);
+                                uint32_t hA = 1, hB = 1;
                 auto step = [&]() {
                     uint32_t lA, lB;
-                    lds64(madlo(mulhi(aA, K_ROW), K_ENT, tA), lA, hA);
-                    lds64(madlo(mulhi(aB, K_ROW), K_ENT, tB), lB, hB);
-                    pack(lA, hA, accA, fA, wA, K_S24);
-                    pack(lB, hB, accB, fB, wB, K_S24);
+                    lds64(t12_addr(aA, tA, K_ROW, K_TOP, K_ENT), lA, hA);
+                    lds64(t12_addr(aB, tB, K_ROW, K_TOP, K_ENT), lB, hB);
+                    pack(oA, lA, hA, K_S24);
+                    pack(oB, lB, hB, K_S24);
                     xA += hA;
                     xB += hB;
                     shift96_ones(aA, bA, cA, hA);
@@ -447,32 +228,16 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     const bool escA = actA && (hA & 0xFFFFu) == 0, escB = actB && (hB & 0xFFFFu) == 0;
                     if (__any_sync(FULL, escA || escB)) {
                         if (escA) {
-                            uint32_t len, r = 0;
-                            if (kEscRows) {                       // second-level table (next 9 bits)
-                                const uint32_t id = hA >> 16;
-                                if (id != 0) {
-                                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r)
-                                                 : "r"(sbase + kOffEsc + (((id - 1) << 9) | ((aA >> (23 - kR)) & 511u)) * 2));
-                                    len = r >> 8;
-                                }
-                            }
-                            if ((r >> 8) == 0) r = rot8(walk(aA, len));
-                            pack(r & 0xFFu, 8u << 24, accA, fA, wA, K_S24);
+                            uint32_t len;
+                            const uint32_t r = rot8(walk(aA, len));
+                            pack(oA, r & 0xFFu, 8u << 24, K_S24);
                             xA += len;
                             shift96_long_ones(aA, bA, cA, len);
                         }
                         if (escB) {
-                            uint32_t len, r = 0;
-                            if (kEscRows) {                       // second-level table (next 9 bits)
-                                const uint32_t id = hB >> 16;
-                                if (id != 0) {
-                                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r)
-                                                 : "r"(sbase + kOffEsc + (((id - 1) << 9) | ((aB >> (23 - kR)) & 511u)) * 2));
-                                    len = r >> 8;
-                                }
-                            }
-                            if ((r >> 8) == 0) r = rot8(walk(aB, len));
-                            pack(r & 0xFFu, 8u << 24, accB, fB, wB, K_S24);
+                            uint32_t len;
+                            const uint32_t r = rot8(walk(aB, len));
+                            pack(oB, r & 0xFFu, 8u << 24, K_S24);
                             xB += len;
                             shift96_long_ones(aB, bB, cB, len);
                         }
@@ -480,10 +245,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 #pragma unroll
                     for (int u = 0; u < kEach; u++) step();
                 }
-                sts32(wA, accA);                                               // the last partial word
-                sts32(wB, accB);
-                uint32_t nA = ((wA - slotA) >> 5) + (fA >> 3);                 // bytes: 4 per 128-byte row
-                uint32_t nB = ((wB - slotB) >> 5) + (fB >> 3);
+                slot_flush(oA);                                               // the last partial word
+                slot_flush(oB);
+                uint32_t nA = slot_bytes(oA);
+                uint32_t nB = slot_bytes(oB);
                 // drop the codes decoded past each chain's end (they start at or after it)
                 if (!exact) {
                     uint32_t offA = xA & kXMask;
@@ -511,7 +276,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     uint32_t n = 0;
                     while (off < lim) {
                         uint32_t el, eh, len;
-                        lds64(madlo(mulhi(a, K_ROW), K_ENT, tab), el, eh);
+                        lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
                         if ((eh & 0xFFFFu) != 0) len = ld8(rlenb + (el & 0xFFu));
                         else walk(a, len);
                         n++;
@@ -563,7 +328,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     const uint32_t lim_off = sub ? 128u : 64u;
                     while (p < pend && off < lim_off) {
                         uint32_t el, eh, len, sym;
-                        lds64(madlo(mulhi(a, K_ROW), K_ENT, tab), el, eh);
+                        lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
                         if ((eh & 0xFFFFu) != 0) { sym = unrot8(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
                         else sym = walk(a, len);
                         out[p] = compose(sym, __ldg(ts.packed_sign_mantissa + p));
@@ -578,8 +343,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             // ---- this warp's output range
             const uint32_t F = wbeg & ~15u;                                    // region byte of e: e - F
             const uint32_t ra = min(wbeg, hi), rb = min(wbeg + wtot, hi);
-            const uint32_t ga = vec_out ? (ra + 15) >> 4 : 0, gb = vec_out ? max(rb >> 4, ga) : 0;
-            const uint32_t ha = vec_out ? min(ga << 4, rb) : rb, tb = vec_out ? max(gb << 4, ha) : rb;
+            // 8-element units [ua, ub) leave with one STG.128 each; head [ra, ha) and tail [tb, rb) (< 8
+            // elements each) one element per lane
+            const uint32_t ua = vec_out ? (ra + 7) >> 3 : 0, ub = vec_out ? max(rb >> 3, ua) : 0;
+            const uint32_t ha = vec_out ? min(ua << 3, rb) : rb, tb = vec_out ? max(ub << 3, ha) : rb;
             const uint32_t es = lane < 16 ? ra + lane : tb + (lane - 16);
             const bool edge = vec_out && (lane < 16 ? es < ha : es < rb);
 
@@ -626,19 +393,27 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 mbar_wait(smbar, qs & 1u);                                     // PackedSignMantissa staged
                 qs++;
                 if (edge) out[es] = compose_r(ebf[es - F], ld8(smb + (es - a0)));
-                for (uint32_t gi = ga + lane; gi < gb; gi += 32) {
-                    const uint32_t e0 = gi << 4;
-                    uint4 sm;
-                    lds128(smb + (e0 - a0), sm.x, sm.y, sm.z, sm.w);
-                    const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - F));
+                // lane l stores units u and u + 32 of each 64-unit stretch: every STG.128 of the warp
+                // covers 512 contiguous bytes
+                for (uint32_t u = ua + lane; u < ub; u += 64) {
+                    const bool two = u + 32 < ub;
+                    const uint32_t e0 = u << 3, e1 = e0 + 256;
+                    uint32_t s0, s1, x0, x1, s2 = 0, s3 = 0, x2 = 0, x3 = 0;
+                    lds64(smb + (e0 - a0), s0, s1);
+                    lds64(sbase + wreg + (e0 - F), x0, x1);
+                    if (two) {
+                        lds64(smb + (e1 - a0), s2, s3);
+                        lds64(sbase + wreg + (e1 - F), x2, x3);
+                    }
                     uint4 o0, o1;
-                    compose4r(ex.x, sm.x, o0.x, o0.y);
-                    compose4r(ex.y, sm.y, o0.z, o0.w);
-                    compose4r(ex.z, sm.z, o1.x, o1.y);
-                    compose4r(ex.w, sm.w, o1.z, o1.w);
-                    uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
-                    dst[0] = o0;
-                    dst[1] = o1;
+                    compose4r(x0, s0, o0.x, o0.y);
+                    compose4r(x1, s1, o0.z, o0.w);
+                    *reinterpret_cast<uint4 *>(out + e0) = o0;
+                    if (two) {
+                        compose4r(x2, s2, o1.x, o1.y);
+                        compose4r(x3, s3, o1.z, o1.w);
+                        *reinterpret_cast<uint4 *>(out + e1) = o1;
+                    }
                 }
                 // the last warp done with this tile's buffer stages the group's next tile into it
                 __syncwarp();
@@ -653,18 +428,15 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 }
             } else {
                 if (edge) out[es] = compose_r(ebf[es - F], __ldg(ts.packed_sign_mantissa + es));
-                for (uint32_t gi = ga + lane; gi < gb; gi += 32) {
-                    const uint32_t e0 = gi << 4;
-                    const uint4 sm = __ldg(psm4 + gi);
-                    const uint4 ex = *reinterpret_cast<const uint4 *>(ebf + (e0 - F));
-                    uint4 o0, o1;
-                    compose4r(ex.x, sm.x, o0.x, o0.y);
-                    compose4r(ex.y, sm.y, o0.z, o0.w);
-                    compose4r(ex.z, sm.z, o1.x, o1.y);
-                    compose4r(ex.w, sm.w, o1.z, o1.w);
-                    uint4 *dst = reinterpret_cast<uint4 *>(out + e0);
-                    dst[0] = o0;
-                    dst[1] = o1;
+                for (uint32_t u = ua + lane; u < ub; u += 32) {
+                    const uint32_t e0 = u << 3;
+                    const uint2 sm = __ldg(psm2 + u);
+                    uint32_t x0, x1;
+                    lds64(sbase + wreg + (e0 - F), x0, x1);
+                    uint4 o0;
+                    compose4r(x0, sm.x, o0.x, o0.y);
+                    compose4r(x1, sm.y, o0.z, o0.w);
+                    *reinterpret_cast<uint4 *>(out + e0) = o0;
                 }
                 if (!vec_out)                                                  // unaligned output: scalar
                     for (uint32_t e = ra + lane; e < rb; e += 32)
@@ -676,15 +448,29 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         seg_begin = seg_end;
     }
 #undef K_ROW
+#undef K_TOP
 #undef K_ENT
-#undef K_S8
-#undef K_S16
 #undef K_S24
 }
 
 int g_sp12_attr_set[64];
 
 }  // namespace
+
+uint32_t fast_grid(uint32_t total_tiles, int num_sms) {
+    return min((uint32_t)num_sms, (total_tiles + kGroups12 - 1) / kGroups12);
+}
+
+// Tensors the product kernel decodes: the paper's format parameters (T = 256, n = 8) and the
+// alignment its bulk copies need (stream, gaps and PackedSignMantissa 16-byte aligned, BF16 output
+// 2-byte aligned); df11_decompress_block_ex sends every other tensor to the Algorithm 1 kernel.
+bool fast_supports(const df11_device_tensor &t) {
+    return t.T == kT && t.n == kN &&
+           (reinterpret_cast<uintptr_t>(t.encoded_exponent) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(t.gaps) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(t.packed_sign_mantissa) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(t.out) & 1) == 0;
+}
 
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches) {
     if (bt.total_tiles == 0) return cudaSuccess;

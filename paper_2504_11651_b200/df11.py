@@ -26,7 +26,7 @@ MAX_BATCH = 64
 EXPORTED_SYMBOLS = ("df11_encode", "df11_encode_group", "df11_host_tensor_free", "df11_decompress",
                     "df11_decompress_block", "df11_decompress_block_ex", "df11_decompress_host",
                     "df11_decompress_host_block", "df11_plan_cta_ranges", "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
-                    "df11_launch_count", "df11_histogram_device", "df11_encode_plan_create",
+                    "df11_launch_count", "df11_last_kernel_mask", "df11_histogram_device", "df11_encode_plan_create",
                     "df11_encode_plan_free", "df11_encode_device")
 
 
@@ -117,6 +117,8 @@ def lib():
         L.df11_version.restype = ctypes.c_char_p
         L.df11_launch_count.argtypes = [ctypes.c_int]
         L.df11_launch_count.restype = ctypes.c_uint64
+        L.df11_last_kernel_mask.argtypes = []
+        L.df11_last_kernel_mask.restype = ctypes.c_uint32
         _lib = L
     return _lib
 
@@ -132,6 +134,12 @@ def library_path() -> str:
 
 def launch_count(reset: bool = False) -> int:
     return int(lib().df11_launch_count(1 if reset else 0))
+
+
+def last_kernels() -> set:
+    """Kernels this thread's last decompress call launched: a subset of {"alg1", "fast"}."""
+    m = int(lib().df11_last_kernel_mask())
+    return {k for b, k in ((1, "alg1"), (2, "fast")) if m & b}
 
 
 # --------------------------------------------------------------------------- host side

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Iteration pass: smoke, GPU parity, bench, ncu launch list + full capture of the fast kernel.
+# Iteration pass: smoke, GPU parity, bench, ncu launch list + full capture of the product kernel.
 # usage: bash scripts/gpu_iter.sh [tag] [pytest -k expr]
 TAG=${1:-iter}
 KEXPR=${2:-}
@@ -12,10 +12,8 @@ if [ -n "$KEXPR" ]; then
 else
   timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
 fi
-timeout 600 python bench.py --steps 400 --warmup 10 --no-cpu-baseline 2>&1 | tail -2
+timeout 600 python bench.py --steps 400 --warmup 10 --no-cpu-baseline --no-e2e --no-transfer 2>&1 | tail -1
 } > gpurun_out/${TAG}.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 12 --csv --log-file gpurun_out/${TAG}_launches.csv \
-  python bench.py --kernel fast --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"(fast|sp|sp12)_kernel" -s 2 -c 1 -o gpurun_out/${TAG}_prof \
-  python bench.py --kernel fast --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sp12_kernel" -s 2 -c 1 -o gpurun_out/${TAG}_prof \
+  python bench.py --kernel fast --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-transfer > gpurun_out/${TAG}_ncu.log 2>&1
 tail -8 gpurun_out/${TAG}.log

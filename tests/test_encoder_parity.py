@@ -27,7 +27,7 @@ def test_library_exports_every_header_symbol():
     import re
     import os
     hdr = open(os.path.join(os.path.dirname(df11.library_path()), "..", "..", "include", "df11.h")).read()
-    declared = set(re.findall(r"^(?:df11_status|void|int|uint64_t|const char)\s+\*?\s*(df11_\w+)\s*\(",
+    declared = set(re.findall(r"^(?:df11_status|void|int|uint32_t|uint64_t|const char)\s+\*?\s*(df11_\w+)\s*\(",
                               hdr, flags=re.M))
     L = ctypes.CDLL(df11.library_path())
     for name in declared:

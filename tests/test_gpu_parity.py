@@ -251,9 +251,9 @@ def test_full_size_llama8b_block(df11, oracle_mod, kernel):
 
 def test_unaligned_sign_mantissa_buffer(df11):
     """PackedSignMantissa at an odd device address (a view into a larger buffer): the fast kernel
-    needs 16-byte aligned streams (TMA bulk copies, 128-bit loads), so `auto` routes the tensor to the
-    Algorithm 1 kernel and an explicit `fast` request is refused; the auto result is still the
-    original tensor bit for bit (P:8)."""
+    needs 16-byte aligned streams (TMA bulk copies), so `auto` routes the tensor to the Algorithm 1
+    kernel and an explicit `fast` request is refused; the auto result is still the original tensor bit
+    for bit (P:8)."""
     w = workloads.gaussian_bf16((700001,), seed=21)
     dt = df11.to_device(df11.encode(w))
     psm = dt.packed_sign_mantissa
@@ -264,6 +264,30 @@ def test_unaligned_sign_mantissa_buffer(df11):
     with pytest.raises(df11.Df11Error):
         df11.decompress(dt, kernel="fast")
     out = df11.decompress(dt, kernel="auto")
+    assert df11.last_kernels() == {"alg1"}
     torch.cuda.synchronize()
     got = out.view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1)
     assert np.array_equal(got, w.reshape(-1))
+
+
+def test_auto_splits_a_mixed_batch(df11):
+    """A block where one tensor cannot take the product kernel (unaligned PackedSignMantissa view, or
+    other format parameters): `auto` sends only that tensor to the Algorithm 1 kernel and the rest of
+    the block to ONE product-kernel launch; the Alg. 1 kernel takes one launch per distinct T (3
+    launches in all here); every output is the original."""
+    ws = [workloads.gaussian_bf16((n,), seed=30 + i) for i, n in enumerate((300001, 65536, 123457))]
+    hs = [df11.encode(ws[0]), df11.encode(ws[1], T=128, n=16), df11.encode(ws[2])]
+    dts = [df11.to_device(h) for h in hs]
+    psm = dts[2].packed_sign_mantissa
+    big = torch.zeros(psm.numel() + 16, dtype=torch.uint8, device=psm.device)
+    big[3:3 + psm.numel()].copy_(psm)
+    dts[2].packed_sign_mantissa = big[3:3 + psm.numel()]
+    before = df11.launch_count()
+    outs = df11.decompress_block(dts)
+    assert df11.launch_count() - before == 3
+    assert df11.last_kernels() == {"alg1", "fast"}
+    torch.cuda.synchronize()
+    for w, o in zip(ws, outs):
+        assert np.array_equal(o.view(torch.int16).cpu().numpy().view(np.uint16), w)
+    df11.decompress_block([dts[0]])
+    assert df11.last_kernels() == {"fast"}
