@@ -36,11 +36,7 @@ namespace {
 #ifndef SP12_FIRST
 #define SP12_FIRST 6
 #endif
-#ifndef SP12_EACH
-#define SP12_EACH 1
-#endif
 constexpr int kFirst = SP12_FIRST;          // decode steps before the first warp check
-constexpr int kEach = SP12_EACH;            // decode steps between later warp checks
 #ifndef SP12_GROUPS
 #define SP12_GROUPS 8
 #endif
@@ -80,7 +76,6 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
     const uint32_t tab = sbase + kOffT;
-    const uint32_t null_ent = sbase + kOffT + kRows * 8u;      // all-zero entry: advances nothing
     const uint32_t wreg = kOffReg + (g * kWarps12 + wig) * kWarpReg12;   // this warp's region (byte offset)
     uint32_t *wsum = smem_w + kOffWsum / 4 + g * 2 * kWarps12;
     const uint32_t stage = sbase + kOffStage + g * kStageBytes;
@@ -202,15 +197,15 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 uint32_t aB = W2, bB = W3, cB = exact ? W4 | (0xFFFFFFFFu >> gapC) : W4;
                 shift96_ones(aA, bA, cA, gapA);
                 shift96_ones(aB, bB, cB, gapB);
-                uint32_t xA = 0, xB = 0, tA = tab, tB = tab;
+                uint32_t xA = 0, xB = 0;
                 Slot oA, oB;
                 slot_init(oA, slotA);
                 slot_init(oB, slotB);
-                                uint32_t hA = 1, hB = 1;
+                uint32_t hA = 1, hB = 1;
                 auto step = [&]() {
                     uint32_t lA, lB;
-                    lds64(t12_addr(aA, tA, K_ROW, K_TOP, K_ENT), lA, hA);
-                    lds64(t12_addr(aB, tB, K_ROW, K_TOP, K_ENT), lB, hB);
+                    lds64(t12_addr(aA, tab, K_ROW, K_TOP, K_ENT), lA, hA);
+                    lds64(t12_addr(aB, tab, K_ROW, K_TOP, K_ENT), lB, hB);
                     pack(oA, lA, hA, K_S24);
                     pack(oB, lB, hB, K_S24);
                     xA += hA;
@@ -223,9 +218,8 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 for (;;) {
                     const bool actA = (xA & kXMask) < limA, actB = (xB & kXMask) < limB;
                     if (!__any_sync(FULL, actA || actB)) break;
-                    if (!actA) { tA = null_ent; aA = 0; }                      // freeze on the null entry
-                    if (!actB) { tB = null_ent; aB = 0; }
-                    const bool escA = actA && (hA & 0xFFFFu) == 0, escB = actB && (hB & 0xFFFFu) == 0;
+                    // an escape row (a code longer than 12 bits) has hi == 0
+                    const bool escA = actA && hA == 0, escB = actB && hB == 0;
                     if (__any_sync(FULL, escA || escB)) {
                         if (escA) {
                             uint32_t len;
@@ -242,8 +236,18 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                             shift96_long_ones(aB, bB, cB, len);
                         }
                     }
-#pragma unroll
-                    for (int u = 0; u < kEach; u++) step();
+                    // one step; a chain past its end skips the lookup: lo = hi = 0 leave its state unchanged
+                    uint32_t lA = 0, lB = 0;
+                    hA = 0;
+                    hB = 0;
+                    lds64_if(t12_addr(aA, tab, K_ROW, K_TOP, K_ENT), lA, hA, actA);
+                    lds64_if(t12_addr(aB, tab, K_ROW, K_TOP, K_ENT), lB, hB, actB);
+                    pack(oA, lA, hA, K_S24);
+                    pack(oB, lB, hB, K_S24);
+                    xA += hA;
+                    xB += hB;
+                    shift96_ones(aA, bA, cA, hA);
+                    shift96_ones(aB, bB, cB, hB);
                 }
                 slot_flush(oA);                                               // the last partial word
                 slot_flush(oB);

@@ -50,7 +50,6 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
     const uint32_t tab = sbase + kOffTW;
-    const uint32_t null_ent = tab + kRows * 8u;             // all-zero entry: advances nothing
     const uint32_t wreg = sbase + kOffRegW + warp * kRegW;   // this warp's region
     const uint32_t stage = sbase + kOffStgW + warp * kStageW;
     const uint32_t mbar = sbase + kOffMbarW + warp * 8;
@@ -160,15 +159,15 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
                     uint32_t aB = W2, bB = W3, cB = exact ? W4 | (0xFFFFFFFFu >> gapC) : W4;
                     shift96_ones(aA, bA, cA, gapA);
                     shift96_ones(aB, bB, cB, gapB);
-                    uint32_t xA = 0, xB = 0, tA = tab, tB = tab;
+                    uint32_t xA = 0, xB = 0;
                     Slot oA, oB;
                     slot_init(oA, slotA);
                     slot_init(oB, slotB);
                                         uint32_t hA = 1, hB = 1;
                     auto step = [&]() {
                         uint32_t lA, lB;
-                        lds64(t12_addr(aA, tA, K_ROW, K_TOP, K_ENT), lA, hA);
-                        lds64(t12_addr(aB, tB, K_ROW, K_TOP, K_ENT), lB, hB);
+                        lds64(t12_addr(aA, tab, K_ROW, K_TOP, K_ENT), lA, hA);
+                        lds64(t12_addr(aB, tab, K_ROW, K_TOP, K_ENT), lB, hB);
                         pack(oA, lA, hA, K_S24);
                         pack(oB, lB, hB, K_S24);
                         xA += hA;
@@ -181,9 +180,8 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
                     for (;;) {
                         const bool actA = (xA & kXMask) < limA, actB = (xB & kXMask) < limB;
                         if (!__any_sync(FULL, actA || actB)) break;
-                        if (!actA) { tA = null_ent; aA = 0; }                      // freeze on the null entry
-                        if (!actB) { tB = null_ent; aB = 0; }
-                        const bool escA = actA && (hA & 0xFFFFu) == 0, escB = actB && (hB & 0xFFFFu) == 0;
+                        // an escape row (a code longer than 12 bits) has hi == 0
+                        const bool escA = actA && hA == 0, escB = actB && hB == 0;
                         if (__any_sync(FULL, escA || escB)) {
                             if (escA) {
                                 uint32_t len;
@@ -200,7 +198,18 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
                                 shift96_long_ones(aB, bB, cB, len);
                             }
                         }
-                        step();
+                        // one step; a chain past its end skips the lookup: lo = hi = 0 leave its state
+                        uint32_t lA = 0, lB = 0;
+                        hA = 0;
+                        hB = 0;
+                        lds64_if(t12_addr(aA, tab, K_ROW, K_TOP, K_ENT), lA, hA, actA);
+                        lds64_if(t12_addr(aB, tab, K_ROW, K_TOP, K_ENT), lB, hB, actB);
+                        pack(oA, lA, hA, K_S24);
+                        pack(oB, lB, hB, K_S24);
+                        xA += hA;
+                        xB += hB;
+                        shift96_ones(aA, bA, cA, hA);
+                        shift96_ones(aB, bB, cB, hB);
                     }
                     slot_flush(oA);                                               // the last partial word
                     slot_flush(oB);

@@ -39,6 +39,11 @@ __device__ __forceinline__ uint32_t ld8(uint32_t addr) {
 __device__ __forceinline__ void lds64(uint32_t addr, uint32_t &lo, uint32_t &hi) {
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(addr));
 }
+// ld.shared.v2.u32 only if p (lo / hi keep their values otherwise)
+__device__ __forceinline__ void lds64_if(uint32_t addr, uint32_t &lo, uint32_t &hi, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q ld.shared.v2.u32 {%0, %1}, [%2];\n\t}"
+                 : "+r"(lo), "+r"(hi) : "r"(addr), "r"((uint32_t)p));
+}
 __device__ __forceinline__ void lds128(uint32_t addr, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
 }
@@ -46,14 +51,13 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 // Output slot of one chain: decoded (rotated) exponents are appended to a lane-column slot (word k at
-// wp0 + 128 k) through a pending word.  State: acc = the pending word (valid low bits only), pw =
-// 2^(tb mod 32), tb = bits appended so far, wp = address of the pending word.
+// wp0 + 128 k) through a pending word.  State: acc = the pending word (valid low bits only), tb = bits
+// appended so far, wp = address of the pending word.
 struct Slot {
-    uint32_t acc, pw, tb, wp;
+    uint32_t acc, tb, wp;
 };
 __device__ __forceinline__ void slot_init(Slot &s, uint32_t wp0) {
     s.acc = 0;
-    s.pw = 1;
     s.tb = 0;
     s.wp = wp0;
 }
@@ -63,14 +67,13 @@ __device__ __forceinline__ void slot_init(Slot &s, uint32_t wp0) {
 // and the bytes that spill into the next word; crossing a word boundary flips bit 5 of tb.
 __device__ __forceinline__ void pack(Slot &s, uint32_t lo, uint32_t hi, uint32_t k_s24) {
     uint64_t v;
-    asm("mul.wide.u32 %0, %1, %2;" : "=l"(v) : "r"(lo), "r"(s.pw));
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(v) : "r"(lo), "r"(__funnelshift_l(0u, 1u, s.tb)));   // lo * 2^(tb mod 32)
     const uint32_t m = (uint32_t)v | s.acc, sp = (uint32_t)(v >> 32);
     sts32(s.wp, m);
     const uint32_t t2 = madhi(hi, k_s24, s.tb);            // tb + 8n
     const uint32_t f32 = (t2 ^ s.tb) & 32u;                // 32: the word is complete
     s.acc = __funnelshift_rc(m, sp, f32);                  // sp if complete, else m
     s.wp = madlo(f32, 4u, s.wp);                           // + 128 if complete
-    s.pw = __funnelshift_l(0u, 1u, t2);                    // 2^(t2 mod 32)
     s.tb = t2;
 }
 #else

@@ -1,11 +1,10 @@
 #!/bin/bash
-# A/B: parity of a variant lib (fast-kernel cases), then bench default vs variants on the 8B block,
-# then an ncu capture of the first variant.  usage: bash scripts/gpu_ab2.sh TAG VARIANT [VARIANT...]
+# A/B: parity of the default lib (fast-kernel cases), then bench default vs variants on the 8B block
+# (two rounds), then an ncu capture of the default lib.  usage: bash scripts/gpu_ab2.sh TAG VARIANT [VARIANT...]
 TAG=$1; shift
 mkdir -p gpurun_out
 {
-V1=paper_2504_11651_b200/lib/variants/$1.so
-DF11_LIB=$V1 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_runtime.py -x -q -k "fast or split or unaligned or block or scratch or corrupt" 2>&1 | tail -4
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_runtime.py -x -q -k "fast or split or unaligned or block or scratch or corrupt" 2>&1 | tail -4
 for round in 1 2; do
 for v in default "$@"; do
   if [ "$v" = default ]; then L=""; else L=paper_2504_11651_b200/lib/variants/$v.so; fi
@@ -16,6 +15,6 @@ for v in default "$@"; do
 done
 done
 } > gpurun_out/${TAG}.log 2>&1
-DF11_LIB=paper_2504_11651_b200/lib/variants/$1.so timeout 900 ncu --set full --clock-control none --import-source on -k regex:"(sp12|wt)_kernel" -s 2 -c 1 -o gpurun_out/${TAG}_prof \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"(sp12|wt)_kernel" -s 2 -c 1 -o gpurun_out/${TAG}_prof \
   python bench.py --kernel fast --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-transfer > gpurun_out/${TAG}_ncu.log 2>&1
 cat gpurun_out/${TAG}.log
