@@ -98,7 +98,6 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         *mcnt = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < 4) smem_w[(kOffT + kRows * 8u) / 4 + tid] = 0;
     uint32_t q = 0, parity = 0, qs = 0;
 
     int ti_idx = tensor_of_tile(bt, c_begin);
@@ -197,7 +196,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 uint32_t aB = W2, bB = W3, cB = exact ? W4 | (0xFFFFFFFFu >> gapC) : W4;
                 shift96_ones(aA, bA, cA, gapA);
                 shift96_ones(aB, bB, cB, gapB);
-                uint32_t xA = 0, xB = 0;
+                uint32_t xA = kXEnd - limA, xB = kXEnd - limB;   // see kXEnd
                 Slot oA, oB;
                 slot_init(oA, slotA);
                 slot_init(oB, slotB);
@@ -216,7 +215,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 #pragma unroll
                 for (int u = 0; u < kFirst; u++) step();
                 for (;;) {
-                    const bool actA = (xA & kXMask) < limA, actB = (xB & kXMask) < limB;
+                    const bool actA = (xA & kXEnd) == 0, actB = (xB & kXEnd) == 0;
                     if (!__any_sync(FULL, actA || actB)) break;
                     // an escape row (a code longer than 12 bits) has hi == 0
                     const bool escA = actA && hA == 0, escB = actB && hB == 0;
@@ -255,11 +254,11 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 uint32_t nB = slot_bytes(oB);
                 // drop the codes decoded past each chain's end (they start at or after it)
                 if (!exact) {
-                    uint32_t offA = xA & kXMask;
+                    uint32_t offA = xA & kXMask;   // kXEnd - limA + consumed
                     while (nA > 0) {
                         const uint32_t j = nA - 1;
                         const uint32_t l = ld8(rlenb + ld8(slotA + (j >> 2) * 128u + (j & 3u)));
-                        if (offA - l < limA) break;
+                        if (offA - l < kXEnd) break;
                         offA -= l;
                         nA--;
                     }
@@ -267,7 +266,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     while (nB > 0) {
                         const uint32_t j = nB - 1;
                         const uint32_t l = ld8(rlenb + ld8(slotB + (j >> 2) * 128u + (j & 3u)));
-                        if (offB - l < limB) break;
+                        if (offB - l < kXEnd) break;
                         offB -= l;
                         nB--;
                     }

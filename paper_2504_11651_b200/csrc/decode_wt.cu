@@ -67,7 +67,6 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
         mbar_init(mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < 4) smem_w[(kOffTW + kRows * 8u) / 4 + tid] = 0;
     uint32_t q = 0;                                          // tiles staged into this warp's stage
 
     int ti_idx = tensor_of_tile(bt, c_begin);
@@ -159,7 +158,7 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
                     uint32_t aB = W2, bB = W3, cB = exact ? W4 | (0xFFFFFFFFu >> gapC) : W4;
                     shift96_ones(aA, bA, cA, gapA);
                     shift96_ones(aB, bB, cB, gapB);
-                    uint32_t xA = 0, xB = 0;
+                    uint32_t xA = kXEnd - limA, xB = kXEnd - limB;   // see kXEnd
                     Slot oA, oB;
                     slot_init(oA, slotA);
                     slot_init(oB, slotB);
@@ -178,7 +177,7 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
 #pragma unroll
                     for (int u = 0; u < kFirstW; u++) step();
                     for (;;) {
-                        const bool actA = (xA & kXMask) < limA, actB = (xB & kXMask) < limB;
+                        const bool actA = (xA & kXEnd) == 0, actB = (xB & kXEnd) == 0;
                         if (!__any_sync(FULL, actA || actB)) break;
                         // an escape row (a code longer than 12 bits) has hi == 0
                         const bool escA = actA && hA == 0, escB = actB && hB == 0;
@@ -217,11 +216,11 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
                     uint32_t nB = slot_bytes(oB);
                     // drop the codes decoded past each chain's end (they start at or after it)
                     if (!exact) {
-                        uint32_t offA = xA & kXMask;
+                        uint32_t offA = xA & kXMask;   // kXEnd - limA + consumed
                         while (nA > 0) {
                             const uint32_t j = nA - 1;
                             const uint32_t l = ld8(rlenb + ld8(slotA + (j >> 2) * 128u + (j & 3u)));
-                            if (offA - l < limA) break;
+                            if (offA - l < kXEnd) break;
                             offA -= l;
                             nA--;
                         }
@@ -229,7 +228,7 @@ __global__ void __launch_bounds__(kCtaW, 1) wt_kernel(const __grid_constant__ Ba
                         while (nB > 0) {
                             const uint32_t j = nB - 1;
                             const uint32_t l = ld8(rlenb + ld8(slotB + (j >> 2) * 128u + (j & 3u)));
-                            if (offB - l < limB) break;
+                            if (offB - l < kXEnd) break;
                             offB -= l;
                             nB--;
                         }

@@ -10,16 +10,22 @@ namespace {
 constexpr uint32_t kR = 12;                 // root bits of T12
 constexpr uint32_t kRows = 1u << kR;
 constexpr uint32_t kCodes = 4;              // codes per entry
-constexpr uint32_t kT12Bytes = kRows * 8 + 48;   // entries + the all-zero null entry (+ pad)
+constexpr uint32_t kT12Bytes = (kRows + 16) * 8;   // entries at r + (r >> 8) < kRows + 15 (+ pad)
 constexpr uint32_t kLutSmem = 8192;         // format LUT bytes staged in SMEM (larger: walked in global)
-constexpr uint32_t kXMask = 0xFFFFu;        // consumed bits of a chain (x += hi; the count sits above)
+// Chain progress x = 2^16 - (chain length in bits) + consumed bits: x += hi adds the consumed bits in the
+// low bits (the count sits in bits 27..31 and never reaches bit 16), so the chain is active while bit 16
+// is clear.
+constexpr uint32_t kXEnd = 1u << 16;
+constexpr uint32_t kXMask = 2 * kXEnd - 1;
 
-// T12 row r lives at entry r ^ (r >> 8) (bank-pair swizzle by the row's top 4 bits; a bijection on
-// [0, 4096) that maps 0 to 0, so a frozen chain (a = 0) on a null-entry base still reads that entry).
-__host__ __device__ __forceinline__ uint32_t t12_slot(uint32_t r) { return r ^ (r >> 8); }
+// T12 row r lives at entry r + (r >> 8): chains near their end look up rows whose low bits are the
+// one-bit padding (see the kernels), which would otherwise all fall into one bank pair (measured 10.5
+// wavefronts per LDS.64 in the decode loop); adding the row's top 4 bits spreads them.  The map is
+// injective on [0, 4096) (block h of 256 rows moves to [257h, 257h + 256)); entries up to 4110.
+__host__ __device__ __forceinline__ uint32_t t12_slot(uint32_t r) { return r + (r >> 8); }
 __device__ __forceinline__ uint32_t t12_addr(uint32_t a, uint32_t base, uint32_t k_row, uint32_t k_top,
                                              uint32_t k_ent) {
-    return madlo(mulhi(a, k_row) ^ mulhi(a, k_top), k_ent, base);   // (a >> 20) ^ (a >> 28)
+    return madlo(madhi(a, k_top, mulhi(a, k_row)), k_ent, base);   // ((a >> 20) + (a >> 28)) * 8 + base
 }
 __device__ __forceinline__ uint32_t rot8(uint32_t e) { return ((e >> 1) | (e << 7)) & 0xFFu; }
 __device__ __forceinline__ uint32_t unrot8(uint32_t r) { return ((r << 1) | (r >> 7)) & 0xFFu; }
