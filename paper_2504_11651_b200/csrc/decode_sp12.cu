@@ -396,6 +396,37 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 mbar_wait(smbar, qs & 1u);                                     // PackedSignMantissa staged
                 qs++;
                 if (edge) out[es] = compose_r(ebf[es - F], ld8(smb + (es - a0)));
+#ifndef SP12_MERGE_LOOP
+                // lane l stores units u0 + 32k: every STG.128 of the warp covers 512 contiguous bytes.
+                // A warp range has <= 64 * 32 outputs (<= 257 units, <= 9 per lane); the unit stride is
+                // an immediate offset of the loads and stores.
+                {
+                    // warp-uniform trip count: every lane stores (ub - ua) / 32 units, lanes below
+                    // (ub - ua) % 32 one more
+                    const uint32_t nun = ub - ua, nfull = nun >> 5;
+                    const uint32_t e0 = (ua + lane) << 3;
+                    uint32_t sa = smb + (e0 - a0), xa = sbase + wreg + (e0 - F);
+                    uint4 *op = reinterpret_cast<uint4 *>(out + e0);
+                    auto unit = [&](uint32_t k) {
+                        uint32_t s0, s1, x0, x1;
+                        lds64(sa + 256u * k, s0, s1);
+                        lds64(xa + 256u * k, x0, x1);
+                        uint4 o;
+                        compose4r(x0, s0, o.x, o.y);
+                        compose4r(x1, s1, o.z, o.w);
+                        op[32 * k] = o;
+                    };
+                    uint32_t k = 0;
+                    for (; k + 4 <= nfull; k += 4) {
+                        unit(k);
+                        unit(k + 1);
+                        unit(k + 2);
+                        unit(k + 3);
+                    }
+                    for (; k < nfull; k++) unit(k);
+                    if (lane < (nun & 31u)) unit(nfull);
+                }
+#else
                 // lane l stores units u and u + 32 of each 64-unit stretch: every STG.128 of the warp
                 // covers 512 contiguous bytes
                 for (uint32_t u = ua + lane; u < ub; u += 64) {
@@ -418,6 +449,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                         *reinterpret_cast<uint4 *>(out + e1) = o1;
                     }
                 }
+#endif
                 // the last warp done with this tile's buffer stages the group's next tile into it
                 __syncwarp();
                 if (lane == 0) {
