@@ -12,9 +12,9 @@
 //    decode 3.8 codes per lookup on LLM-like exponents vs 2.8 for a 9-bit, 3-code table, and codes
 //    longer than 12 bits (resolved by the paper's LUT walk) are 8x rarer.  The table is not
 //    lane-replicated (32 KB); its LDS.64 bank conflicts are the price of 1.35x fewer lookups.  Row r is
-//    stored at index r ^ (r >> 8): chains near their end look up rows whose low bits are the one-bit
+//    stored at index r + (r >> 8): chains near their end look up rows whose low bits are the one-bit
 //    padding (below), which would otherwise all fall into one bank pair (measured 10.5 wavefronts per
-//    LDS.64 in the decode loop; the XOR spreads them by the row's top 4 bits).
+//    LDS.64 in the decode loop; adding the row's top 4 bits spreads them).
 //  * Exponents are stored rotated right by one bit, r = (e >> 1) | (e & 1) << 7: the BF16 high byte is
 //    then sign | (r & 0x7F) and the low byte (r & 0x80) | mantissa, two bit-selects per 4
 //    elements in the merge instead of a shift, a multiply and two bit-selects.
@@ -46,21 +46,26 @@ constexpr uint32_t kWarps12 = kLanes / 32;
 constexpr uint32_t kSubW = 12;              // slot words per chain: <= 32 codes + overshoot
 constexpr uint32_t kWarpReg12 = 16 + 2 * kSubW * 128;   // frame pad + lane-column slots of 2 chains
 
-constexpr uint32_t kOffT = 0;                                       // uint2 [kRows] + null entry
+constexpr uint32_t kOffT = 0;                                       // T12 (t12_common.cuh)
 constexpr uint32_t kOffLut = kOffT + kT12Bytes;
 constexpr uint32_t kOffLen = kOffLut + kLutSmem;                    // CodeLengths[e]
 constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengths[unrot(r)]
-constexpr uint32_t kOffWsum = kOffRLen + 256;                       // [groups][2][warps]
-constexpr uint32_t kOffReg = kOffWsum + kGroups12 * 2 * kWarps12 * 4;
-constexpr uint32_t kOffStage = kOffReg + kGroups12 * kWarps12 * kWarpReg12;
 constexpr uint32_t kSmCap = 7168;           // PackedSignMantissa bytes of one tile staged in SMEM
-constexpr uint32_t kOffSm = kOffStage + kGroups12 * kStageBytes;    // [groups][kSmCap]
-constexpr uint32_t kOffCnt = kOffSm + kGroups12 * kSmCap;          // [groups] warps done with the merge
-constexpr uint32_t kOffMbar = kOffCnt + kGroups12 * 8;             // [groups][stage, sign/mantissa]
-constexpr uint32_t kSmem12 = kOffMbar + kGroups12 * 16;
-static_assert(kOffReg % 16 == 0 && kWarpReg12 % 16 == 0 && kOffStage % 16 == 0 && kOffSm % 16 == 0 &&
-                  kOffMbar % 8 == 0,
+// one block per group, so that every per-group / per-warp address is one base register plus an
+// immediate offset
+constexpr uint32_t kOffGrp = kOffRLen + 256;                        // [groups][kGrpBytes]
+constexpr uint32_t kGStage = 0;                                     // stream chunk + gaps (TMA)
+constexpr uint32_t kGSm = kGStage + kStageBytes;                    // PackedSignMantissa (TMA)
+constexpr uint32_t kGReg = kGSm + kSmCap;                           // [warps][kWarpReg12] slots / regions
+constexpr uint32_t kGWsum = kGReg + kWarps12 * kWarpReg12;          // [2][warps] warp totals
+constexpr uint32_t kGCnt = kGWsum + 2 * kWarps12 * 4;               // warps done with the merge
+constexpr uint32_t kGMbar = kGCnt + 16;                             // [stage, sign/mantissa] mbarriers
+constexpr uint32_t kGrpBytes = kGMbar + 16;
+constexpr uint32_t kSmem12 = kOffGrp + kGroups12 * kGrpBytes;
+static_assert(kOffGrp % 16 == 0 && kGSm % 16 == 0 && kGReg % 16 == 0 && kWarpReg12 % 16 == 0 &&
+                  kGWsum % 16 == 0 && kGMbar % 8 == 0 && kGrpBytes % 16 == 0,
               "alignment");
+static_assert(kWarps12 * kWarpReg12 >= 8192, "first-code table scratch fits group 0's warp regions");
 static_assert(kSmem12 <= 232448, "SMEM budget");
 
 __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__ Batch bt) {
@@ -76,14 +81,14 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
     const uint32_t tab = sbase + kOffT;
-    const uint32_t wreg = kOffReg + (g * kWarps12 + wig) * kWarpReg12;   // this warp's region (byte offset)
-    uint32_t *wsum = smem_w + kOffWsum / 4 + g * 2 * kWarps12;
-    const uint32_t stage = sbase + kOffStage + g * kStageBytes;
-    const uint32_t mbar = sbase + kOffMbar + g * 16;
+    const uint32_t gbase = sbase + kOffGrp + g * kGrpBytes;           // this group's block
+    const uint32_t wreg = gbase + kGReg + wig * kWarpReg12;           // this warp's region
+    const uint32_t stage = gbase + kGStage;
+    const uint32_t mbar = gbase + kGMbar;
     const uint32_t smbar = mbar + 8;                        // the tile's PackedSignMantissa has landed
-    const uint32_t smb = sbase + kOffSm + g * kSmCap;
-    uint32_t *mcnt = smem_w + kOffCnt / 4 + g;
-    const uint32_t slotA = sbase + wreg + 16u + lane * 4u, slotB = slotA + kSubW * 128u;
+    const uint32_t smb = gbase + kGSm;
+    const uint32_t mcnt = gbase + kGCnt;
+    const uint32_t slotA = wreg + 16u + lane * 4u, slotB = slotA + kSubW * 128u;
     const uint32_t rlenb = sbase + kOffRLen;
 
     const uint32_t total = bt.total_tiles;
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     if (t == 0) {
         mbar_init(mbar, 1);
         mbar_init(smbar, 1);
-        *mcnt = 0;
+        sts32(mcnt, 0);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     uint32_t q = 0, parity = 0, qs = 0;
@@ -119,7 +124,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             if (t == 0) issue_tile(ts, tile - base_tile, stage, mbar);
         }
         bool safe, lut_in_smem;
-        const bool long_codes = build_t12<kCta12>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen, kOffReg, tid,
+        const bool long_codes = build_t12<kCta12>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen, kOffGrp + kGReg, tid,
                                                   safe, lut_in_smem);
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
 
@@ -304,14 +309,15 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 const uint32_t v = __shfl_up_sync(FULL, incl, d);
                 if (lane >= (uint32_t)d) incl += v;
             }
-            uint32_t *ws = wsum + parity * kWarps12;
-            if (lane == 31) ws[wig] = incl;
+            const uint32_t ws = gbase + kGWsum + parity * (kWarps12 * 4);
+            if (lane == 31) sts32(ws + wig * 4, incl);
             group_bar(g);                          // also: every thread has read this tile's stage
             parity ^= 1u;
             if (t == 0 && has_next) issue_tile(ts, b + kGroups12, stage, mbar);
             uint32_t wpre = 0;
             {
-                const uint4 v = *reinterpret_cast<const uint4 *>(ws);
+                uint4 v;
+                lds128(ws, v.x, v.y, v.z, v.w);
                 wpre = (wig > 0 ? v.x : 0u) + (wig > 1 ? v.y : 0u) + (wig > 2 ? v.z : 0u);
             }
             const uint32_t wtot = __shfl_sync(FULL, incl, 31);
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     wb[k] = lds32(slotB + 128u * k);
                 }
                 __syncwarp();
-                const uint32_t dA = sbase + wreg + (wbeg - F) + lpos, dB = dA + cntA;
+                const uint32_t dA = wreg + (wbeg - F) + lpos, dB = dA + cntA;
                 compact_words(dA, wa, cntA);
                 compact_words(dB, wb, cntB);
                 __syncwarp();
@@ -390,12 +396,11 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             __syncwarp();
 
             // ---- per-warp merge of [ra, rb): compose BF16 and store
-            const uint8_t *ebf = sb + wreg;                                    // ebf[e - F]
             uint32_t a0, a1;
             if (sm_range(lo, hi, a0, a1)) {
                 mbar_wait(smbar, qs & 1u);                                     // PackedSignMantissa staged
                 qs++;
-                if (edge) out[es] = compose_r(ebf[es - F], ld8(smb + (es - a0)));
+                if (edge) out[es] = compose_r(ld8(wreg + (es - F)), ld8(smb + (es - a0)));
 #ifndef SP12_MERGE_LOOP
                 // lane l stores units u0 + 32k: every STG.128 of the warp covers 512 contiguous bytes.
                 // A warp range has <= 64 * 32 outputs (<= 257 units, <= 9 per lane); the unit stride is
@@ -405,7 +410,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     // (ub - ua) % 32 one more
                     const uint32_t nun = ub - ua, nfull = nun >> 5;
                     const uint32_t e0 = (ua + lane) << 3;
-                    uint32_t sa = smb + (e0 - a0), xa = sbase + wreg + (e0 - F);
+                    uint32_t sa = smb + (e0 - a0), xa = wreg + (e0 - F);
                     uint4 *op = reinterpret_cast<uint4 *>(out + e0);
                     auto unit = [&](uint32_t k) {
                         uint32_t s0, s1, x0, x1;
@@ -434,10 +439,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     const uint32_t e0 = u << 3, e1 = e0 + 256;
                     uint32_t s0, s1, x0, x1, s2 = 0, s3 = 0, x2 = 0, x3 = 0;
                     lds64(smb + (e0 - a0), s0, s1);
-                    lds64(sbase + wreg + (e0 - F), x0, x1);
+                    lds64(wreg + (e0 - F), x0, x1);
                     if (two) {
                         lds64(smb + (e1 - a0), s2, s3);
-                        lds64(sbase + wreg + (e1 - F), x2, x3);
+                        lds64(wreg + (e1 - F), x2, x3);
                     }
                     uint4 o0, o1;
                     compose4r(x0, s0, o0.x, o0.y);
@@ -454,20 +459,22 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 __syncwarp();
                 if (lane == 0) {
                     __threadfence_block();
-                    if (atomicAdd(mcnt, 1u) == kWarps12 - 1) {
-                        *mcnt = 0;
+                    uint32_t done;
+                    asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(done) : "r"(mcnt) : "memory");
+                    if (done == kWarps12 - 1) {
+                        sts32(mcnt, 0);
                         __threadfence_block();
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         if (has_next) stage_sm(nlo, nhi);
                     }
                 }
             } else {
-                if (edge) out[es] = compose_r(ebf[es - F], __ldg(ts.packed_sign_mantissa + es));
+                if (edge) out[es] = compose_r(ld8(wreg + (es - F)), __ldg(ts.packed_sign_mantissa + es));
                 for (uint32_t u = ua + lane; u < ub; u += 32) {
                     const uint32_t e0 = u << 3;
                     const uint2 sm = __ldg(psm2 + u);
                     uint32_t x0, x1;
-                    lds64(sbase + wreg + (e0 - F), x0, x1);
+                    lds64(wreg + (e0 - F), x0, x1);
                     uint4 o0;
                     compose4r(x0, sm.x, o0.x, o0.y);
                     compose4r(x1, sm.y, o0.z, o0.w);
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 }
                 if (!vec_out)                                                  // unaligned output: scalar
                     for (uint32_t e = ra + lane; e < rb; e += 32)
-                        out[e] = compose_r(ebf[e - F], __ldg(ts.packed_sign_mantissa + e));
+                        out[e] = compose_r(ld8(wreg + (e - F)), __ldg(ts.packed_sign_mantissa + e));
                 if (t == 0 && has_next) stage_sm(nlo, nhi);
                 __syncwarp();                  // the region's reads are done before the next tile's slots
             }
