@@ -43,7 +43,11 @@ constexpr int kFirst = SP12_FIRST;          // decode steps before the first war
 constexpr uint32_t kGroups12 = SP12_GROUPS;
 constexpr uint32_t kCta12 = kLanes * kGroups12;
 constexpr uint32_t kWarps12 = kLanes / 32;
-constexpr uint32_t kSubW = 12;              // slot words per chain: <= 32 codes + overshoot
+// slot words per chain: a chain holds <= 32 codes (<= 64 bits of code starts, codes >= 2 bits: 1-bit
+// codes take the direct path); without exact ends it may overshoot its end by <= 3 codes (one lookup
+// past it in the loop; the unrolled steps consume >= 52 bits only in >= 5 lookups): <= 35 bytes, so the
+// pending word never passes word 8.
+constexpr uint32_t kSubW = 10;
 constexpr uint32_t kWarpReg12 = 16 + 2 * kSubW * 128;   // frame pad + lane-column slots of 2 chains
 
 constexpr uint32_t kOffT = 0;                                       // T12 (t12_common.cuh)

@@ -28,10 +28,10 @@ ins("            mbar_wait(mbar, q & 1u);\n", "            PROF_MARK(1);\n", aft
 ins("            const uint32_t cnt = cntA + cntB;\n", "            PROF_MARK(2);\n")
 ins("            group_bar(g);                          // also: every thread has read this tile's stage\n", "            PROF_MARK(3);\n")
 ins("            group_bar(g);                          // also: every thread has read this tile's stage\n", "            PROF_MARK(4);\n", after=True)
-ins("                const uint32_t dA = sbase + wreg + (wbeg - F) + lpos, dB = dA + cntA;\n", "                PROF_MARK(5);\n")
+ins("                const uint32_t dA = wreg + (wbeg - F) + lpos, dB = dA + cntA;\n", "                PROF_MARK(5);\n")
 ins("            // ---- per-warp merge of [ra, rb): compose BF16 and store (P:439-441)\n", "            PROF_MARK(6);\n")
 ins("                mbar_wait(smbar, qs & 1u);                                     // PackedSignMantissa staged\n", "                PROF_MARK(7);\n", after=True)
-ins("#undef K_ROW\n#undef K_ENT", """    if (lane == 0)
+ins("#undef K_ROW\n#undef K_TOP", """    if (lane == 0)
         for (int i = 0; i < 8; i++) g_sp12_prof[blockIdx.x * 32 + (tid >> 5)][i] = prof[i];
 """)
 ins("cudaError_t launch_sp12(", """extern "C" int df11_debug_sp12_prof(unsigned long long *host) {
