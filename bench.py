@@ -7,8 +7,9 @@
 
 A step = one df11_decompress_block call over every tensor of one transformer block (all §8(a) rows:
 tile map, LUT staging, chunk staging, gaps, phase 1, scan, phase 2, write-back), inputs resident in
-HBM.  Each rank decodes its own block (different seeds): no collective on the data path; NCCL is
-used only for the start barrier and the max-over-ranks of the timings.  Rank 0 prints ONE JSON line.
+HBM.  Each rank decodes its own block (different seeds): no collective on the data path and NCCL is
+never initialised; a gloo (CPU) group aligns the start (barrier) and combines the per-rank timings
+(max) and byte counts (sum).  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -44,6 +45,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-transfer", action="store_true", help="skip the CPU->GPU transfer baseline (NEXT-2)")
+    p.add_argument("--selftest-dist", action="store_true",
+                   help="host-side multi-rank check without a GPU: gloo group, per-rank shard placement and "
+                        "the whole-job aggregation of synthetic per-rank bytes/times (tests/test_shard_dist.py)")
     p.add_argument("--unique-blocks", type=int, default=2,
                    help="model configs: distinct encoded blocks per rank (device copies fill the shard)")
     return p.parse_args()
@@ -120,36 +124,74 @@ def ncu_traffic(config: str, kernel: str):
 
 
 # --------------------------------------------------------------------------- CPU oracle timing
-def oracle_decode_rate(tensors_np, budget_s: float = 12.0):
-    """Time the oracle's sequential decoder (D1) on a bounded sample of this workload: whole tensors
-    in config order until ~budget_s of CPU work.  One thread per tensor (the oracle is single-
-    threaded); returns (GB/s of BF16, cores, sample description, seconds)."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_decode_rate(tensors_np, budget_s: float = 8.0):
+    """Time the CPU oracle on a bounded sample of this workload (whole tensors in config order until
+    ~budget_s of single-thread work), two ways (SURVEY 8(d) "CPU oracle timing"):
+      D1: the sequential decoder, one thread per tensor (it is sequential by definition);
+      D2: the Algorithm 1 emulator with all host cores spread over the format blocks of each tensor.
+    Returns the cpu_baseline dict (value = the faster of the two, with the threads it used)."""
     import concurrent.futures as cf
 
     import oracle
     fmts = []
     spent = 0.0
-    est_rate = 60e6                                      # el/s, refined after the first tensor
+    est_rate = 60e6                                      # el/s per thread (D1), for the sample size
     for name, w in tensors_np:
         if fmts and spent + w.size / est_rate > budget_s:
             break
         fmts.append((name, oracle.encode(w.reshape(-1)), w))
         spent += w.size / est_rate
-    cores = min(len(fmts), os.cpu_count() or 1)
+    elems = sum(w.size for _, _, w in fmts)
+    host_cores = os.cpu_count() or 1
+
+    # D1: one thread per tensor, whole passes until ~budget_s of thread time (at most 8 passes)
+    d1_threads = min(len(fmts), host_cores)
     passes, dt = 0, 0.0
-    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
-        # whole passes over the sample until ~budget_s of thread-time (at most 8 passes)
-        while passes < 8 and (passes == 0 or dt * cores < budget_s):
+    with cf.ThreadPoolExecutor(max_workers=d1_threads) as ex:
+        while passes < 8 and (passes == 0 or dt * d1_threads < budget_s):
             t0 = time.perf_counter()
             outs = list(ex.map(lambda f: oracle.decode_sequential(f[1]), fmts))
             dt += time.perf_counter() - t0
             passes += 1
     for (name, _, w), o in zip(fmts, outs):
         assert np.array_equal(o, w.reshape(-1)), name
-    elems = sum(w.size for _, _, w in fmts)
-    sample = f"D1 sequential decode of {len(fmts)} tensor(s) ({elems} elements: " + \
-        ", ".join(n for n, _, _ in fmts) + f") of the workload, {cores} thread(s), {passes} pass(es)"
-    return 2 * elems * passes / dt / 1e9, cores, sample, dt
+    d1 = {"gbs": 2 * elems * passes / dt / 1e9, "threads": d1_threads, "passes": passes, "seconds": round(dt, 2)}
+
+    # D2: every host core on the format blocks of each tensor in turn
+    jobs = []
+    outs2 = [np.zeros(w.size, np.uint16) for _, _, w in fmts]
+    for (name, f, w), o in zip(fmts, outs2):
+        B = int(f["B"])
+        step = max(1, -(-B // (4 * host_cores)))
+        jobs += [(f, b, min(B, b + step), o) for b in range(0, B, step)]
+    passes2, dt2 = 0, 0.0
+    with cf.ThreadPoolExecutor(max_workers=host_cores) as ex:
+        while passes2 < 8 and (passes2 == 0 or dt2 * host_cores < 2 * budget_s):
+            t0 = time.perf_counter()
+            list(ex.map(lambda j: oracle.decode_alg1_range(*j), jobs))
+            dt2 += time.perf_counter() - t0
+            passes2 += 1
+    for (name, _, w), o in zip(fmts, outs2):
+        assert np.array_equal(o, w.reshape(-1)), name
+    d2 = {"gbs": 2 * elems * passes2 / dt2 / 1e9, "threads": host_cores, "passes": passes2,
+          "seconds": round(dt2, 2)}
+    best = d2 if d2["gbs"] >= d1["gbs"] else d1
+    sample = (f"{len(fmts)} tensor(s) of the workload ({elems} elements: " + ", ".join(n for n, _, _ in fmts) +
+              f"); D1 sequential decode, {d1_threads} thread(s) (one per tensor); D2 Alg. 1 emulation, "
+              f"{host_cores} threads over the format blocks")
+    return {"value": best["gbs"], "unit": UNIT, "cores": best["threads"], "kind": "oracle", "sample": sample,
+            "d1": d1, "d2": d2, "host_cores": host_cores, "cpu_model": cpu_model()}
 
 
 def run_reference(args):
@@ -182,30 +224,58 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
+def selftest_dist(args):
+    """--selftest-dist: the bench's multi-rank host logic on CPU (gloo): rank r pretends to produce
+    (r + 1) GB of BF16 per step in (10 + r) ms per step; rank 0 prints the aggregate and the shard each
+    rank would decode for the 70B (strong) and 405B (weak, shard r of 8) sweeps."""
+    from paper_2504_11651_b200 import shard
+    rank, world, _ = shard.rank_info()
+    shard.init_host_group()
+    shard.barrier()
+    value, tot, ms = shard.aggregate_rate((rank + 1) * 1e9, (10.0 + rank) * args.steps, args.steps)
+    cfg70 = dict(workloads.MODELS["llama70b_model"], block_elems=workloads.config_numel("llama70b_block"))
+    cfg405 = dict(workloads.MODELS["llama405b_model"], block_elems=workloads.config_numel("llama405b_block"))
+    r70, s70 = shard.model_shard(cfg70, rank, world)
+    r405, s405 = shard.model_shard(cfg405, rank, world, weak_shards=8)
+    units70 = shard.sum_over_ranks([len(r70)])[0]
+    mine = {"rank": rank, "llama70b_units": [r70.start, r70.stop], "llama405b_units": [r405.start, r405.stop]}
+    import torch.distributed as dist
+    allmine = [None] * world
+    if world > 1:
+        dist.all_gather_object(allmine, mine)
+    else:
+        allmine = [mine]
+    if rank == 0:
+        print(json.dumps({"selftest": "dist", "n_ranks": world, "value": value, "unit": UNIT,
+                          "bf16_bytes_all_ranks_per_step": tot, "max_ms": ms, "llama70b_units_total": units70,
+                          "scaling": {"llama70b_model": s70, "llama405b_model": s405}, "ranks": allmine}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.selftest_dist:
+        selftest_dist(args)
+        return
     import torch
     import torch.distributed as dist
 
-    from paper_2504_11651_b200 import df11
+    from paper_2504_11651_b200 import df11, shard
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = shard.rank_info()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    shard.init_host_group()                      # gloo on the host; NCCL is never initialised
+    barrier = shard.barrier
+    nvml = shard.nvml_index(dev)
 
     if args.config in workloads.MODELS:
-        run_model(args, df11, dev, rank, world, local, barrier)
+        run_model(args, df11, dev, rank, world, nvml, barrier)
         if world > 1:
             dist.destroy_process_group()
         return
@@ -241,39 +311,63 @@ def main():
         del ref
     bf16_bytes = 2 * N
     algo_bytes = sum(dt.compressed_bytes for dt in dts) + bf16_bytes       # read DF11 + write BF16
+    # ---- L2: a step that moves less than 4x L2 would be served partly from L2 when repeated, so the
+    # timed steps rotate over device copies of the DF11 arrays and outputs (SURVEY 8(d) timing step 2)
+    l2 = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 << 20) or (126 << 20))
+    copies = 1 if algo_bytes >= 4 * l2 else min(32, -(-4 * l2 // algo_bytes))
+    plans = [plan]
+    for c in range(1, copies):
+        cdts = [df11.clone_device_tensor(d) for d in dts]
+        cscratch = torch.empty_like(scratch)
+        couts, o = [], 0
+        for h in hs:
+            couts.append(cscratch[o:o + h.num_elements])
+            o += (h.num_elements + 7) // 8 * 8
+        cp = df11.BlockPlan(cdts, couts)
+        cp.run(kernel=kernel_used)
+        torch.cuda.synchronize()
+        for (name, w), out in zip(tensors, cp.outputs()):
+            if not torch.equal(out.reshape(-1).view(torch.int16),
+                               torch.from_numpy(w.reshape(-1).view(np.int16)).to(dev)):
+                raise SystemExit(f"bit-exact check failed on copy {c} of {name}")
+        plans.append(cp)
+    l2_note = (f"inputs larger than L2: {algo_bytes / 1e6:.0f} MB moved per step vs {l2 / 1e6:.0f} MB L2"
+               if copies == 1 else
+               f"L2 defeated: the timed steps rotate over {copies} device copies of the block "
+               f"({copies * algo_bytes / 1e6:.0f} MB >= 4x the {l2 / 1e6:.0f} MB L2; {algo_bytes / 1e6:.0f} MB per step)")
 
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        plan.run(stream, kernel_used)
+    for i in range(args.warmup):
+        plans[i % copies].run(stream, kernel_used)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     df11.launch_count(reset=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(nvml) as clocks:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
-            plan.run(stream, kernel_used)
+            plans[(args.warmup + i) % copies].run(stream, kernel_used)
             ev[i][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = df11.launch_count()
     barrier()
-    total_ms = t_start.elapsed_time(t_end)
     launch_ms = [a.elapsed_time(b) for a, b in ev]
-    t = torch.tensor([total_ms, float(np.mean(launch_ms))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, avg_launch_ms = float(t[0]), float(t[1])
-    value = world * bf16_bytes * args.steps / (total_ms / 1e3) / 1e9
+    # whole job: sum of every rank's BF16 bytes / the slowest rank's time (gloo reductions on the host)
+    value, tot_bf16, total_ms = shard.aggregate_rate(bf16_bytes, t_start.elapsed_time(t_end), args.steps)
+    avg_launch_ms = shard.max_over_ranks([float(np.mean(launch_ms))])[0]
 
     peak, peak_src = measured_peaks()
     achieved = algo_bytes / (avg_launch_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config, kernel_used), "peak_source": peak_src,
+                "traffic": ncu_traffic(args.config, kernel_used),
+                "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu "
+                                  "--set full capture (profiles/ncu_summary.json), not measured in this run",
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": algo_bytes,
                 "frac_of_nominal_8tbs": achieved / 8000.0,
                 "launch_us": {"mean": avg_launch_ms * 1e3, "median": float(np.median(launch_ms)) * 1e3,
@@ -284,19 +378,17 @@ def main():
     # ---- e2e: through the C ABI with host buffers (pinned H2D of the DF11 arrays, decode, D2H of BF16)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(df11, hs, dts, dev, args.e2e_steps, world, barrier, tensors)
+        e2e = run_e2e(df11, hs, dts, dev, args.e2e_steps, barrier, tensors)
 
     # ---- NEXT-2: CPU->GPU transfer of the same BF16 bytes (the paper's comparator)
     transfer = None
     if not args.no_transfer:
-        transfer = run_transfer(tensors, dev, world, barrier, value)
+        transfer = run_transfer(tensors, dev, barrier, value)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
-            v, cores, sample, secs = oracle_decode_rate(tensors)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-                   "seconds": round(secs, 2)}
+            cpu = oracle_decode_rate(tensors)
         except Exception as exc:                                           # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle", "sample": f"failed: {exc}"}
 
@@ -309,7 +401,7 @@ def main():
                        "bf16_bytes_per_gpu": bf16_bytes, "df11_bytes_per_gpu": algo_bytes - bf16_bytes,
                        "bits_per_weight": 8 * (algo_bytes - bf16_bytes) / N, "T": hs[0].T, "n": hs[0].n,
                        "kernel": kernel_used, "parallelism": f"shard{world} (one block per GPU, no collective)",
-                       "l2": f"inputs larger than L2: {algo_bytes / 1e6:.0f} MB moved per step vs 126 MB L2"},
+                       "bf16_bytes_all_ranks_per_step": tot_bf16, "l2": l2_note, "l2_copies": copies},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -323,7 +415,7 @@ def main():
         dist.destroy_process_group()
 
 
-def run_transfer(tensors, dev, world, barrier, decode_gbs):
+def run_transfer(tensors, dev, barrier, decode_gbs):
     """Pinned host -> device copy of the block's BF16 weights (what DF11 decode replaces when weights
     are offloaded to CPU memory).  Returns GB/s of BF16 delivered and the decode/transfer ratio."""
     import torch
@@ -343,16 +435,14 @@ def run_transfer(tensors, dev, world, barrier, decode_gbs):
             d.copy_(h, non_blocking=True)
     b.record(stream)
     torch.cuda.synchronize()
-    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    from paper_2504_11651_b200 import shard
     nbytes = sum(h.numel() * 2 for h in host)
-    gbs = world * nbytes * reps / (float(ms[0]) / 1e3) / 1e9
+    gbs, _, _ = shard.aggregate_rate(nbytes * reps, a.elapsed_time(b), 1)
     return {"h2d_gbs": gbs, "unit": UNIT, "decode_over_transfer": decode_gbs / gbs,
             "what": "pinned H2D of the block's BF16 weights vs DF11 decode of the same weights on the GPU"}
 
 
-def run_model(args, df11, dev, rank, world, local, barrier):
+def run_model(args, df11, dev, rank, world, nvml, barrier):
     """Whole-model sweeps (BASELINE configs[2] and [4]): the model's transformer blocks (+ embedding,
     LM head) are placed on ranks by plan_shards; a step decodes every block of this rank's shard, one
     df11_decompress_block launch per block into a reused BF16 scratch.
@@ -364,18 +454,15 @@ def run_model(args, df11, dev, rank, world, local, barrier):
     import torch
     import torch.distributed as dist
 
-    from paper_2504_11651_b200.shard import plan_shards
+    from paper_2504_11651_b200.shard import model_shard, model_units
     m = workloads.MODELS[args.config]
     block_cfg = m["block"]
     shapes = workloads.CONFIGS[block_cfg]
-    block_elems = sum(int(np.prod(sh)) for _, sh in shapes)
-    head_elems = m["vocab"] * m["hidden"]
-    units = [head_elems] + [block_elems] * m["blocks"] + [head_elems]      # embed, blocks..., lm_head
-    if args.config == "llama405b_model":
-        shard_world, shard_id, scaling = 8, rank % 8, "weak"
-    else:
-        shard_world, shard_id, scaling = world, rank, "strong"
-    mine = list(plan_shards(units, shard_world)[shard_id])
+    cfg = dict(m, block_elems=sum(int(np.prod(sh)) for _, sh in shapes))
+    units = model_units(cfg)                                               # embed, blocks..., lm_head
+    # 405B: the 8-GPU shard set, rank r decodes shard r of 8 (weak); 70B: the model over N ranks (strong)
+    rng, scaling = model_shard(cfg, rank, world, weak_shards=8 if args.config == "llama405b_model" else 0)
+    mine = list(rng)
     t0 = time.perf_counter()
     # unique encoded units of this rank: up to U blocks + the head/embedding if present
     kinds = []
@@ -436,14 +523,7 @@ def run_model(args, df11, dev, rank, world, local, barrier):
             if nb < len(block_protos):
                 dts = src
             else:                                   # device copy of a verified prototype
-                dts = []
-                for d in src:
-                    c = df11.DeviceTensor.__new__(df11.DeviceTensor)
-                    c.__dict__.update(d.__dict__)
-                    for key in ("encoded_exponent", "packed_sign_mantissa", "gaps", "luts", "code_lengths",
-                                "block_output_pos"):
-                        setattr(c, key, getattr(d, key).clone())
-                    dts.append(c)
+                dts = [df11.clone_device_tensor(d, out=d.out) for d in src]
                 keep.append(dts)
             nb += 1
         else:
@@ -460,7 +540,7 @@ def run_model(args, df11, dev, rank, world, local, barrier):
     barrier()
     torch.cuda.synchronize()
     df11.launch_count(reset=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(nvml) as clocks:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.steps):
@@ -470,10 +550,9 @@ def run_model(args, df11, dev, rank, world, local, barrier):
         torch.cuda.synchronize()
     launches = df11.launch_count()
     barrier()
-    from paper_2504_11651_b200.shard import max_over_ranks, sum_over_ranks
-    ms = max_over_ranks([a.elapsed_time(b)], dev)[0]
-    tot_bf16, tot_algo = sum_over_ranks([bf16_bytes, algo], dev)
-    value = tot_bf16 * args.steps / (ms / 1e3) / 1e9
+    from paper_2504_11651_b200.shard import aggregate_rate, sum_over_ranks
+    value, tot_bf16, ms = aggregate_rate(bf16_bytes, a.elapsed_time(b), args.steps)
+    tot_algo = sum_over_ranks([algo])[0]
     peak, peak_src = measured_peaks()
     achieved = algo * args.steps / (a.elapsed_time(b) / 1e3) / 1e9
     if rank == 0:
@@ -495,9 +574,10 @@ def run_model(args, df11, dev, rank, world, local, barrier):
         }), flush=True)
 
 
-def run_e2e(df11, hs, dts, dev, steps, world, barrier, tensors):
+def run_e2e(df11, hs, dts, dev, steps, barrier, tensors):
     import torch
-    import torch.distributed as dist
+
+    from paper_2504_11651_b200 import shard
     stream = torch.cuda.current_stream()
     pinned_in, host_views, host_outs = [], [], []
     for h in hs:
@@ -546,15 +626,12 @@ def run_e2e(df11, hs, dts, dev, steps, world, barrier, tensors):
         step()
     b.record(stream)
     torch.cuda.synchronize()
-    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     # the last step's host output must be the original weights
     for ho, h, (name, w) in zip(host_outs, hs, tensors):
         got = ho[: h.num_elements].view(torch.int16).numpy().view(np.uint16)
         if not np.array_equal(got, w.reshape(-1)):
             raise SystemExit(f"e2e bit-exact check failed on {name}")
-    value = world * 2 * N * steps / (float(ms[0]) / 1e3) / 1e9
+    value, _, _ = shard.aggregate_rate(2 * N, a.elapsed_time(b), steps)
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "steps": steps, "path": "df11_decompress_host_block (pinned H2D + decode on one stream, D2H overlapped on a second)"}
 

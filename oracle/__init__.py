@@ -11,5 +11,6 @@ Pins: every function here is checked by tests/test_oracle_*.py against the paper
 is listed in DESIGN.md §4.
 """
 from .oracle import (FormatError, build_oracle, compose, compressed_bytes, decode_alg1,  # noqa: F401
-                     decode_alg1_blocks, decode_sequential, encode, entropy_bits, histogram, split)
+                     decode_alg1_blocks, decode_alg1_range, decode_sequential, encode, entropy_bits,
+                     histogram, split)
 from . import huffman  # noqa: F401

@@ -219,6 +219,28 @@ def decode_alg1(fmt: dict, check_counts: bool = True) -> np.ndarray:
     return out
 
 
+def decode_alg1_range(fmt: dict, b0: int, b1: int, out: np.ndarray) -> None:
+    """D2 over format blocks [b0, b1) only, writing their outputs into `out` (the whole tensor's uint16
+    array): the same Alg. 1 emulation as decode_alg1, on views that start at block b0 (BlockOutputPos
+    values are absolute, so outputs land at their final positions).  Lets a caller spread the blocks
+    of one tensor over threads (ctypes releases the GIL); requires 5*T*b0 to be a whole number of
+    bytes (true for T = 256)."""
+    T, n = int(fmt["T"]), int(fmt["n"])
+    if b1 <= b0:
+        return
+    if (5 * T * b0) % 8:
+        raise ValueError("block range start must fall on a byte of the gap stream")
+    s = fmt["encoded_exponent"][b0 * T * n:]
+    g = fmt["gaps"][(5 * T * b0) // 8:]
+    bop = np.ascontiguousarray(fmt["block_output_pos"][b0:b1 + 1])
+    rc = _load().df11o_decode_alg1(
+        _ptr(fmt["luts"]), fmt["lut_entry_bytes"], fmt["k"], _ptr(fmt["code_lengths"]),
+        _ptr(s), s.size, _ptr(g), g.size, _ptr(bop),
+        _ptr(fmt["packed_sign_mantissa"]), b1 - b0, T, n, fmt["num_elements"], 1, _ptr(out))
+    if rc != 0:
+        raise FormatError("corrupt", f"Alg. 1 emulation failed ({rc})")
+
+
 def decode_alg1_blocks(fmt: dict, blocks) -> dict:
     """D2 restricted to the given format blocks: returns {block b: (start, uint16 values)} for
     sampled parity checks at full size.  Runs Alg. 1 on a view containing only those blocks."""

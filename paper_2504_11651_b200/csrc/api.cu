@@ -66,6 +66,9 @@ df11_status validate(const df11_device_tensor &t, uint32_t idx) {
     if (t.lut_entry_bytes != 1 && t.lut_entry_bytes != 2) return bad("lut_entry_bytes must be 1 or 2");
     if (t.k == 0) return bad("k == 0 with N > 0");
     if (t.lut_entry_bytes == 1 && t.k > 17) return bad("narrow LUTs allow at most 17 tables");
+    // a codebook of <= 256 symbols has <= 255 internal nodes, so <= 256 tables; the bound also keeps
+    // every LUT byte offset k * 256 * entry_bytes (<= 128 KB) inside 32-bit arithmetic in the kernels
+    if (t.k > 256) return bad("at most 256 LUTs");
     if ((uint64_t)t.B * t.T * t.n * 8 > (uint64_t)t.num_elements * 32 + (uint64_t)t.T * t.n * 8)
         return bad("B too large for N (codes are at most 32 bits)");
     if (!t.encoded_exponent || !t.packed_sign_mantissa || !t.gaps || !t.luts || !t.code_lengths ||
@@ -314,8 +317,11 @@ extern "C" df11_status df11_decompress_host_block(const df11_host_tensor *hs, co
                 cudaSuccess)
             st = cuda_fail(e, "D2H copy");
     }
-    if (st == DF11_OK && ((e = cudaEventRecord(ev, cs)) != cudaSuccess || (e = cudaStreamWaitEvent(s, ev, 0)) != cudaSuccess))
-        st = cuda_fail(e, "stream join");
+    // join the copy stream back into `stream` on every path (D2H copies already enqueued for earlier
+    // tensors must be covered by a synchronisation of `stream` even when a later tensor failed)
+    if ((e = cudaEventRecord(ev, cs)) != cudaSuccess || (e = cudaStreamWaitEvent(s, ev, 0)) != cudaSuccess) {
+        if (st == DF11_OK) st = cuda_fail(e, "stream join");
+    }
     cudaEventDestroy(ev);                            // released once the pending work completes
     return st;
 }

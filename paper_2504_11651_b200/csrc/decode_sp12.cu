@@ -459,7 +459,12 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     }
                 }
 #endif
-                // the last warp done with this tile's buffer stages the group's next tile into it
+#ifndef SP12_SM_BARRIER
+                // the last warp done with this tile's buffer stages the group's next tile into it.
+                // Ordering: each warp's reads of the buffer are complete before its
+                // lane 0 passes __syncwarp; the warp's fence + relaxed atomic increment publish that, the
+                // last incrementer's fence orders all four warps' reads before its proxy fence, and
+                // fence.proxy.async orders those generic-proxy reads before the async-proxy TMA write.
                 __syncwarp();
                 if (lane == 0) {
                     __threadfence_block();
@@ -472,6 +477,14 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                         if (has_next) stage_sm(nlo, nhi);
                     }
                 }
+#else
+                // A/B reference for the race evidence: a group barrier instead of the atomic hand-off
+                group_bar(g);
+                if (t == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if (has_next) stage_sm(nlo, nhi);
+                }
+#endif
             } else {
                 if (edge) out[es] = compose_r(ld8(wreg + (es - F)), __ldg(ts.packed_sign_mantissa + es));
                 for (uint32_t u = ua + lane; u < ub; u += 32) {

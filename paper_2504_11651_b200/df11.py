@@ -316,6 +316,17 @@ class DeviceTensor:
                                             self.luts, self.code_lengths, self.block_output_pos))
 
 
+def clone_device_tensor(d: "DeviceTensor", out=None) -> "DeviceTensor":
+    """A second device copy of a DF11 tensor (same format, fresh buffers; a new BF16 output unless
+    `out` is given): e.g. to rotate over copies larger than L2 in timing loops."""
+    c = DeviceTensor.__new__(DeviceTensor)
+    c.__dict__.update(d.__dict__)
+    for key in ("encoded_exponent", "packed_sign_mantissa", "gaps", "luts", "code_lengths", "block_output_pos"):
+        setattr(c, key, getattr(d, key).clone())
+    c.out = out if out is not None else d.out.clone()
+    return c
+
+
 def _u16_dtypes():
     import torch
     return (torch.bfloat16, torch.int16, torch.uint16)
@@ -440,15 +451,25 @@ def _dev_u16(x):
     return x.contiguous()
 
 
+def _on(stream):
+    """Context in which torch allocations, copies and read-backs run on `stream` (the current stream
+    when None), so that buffers the library fills on that stream are ordered with everything around
+    them (allocations are tied to the stream by the caching allocator)."""
+    import contextlib
+    import torch
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
 def histogram_device(x, out=None, stream=None):
     """df11_histogram_device: exponent histogram of a device BF16 tensor, accumulated into `out`
-    (int64[256] on the same device; zeroed when created here)."""
+    (int64[256] on the same device; zeroed when created here).  Everything runs on `stream`."""
     import torch
-    x = _dev_u16(x)
-    if out is None:
-        out = torch.zeros(256, dtype=torch.int64, device=x.device)
-    _check(lib().df11_histogram_device(ctypes.c_void_p(x.data_ptr()), x.numel(), ctypes.c_void_p(out.data_ptr()),
-                                       _stream_ptr(stream)))
+    with _on(stream):
+        x = _dev_u16(x)
+        if out is None:
+            out = torch.zeros(256, dtype=torch.int64, device=x.device)
+        _check(lib().df11_histogram_device(ctypes.c_void_p(x.data_ptr()), x.numel(),
+                                           ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
     return out
 
 
@@ -457,14 +478,19 @@ def encode_device(x, T: int = 256, n: int = 8, lut_mode: str = "auto", codebook_
     """GPU encoder: device BF16 tensor -> DeviceTensor (histogram on the GPU, codebook on the host,
     packing on the GPU).  Byte-identical to encode(x.cpu()) with the same options; with
     `codebook_hist` (host, 256 bins, e.g. a group's summed histogram) the codebook is built from it."""
-    import torch
-    x = _dev_u16(x)
-    th = histogram_device(x, stream=stream).cpu().numpy().view(np.uint64)   # synchronises
+    with _on(stream):
+        x = _dev_u16(x)
+        th = histogram_device(x, stream=stream).cpu().numpy().view(np.uint64)   # read back on `stream`
     plan = EncodePlan(th if codebook_hist is None else codebook_hist, th, T, n, lut_mode)
     return encode_device_with_plan(x, plan, stream=stream, out=out)
 
 
 def encode_device_with_plan(x, plan: EncodePlan, stream=None, out=None) -> "DeviceTensor":
+    with _on(stream):
+        return _encode_device_with_plan(x, plan, stream, out)
+
+
+def _encode_device_with_plan(x, plan, stream, out):
     import torch
     x = _dev_u16(x)
     if x.numel() != plan.num_elements:
@@ -502,8 +528,9 @@ def encode_device_group(xs, T: int = 256, n: int = 8, lut_mode: str = "auto", sh
                         stream=None):
     """GPU encoder for a group of tensors (e.g. one transformer block); shared_codebook builds one
     codebook from the summed histogram (R5)."""
-    hists = [histogram_device(x, stream=stream) for x in xs]
-    hs = [h.cpu().numpy().view(np.uint64) for h in hists]
+    with _on(stream):
+        hists = [histogram_device(x, stream=stream) for x in xs]
+        hs = [h.cpu().numpy().view(np.uint64) for h in hists]
     total = np.sum(np.stack(hs), axis=0, dtype=np.uint64) if hs else np.zeros(256, np.uint64)
     res = []
     for x, h in zip(xs, hs):

@@ -12,12 +12,6 @@ import workloads
 from conftest import load_golden
 
 
-def _rescan_gaps_bop(fmt):
-    """Definition recomputed with numpy from the code lengths of the input."""
-    lengths = fmt["code_lengths"].astype(np.int64)
-    return lengths
-
-
 def _check_metadata(oracle_mod, w, fmt):
     T, n, B, N = fmt["T"], fmt["n"], fmt["B"], fmt["num_elements"]
     exp, _ = oracle_mod.split(w)

@@ -51,6 +51,7 @@ CONFIGS = {
     "flux_double_block": _flux_double_block(),
     "flux_single_block": _flux_single_block(),
     "llama70b_embed": [("embed_tokens", (128256, 8192))],
+    "llama405b_embed": [("embed_tokens", (128256, 16384))],      # 2.10 G elements: positions past 2^30
 }
 
 # BASELINE.json configs -> workload names
