@@ -26,7 +26,7 @@ def df11():
 
 
 def _sampled_blocks(B):
-    return sorted({0, 1, B // 3, B // 2, (2 * B) // 3, max(B - 2, 0), B - 1})
+    return sorted(b for b in {0, 1, B // 3, B // 2, (2 * B) // 3, B - 2, B - 1} if 0 <= b < B)
 
 
 @pytest.mark.parametrize("config", ["flux_double_block", "llama70b_block", "llama405b_block", "llama405b_embed"])
@@ -45,9 +45,9 @@ def test_full_size_config(df11, oracle_mod, config):
         ws.append(w)
     before = df11.launch_count()
     outs = df11.decompress_block(dts, kernel="auto")
-    assert df11.launch_count() - before == 1          # one launch for the whole block
-    assert df11.last_kernels() == {"fast"}
     torch.cuda.synchronize()
+    assert df11.launch_count() - before == 1, "one launch for the whole block (P:157)"
+    assert df11.last_kernels() == {"fast"}
     for name, w, o, h in zip(names, ws, outs, hs):
         ref = torch.from_numpy(w.reshape(-1).view(np.int16)).to(dev)
         got = o.reshape(-1).view(torch.int16)
