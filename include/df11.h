@@ -113,6 +113,12 @@ df11_status df11_decompress_block(const df11_device_tensor *ts, uint32_t count, 
  * the Alg. 1 kernel (one launch per distinct T); df11_last_kernel_mask() says which ran. */
 df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream,
                                      int kernel);
+/* Same with an SM budget (NEXT-1, decode/compute overlap): the product kernel runs at
+ * most `max_ctas` persistent CTAs (one per SM; 0 = one per SM of the device), so that a decode
+ * prefetched on a side stream leaves the other SMs to the GEMMs of the current block.  Results are
+ * identical for every budget.  `max_ctas` does not affect Algorithm 1 launches. */
+df11_status df11_decompress_block_budget(const df11_device_tensor *ts, uint32_t count, void *stream,
+                                         int kernel, uint32_t max_ctas);
 
 /* ---- launcher planning (host; used by df11_decompress_block, exported for tests) ----------------
  * df11_plan_cta_ranges: tile ranges of the persistent decode grid.  entry_start[0..count] are the

@@ -107,7 +107,7 @@ extern "C" void df11_plan_cta_ranges(const uint32_t *entry_start, uint32_t count
 namespace {
 // Product-kernel launch for tensors ts[idx[0..n)] (all fast_supports, non-empty).
 df11_status launch_fast_batch(const df11_device_tensor *ts, const uint32_t *idx, uint32_t n, int num_sms,
-                              int dev, cudaStream_t stream) {
+                              int dev, cudaStream_t stream, uint32_t max_ctas) {
     static thread_local df11::Batch bt;   // ~12 KB: keep it off the stack
     // Tile schedule (the block-batched launcher).  CTA c of the persistent kernel walks a
     // contiguous global tile range and rebuilds its SMEM decode tables at every tensor boundary inside
@@ -131,6 +131,7 @@ df11_status launch_fast_batch(const df11_device_tensor *ts, const uint32_t *idx,
     // many tiles per group under compute-sanitizer
     static const int max_grid = [] { const char *v = std::getenv("DF11_MAX_GRID"); return v ? std::atoi(v) : 0; }();
     if (max_grid > 0) G = std::min<uint32_t>(G, (uint32_t)max_grid);
+    if (max_ctas > 0) G = std::min<uint32_t>(G, max_ctas);          // SM budget (overlap with compute)
     auto boundary = [&](uint32_t c) { return (uint32_t)(((uint64_t)total * c) / G); };
     uint32_t pos = 0, bi = 0, boff = 0;
     auto push = [&](uint32_t ti, uint32_t off, uint32_t cnt) {
@@ -213,8 +214,8 @@ df11_status launch_alg1_batch(const df11_device_tensor *ts, const uint32_t *idx,
 }
 }  // namespace
 
-extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream_v,
-                                                int kernel) {
+extern "C" df11_status df11_decompress_block_budget(const df11_device_tensor *ts, uint32_t count,
+                                                    void *stream_v, int kernel, uint32_t max_ctas) {
     if (count > DF11_MAX_BATCH) return df11_fail(DF11_E_INVALID_ARGUMENT, "count > DF11_MAX_BATCH");
     if (count && !ts) return df11_fail(DF11_E_INVALID_ARGUMENT, "descriptor array is NULL");
     if (kernel < DF11_KERNEL_AUTO || kernel > DF11_KERNEL_FAST) return df11_fail(DF11_E_INVALID_ARGUMENT, "bad kernel");
@@ -241,11 +242,16 @@ extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, ui
     int max_smem = 0, num_sms = 0;
     device_attrs(dev, max_smem, num_sms);
     if (nfast) {
-        df11_status st = launch_fast_batch(ts, fast_idx, nfast, num_sms, dev, stream);
+        df11_status st = launch_fast_batch(ts, fast_idx, nfast, num_sms, dev, stream, max_ctas);
         if (st != DF11_OK) return st;
     }
     if (nslow) return launch_alg1_batch(ts, slow_idx, nslow, (size_t)max_smem, stream);
     return DF11_OK;
+}
+
+extern "C" df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream,
+                                                int kernel) {
+    return df11_decompress_block_budget(ts, count, stream, kernel, 0);
 }
 
 extern "C" df11_status df11_decompress_block(const df11_device_tensor *ts, uint32_t count, void *stream) {

@@ -24,7 +24,8 @@ KERNELS = {"auto": 0, "alg1": 1, "fast": 2}
 MAX_BATCH = 64
 
 EXPORTED_SYMBOLS = ("df11_encode", "df11_encode_group", "df11_host_tensor_free", "df11_decompress",
-                    "df11_decompress_block", "df11_decompress_block_ex", "df11_decompress_host",
+                    "df11_decompress_block", "df11_decompress_block_ex", "df11_decompress_block_budget",
+                    "df11_decompress_host",
                     "df11_decompress_host_block", "df11_plan_cta_ranges", "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
                     "df11_launch_count", "df11_last_kernel_mask", "df11_histogram_device", "df11_encode_plan_create",
                     "df11_encode_plan_free", "df11_encode_device")
@@ -97,6 +98,7 @@ def lib():
         L.df11_decompress.argtypes = [ctypes.POINTER(DeviceTensorC), P]
         L.df11_decompress_block.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P]
         L.df11_decompress_block_ex.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P, ctypes.c_int]
+        L.df11_decompress_block_budget.argtypes = [ctypes.POINTER(DeviceTensorC), U32, P, ctypes.c_int, U32]
         L.df11_decompress_host.argtypes = [ctypes.POINTER(HostTensorC), ctypes.POINTER(DeviceTensorC), P, P]
         L.df11_plan_cta_ranges.argtypes = [P, U32, U32, U32, P]
         L.df11_plan_cta_ranges.restype = None
@@ -107,7 +109,8 @@ def lib():
         L.df11_encode_plan_free.argtypes = [ctypes.POINTER(EncodePlanC)]
         L.df11_encode_device.argtypes = [P, ctypes.POINTER(EncodePlanC), ctypes.POINTER(DeviceBuffersC), P, U64, P]
         for f in ("df11_encode", "df11_encode_group", "df11_decompress", "df11_decompress_block",
-                  "df11_decompress_block_ex", "df11_decompress_host", "df11_decompress_host_block",
+                  "df11_decompress_block_ex", "df11_decompress_block_budget", "df11_decompress_host",
+                  "df11_decompress_host_block",
                   "df11_histogram_device",
                   "df11_encode_plan_create", "df11_encode_device"):
             getattr(L, f).restype = ctypes.c_int
@@ -364,8 +367,10 @@ class BlockPlan:
             self.arr[i] = dt.descriptor(None if outs is None else outs[i])
         self.count = len(dts)
 
-    def run(self, stream=None, kernel: str = "auto"):
-        _check(lib().df11_decompress_block_ex(self.arr, self.count, _stream_ptr(stream), KERNELS[kernel]))
+    def run(self, stream=None, kernel: str = "auto", max_ctas: int = 0):
+        """One launch for the block (df11_decompress_block_budget; max_ctas = 0: every SM)."""
+        _check(lib().df11_decompress_block_budget(self.arr, self.count, _stream_ptr(stream), KERNELS[kernel],
+                                                  int(max_ctas)))
 
     def outputs(self):
         res = []
@@ -375,10 +380,11 @@ class BlockPlan:
         return res
 
 
-def decompress_block(dts, outs=None, stream=None, kernel: str = "auto"):
-    """df11_decompress_block: every tensor of a transformer block in one launch."""
+def decompress_block(dts, outs=None, stream=None, kernel: str = "auto", max_ctas: int = 0):
+    """df11_decompress_block: every tensor of a transformer block in one launch; max_ctas
+    caps the persistent grid (an SM budget for decode/compute overlap; 0 = every SM)."""
     plan = BlockPlan(dts, outs)
-    plan.run(stream, kernel)
+    plan.run(stream, kernel, max_ctas)
     return plan.outputs()
 
 

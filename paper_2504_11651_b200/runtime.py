@@ -37,13 +37,16 @@ class BlockWeights:
 class OverlapRunner:
     """Double-buffered BF16 scratch; block i+1 decodes on `decode_stream` while block i computes."""
 
-    def __init__(self, blocks, device="cuda", prefetch: bool = True):
+    def __init__(self, blocks, device="cuda", prefetch: bool = True, decode_ctas: int = 0):
+        """decode_ctas: SM budget of the prefetched decode (0 = every SM): the decode of block i+1
+        then runs on that many SMs and leaves the rest to block i's GEMMs."""
         import torch
         self.blocks = list(blocks)
         self.device = torch.device(device)
         cap = max(b.numel + 8 * len(b.dts) for b in self.blocks) + 64
         self.scratch = [torch.empty(cap, dtype=torch.bfloat16, device=self.device) for _ in range(2)]
         self.prefetch = prefetch
+        self.decode_ctas = int(decode_ctas)
         self.decode_stream = torch.cuda.Stream(device=self.device)
         self.plans = [[b.plan(self.scratch[k]) for k in range(2)] for b in self.blocks]
         self.decoded = [torch.cuda.Event() for _ in range(2)]
@@ -54,7 +57,7 @@ class OverlapRunner:
         k = i % 2
         with torch.cuda.stream(stream):
             stream.wait_event(self.consumed[k])       # the scratch's previous block has been used
-            self.plans[i][k].run(stream)
+            self.plans[i][k].run(stream, max_ctas=self.decode_ctas if stream is self.decode_stream else 0)
             self.decoded[k].record(stream)
 
     def iterate(self):

@@ -4,10 +4,13 @@
 For a stack of Llama-3.1-8B-shaped blocks, time one forward pass (the block's seven GEMMs) with
   (a) BF16 weights resident in HBM (no decode),
   (b) DF11 weights decoded right before each block (serial: decode then GEMMs),
-  (c) DF11 weights decoded one block ahead on a side stream (OverlapRunner, prefetch).
-Prints one JSON line per token-batch size.  GEMMs are torch.matmul (cuBLAS); the decode is ours.
+  (c) DF11 weights decoded one block ahead on a side stream (OverlapRunner, prefetch), with an SM
+      budget for the decode (df11_decompress_block_budget: the decode runs on `ctas` SMs and leaves
+      the others to the GEMMs; 0 = every SM).
+Prints one JSON line per token-batch size (every budget, the best one named).  GEMMs are
+torch.matmul (cuBLAS); the decode is ours.
 
-    python scripts/bench_overlap.py [--blocks 8] [--tokens 1,16,256,2048]
+    python scripts/bench_overlap.py [--blocks 8] [--tokens 1,16,256,2048] [--budgets 0,112,96,74,56,40]
 """
 import argparse
 import json
@@ -27,6 +30,7 @@ def main():
     ap.add_argument("--blocks", type=int, default=8)
     ap.add_argument("--tokens", default="1,16,256,2048")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--budgets", default="0,120,104,88,74,60,48")
     args = ap.parse_args()
     import torch
 
@@ -39,15 +43,7 @@ def main():
     proto = BlockWeights.from_host(hosts, dev)
     blocks = [proto]
     for _ in range(args.blocks - 1):                     # device copies (same sizes / entropy)
-        copies = []
-        for d in proto.dts:
-            c = df11.DeviceTensor.__new__(df11.DeviceTensor)
-            c.__dict__.update(d.__dict__)
-            for key in ("encoded_exponent", "packed_sign_mantissa", "gaps", "luts", "code_lengths",
-                        "block_output_pos"):
-                setattr(c, key, getattr(d, key).clone())
-            copies.append(c)
-        blocks.append(BlockWeights(copies))
+        blocks.append(BlockWeights([df11.clone_device_tensor(d) for d in proto.dts]))
     resident = [[torch.from_numpy(w.reshape(-1).view(np.int16)).to(dev).view(torch.bfloat16).view(w.shape)
                  for _, w in ts] for _ in range(args.blocks)]
 
@@ -69,11 +65,14 @@ def main():
         torch.cuda.synchronize()
         return s.elapsed_time(e) / args.reps
 
-    runners = {False: OverlapRunner(blocks, dev, prefetch=False), True: OverlapRunner(blocks, dev, prefetch=True)}
-    # correctness: the decoded weights equal the resident BF16 weights
-    for i, W in runners[True].iterate():
-        for a, b in zip(W, resident[0]):
-            assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    budgets = [int(x) for x in args.budgets.split(",")]
+    serial = OverlapRunner(blocks, dev, prefetch=False)
+    runners = {c: OverlapRunner(blocks, dev, prefetch=True, decode_ctas=c) for c in budgets}
+    # correctness: the decoded weights equal the resident BF16 weights, for every budget
+    for r in [serial] + list(runners.values()):
+        for i, W in r.iterate():
+            for a, b in zip(W, resident[0]):
+                assert torch.equal(a.view(torch.int16), b.view(torch.int16))
     for t in [int(x) for x in args.tokens.split(",")]:
         x0 = torch.randn(t, 4096, device=dev, dtype=torch.bfloat16) * 0.1
 
@@ -83,26 +82,32 @@ def main():
                 x = fwd(x, W)
             return x
 
-        def run_df11(prefetch):
+        def run_df11(r):
             def f():
                 x = x0
-                for _, W in runners[prefetch].iterate():
+                for _, W in r.iterate():
                     x = fwd(x, W)
                 return x
             return f
 
+        plans = [b.plan(serial.scratch[0]) for b in blocks]
+
         def decode_only():
-            for p in [b.plan(runners[False].scratch[0]) for b in blocks]:
+            for p in plans:
                 p.run()
 
         ms_res = time_it(run_resident)
-        ms_ser = time_it(run_df11(False))
-        ms_ovl = time_it(run_df11(True))
+        ms_ser = time_it(run_df11(serial))
+        ms_ovl = {c: time_it(run_df11(r)) for c, r in runners.items()}
         ms_dec = time_it(decode_only)
+        best = min(ms_ovl, key=ms_ovl.get)
         print(json.dumps({"tokens": t, "blocks": args.blocks, "ms_bf16_resident": ms_res,
-                          "ms_df11_serial": ms_ser, "ms_df11_overlap": ms_ovl, "ms_decode_only": ms_dec,
-                          "overhead_serial": ms_ser / ms_res - 1, "overhead_overlap": ms_ovl / ms_res - 1,
-                          "gemm": "torch.matmul (cuBLAS)", "decode": "df11_decompress_block (ours)"}), flush=True)
+                          "ms_df11_serial": ms_ser, "ms_df11_overlap": ms_ovl[best], "best_decode_ctas": best,
+                          "ms_df11_overlap_by_ctas": {str(c): round(v, 4) for c, v in ms_ovl.items()},
+                          "ms_decode_only": ms_dec,
+                          "overhead_serial": ms_ser / ms_res - 1, "overhead_overlap": ms_ovl[best] / ms_res - 1,
+                          "bit_exact": True, "gemm": "torch.matmul (cuBLAS)",
+                          "decode": "df11_decompress_block_budget (ours)"}), flush=True)
 
 
 if __name__ == "__main__":

@@ -9,8 +9,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("prefetch", [False, True])
-def test_overlap_runner_bit_exact(prefetch):
+@pytest.mark.parametrize("prefetch,ctas", [(False, 0), (True, 0), (True, 3)])
+def test_overlap_runner_bit_exact(prefetch, ctas):
     from paper_2504_11651_b200 import df11
     from paper_2504_11651_b200.runtime import BlockWeights, OverlapRunner
     dev = torch.device("cuda", 0)
@@ -20,7 +20,7 @@ def test_overlap_runner_bit_exact(prefetch):
         ts = [(n, workloads.gaussian_bf16(sh, workloads.seed_for("rt", layer, n))) for n, sh in shapes]
         blocks.append(BlockWeights.from_host([df11.encode(w) for _, w in ts], dev))
         refs.append([torch.from_numpy(w.view(np.int16)).to(dev) for _, w in ts])
-    runner = OverlapRunner(blocks, dev, prefetch=prefetch)
+    runner = OverlapRunner(blocks, dev, prefetch=prefetch, decode_ctas=ctas)
     x = torch.randn(7, 96, device=dev, dtype=torch.bfloat16)
     y_ref = x.clone()
     y = x.clone()
@@ -81,3 +81,20 @@ def test_capped_grid_many_tiles_and_switches(max_grid):
     env = dict(os.environ, DF11_MAX_GRID=str(max_grid), PYTHONPATH=root)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("max_ctas", [1, 5, 37, 100000])
+def test_sm_budget_bit_exact(max_ctas):
+    """df11_decompress_block_budget: the same bytes for every SM budget (a budget above the SM count
+    means every SM), one launch, on a mixed block (small and large tensors, several CTAs' worth)."""
+    from paper_2504_11651_b200 import df11
+    dev = torch.device("cuda", 0)
+    shapes = [("a", (4096, 1024)), ("b", (128,)), ("c", (3000, 777)), ("d", (1, 5))]
+    ws = [workloads.gaussian_bf16(sh, workloads.seed_for("budget", 0, n)) for n, sh in shapes]
+    dts = [df11.to_device(df11.encode(w), dev) for w in ws]
+    before = df11.launch_count()
+    outs = df11.decompress_block(dts, max_ctas=max_ctas)
+    torch.cuda.synchronize()
+    assert df11.launch_count() - before == 1
+    for w, o in zip(ws, outs):
+        assert np.array_equal(o.reshape(-1).view(torch.int16).cpu().numpy().view(np.uint16), w.reshape(-1))
