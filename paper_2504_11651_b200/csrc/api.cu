@@ -17,7 +17,6 @@
 namespace df11 {
 cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
-cudaError_t launch_wt(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 bool fast_supports(const df11_device_tensor &t);
 uint32_t fast_grid(uint32_t total_tiles, int num_sms);
 }  // namespace df11
@@ -122,11 +121,7 @@ df11_status launch_fast_batch(const df11_device_tensor *ts, const uint32_t *idx,
         (ts[i].B < kSmall ? small[nsmall++] : big[nbig++]) = i;
         total += ts[i].B;
     }
-#ifdef DF11_WT
-    uint32_t G = std::min<uint32_t>((uint32_t)num_sms, (total + 31) / 32);
-#else
     uint32_t G = df11::fast_grid(total, num_sms);
-#endif
     // DF11_MAX_GRID (debug knob, read once): cap the persistent grid, e.g. so that a small input walks
     // many tiles per group under compute-sanitizer
     static const int max_grid = [] { const char *v = std::getenv("DF11_MAX_GRID"); return v ? std::atoi(v) : 0; }();
@@ -175,11 +170,7 @@ df11_status launch_fast_batch(const df11_device_tensor *ts, const uint32_t *idx,
     }
     const uint32_t kpow[12] = {1u << 12, 1u << 4, 1u << 8, 8u, 0, 0, 0, 0, 0, 0, 0, 0};
     std::memcpy(bt.kpow, kpow, sizeof(kpow));
-#ifdef DF11_WT
-    cudaError_t e = df11::launch_wt(bt, dev, stream, &g_launches);
-#else
     cudaError_t e = df11::launch_sp12(bt, dev, stream, &g_launches);
-#endif
     if (e != cudaSuccess) return cuda_fail(e, "fast decode launch");
     g_kernel_mask |= 2u;
     return DF11_OK;
