@@ -39,6 +39,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default=workloads.BASELINE_CONFIGS[1])
     p.add_argument("--kernel", choices=["auto", "alg1", "fast"], default="auto")
+    p.add_argument("--format", choices=["256x8", "128x16"], default="256x8",
+                   help="DF11 format parameters T x n (P:138: n = 8; 128x16 halves the gap bits, NEXT-4)")
     p.add_argument("--dist", choices=["gauss", "t5", "sigma-lu"], default="gauss",
                    help="weight distribution: gauss = the headline recipe; t5 / sigma-lu = realism variants")
     p.add_argument("--no-e2e", action="store_true")
@@ -284,7 +286,8 @@ def main():
     tensors = workloads.config_tensors(args.config, layer=rank, dist=args.dist)
     # host encoder threads: share the host's cores among the ranks of this node
     enc_threads = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", str(world))))
-    hs = [df11.encode(w, num_threads=enc_threads) for _, w in tensors]
+    fT, fn = (int(v) for v in args.format.split("x"))
+    hs = [df11.encode(w, T=fT, n=fn, num_threads=enc_threads) for _, w in tensors]
     N = sum(h.num_elements for h in hs)
     scratch = torch.empty(N + 64, dtype=torch.bfloat16, device=dev)        # reused BF16 scratch
     outs, o = [], 0
@@ -400,6 +403,7 @@ def main():
             "config": {"workload": args.config, "dist": args.dist, "tensors": len(hs), "elements_per_gpu": N,
                        "bf16_bytes_per_gpu": bf16_bytes, "df11_bytes_per_gpu": algo_bytes - bf16_bytes,
                        "bits_per_weight": 8 * (algo_bytes - bf16_bytes) / N, "T": hs[0].T, "n": hs[0].n,
+                       "format": args.format,
                        "kernel": kernel_used, "parallelism": f"shard{world} (one block per GPU, no collective)",
                        "bf16_bytes_all_ranks_per_step": tot_bf16, "l2": l2_note, "l2_copies": copies},
             "roofline": roofline,

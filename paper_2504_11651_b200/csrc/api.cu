@@ -225,7 +225,8 @@ extern "C" df11_status df11_decompress_block_budget(const df11_device_tensor *ts
     if (total >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "batch has >= 2^32 format blocks");
     if (kernel == DF11_KERNEL_FAST && nslow)
         return df11_fail(DF11_E_UNSUPPORTED,
-                         "fast kernel: a tensor is outside its parameter range (T=256, n=8, 16-byte aligned buffers)");
+                         "fast kernel: a tensor is outside its parameter range (T=256, n=8 or T=128, n=16; 16-byte "
+                         "aligned buffers)");
     cudaStream_t stream = (cudaStream_t)stream_v;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -233,8 +234,17 @@ extern "C" df11_status df11_decompress_block_budget(const df11_device_tensor *ts
     int max_smem = 0, num_sms = 0;
     device_attrs(dev, max_smem, num_sms);
     if (nfast) {
-        df11_status st = launch_fast_batch(ts, fast_idx, nfast, num_sms, dev, stream, max_ctas);
-        if (st != DF11_OK) return st;
+        // one product launch per chunk size (n = 8 and n = 16 tensors take different kernel builds)
+        uint32_t n8[DF11_MAX_BATCH], n16[DF11_MAX_BATCH], k8 = 0, k16 = 0;
+        for (uint32_t k = 0; k < nfast; k++) (ts[fast_idx[k]].n == 16 ? n16[k16++] : n8[k8++]) = fast_idx[k];
+        if (k8) {
+            df11_status st = launch_fast_batch(ts, n8, k8, num_sms, dev, stream, max_ctas);
+            if (st != DF11_OK) return st;
+        }
+        if (k16) {
+            df11_status st = launch_fast_batch(ts, n16, k16, num_sms, dev, stream, max_ctas);
+            if (st != DF11_OK) return st;
+        }
     }
     if (nslow) return launch_alg1_batch(ts, slow_idx, nslow, (size_t)max_smem, stream);
     return DF11_OK;

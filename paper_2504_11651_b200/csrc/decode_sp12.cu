@@ -72,6 +72,10 @@ static_assert(kOffGrp % 16 == 0 && kGSm % 16 == 0 && kGReg % 16 == 0 && kWarpReg
 static_assert(kWarps12 * kWarpReg12 >= 8192, "first-code table scratch fits group 0's warp regions");
 static_assert(kSmem12 <= 232448, "SMEM budget");
 
+// kNB = 8: the paper's format (T = 256, n = 8); a lane decodes two 8-byte chunks as two chains.
+// kNB = 16: T = 128, n = 16 (NEXT-4: half the gap bits); a format block has the same 2 048 stream
+// bytes and a lane decodes its one 16-byte chunk as one chain in a 160-bit buffer.
+template <uint32_t kNB>
 __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__ Batch bt) {
     const uint32_t tid = threadIdx.x;
     const uint32_t g = tid / kLanes;
@@ -125,7 +129,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         if (tile < seg_end) {
             nlo = __ldg(ts.block_output_pos + tile - base_tile);
             nhi = __ldg(ts.block_output_pos + tile - base_tile + 1);
-            if (t == 0) issue_tile(ts, tile - base_tile, stage, mbar);
+            if (t == 0) {
+                if constexpr (kNB == 8) issue_tile(ts, tile - base_tile, stage, mbar);
+                else issue_tile16(ts, tile - base_tile, stage, mbar);
+            }
         }
         bool safe, lut_in_smem;
         const bool long_codes = build_t12<kCta12>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen, kOffGrp + kGReg, tid,
@@ -177,15 +184,25 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             {
                 lds128(stage + t * 16, r0, r1, r2, r3);
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r4) : "r"(stage + t * 16 + 16));
-                const uint32_t gb0 = stage + kChunkBytes + ((t * 10) >> 3);
-                // gaps of chunks 2t, 2t+1 and 2t+2 (the next tile's first for t = 127: the stage holds
-                // 16 bytes of gaps past the tile) start at bit 10t
-                const uint32_t h0 = ld8(gb0), h1 = ld8(gb0 + 1), h2 = ld8(gb0 + 2), h3 = ld8(gb0 + 3);
-                const uint32_t g32 = (h0 << 24) | (h1 << 16) | (h2 << 8) | h3;
-                const uint32_t g15 = (g32 >> (17u - ((t * 10) & 7u))) & 32767u;
-                gapA = g15 >> 10;
-                gapB = (g15 >> 5) & 31u;
-                gapC = g15 & 31u;
+                if constexpr (kNB == 8) {
+                    const uint32_t gb0 = stage + kChunkBytes + ((t * 10) >> 3);
+                    // gaps of chunks 2t, 2t+1 and 2t+2 (the next tile's first for t = 127: the stage
+                    // holds 16 bytes of gaps past the tile) start at bit 10t
+                    const uint32_t h0 = ld8(gb0), h1 = ld8(gb0 + 1), h2 = ld8(gb0 + 2), h3 = ld8(gb0 + 3);
+                    const uint32_t g32 = (h0 << 24) | (h1 << 16) | (h2 << 8) | h3;
+                    const uint32_t g15 = (g32 >> (17u - ((t * 10) & 7u))) & 32767u;
+                    gapA = g15 >> 10;
+                    gapB = (g15 >> 5) & 31u;
+                    gapC = g15 & 31u;
+                } else {
+                    // gaps of chunks t and t+1 start at bit 5t (gapB: the end of this lane's chain)
+                    const uint32_t gb0 = stage + kChunkBytes + ((t * 5) >> 3);
+                    const uint32_t g24 = (ld8(gb0) << 16) | (ld8(gb0 + 1) << 8) | ld8(gb0 + 2);
+                    const uint32_t g10 = (g24 >> (14u - ((t * 5) & 7u))) & 1023u;
+                    gapA = g10 >> 5;
+                    gapB = g10 & 31u;
+                    gapC = 0;
+                }
             }
             const uint32_t lo = min(clo, N);
             const uint32_t hi = min(max(min(chi, N), lo), lo + 8 * kN * kT);
@@ -193,75 +210,159 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                            W4 = bswap32(r4);
 
             uint32_t cntA, cntB;
-            if (!safe) {
-                // ---- single decode pass into the private slots (chains A: [gapA, 64), B: [64+gapB, 128))
-                // exact chain ends when the next chunk's gap marks a code start (every tile but the
-                // one holding the tensor's last code): A = [gapA, 64 + gapB), B = [64 + gapB, 128 + gapC),
-                // enforced by one-bits after the end; otherwise [.., 64) / [.., 128) + walk back
-                const bool exact = long_codes && hi < N;
-                const uint32_t limA = exact ? 64u + gapB - gapA : 64u - gapA;
-                const uint32_t limB = exact ? 64u + gapC - gapB : 64u - gapB;
-                uint32_t aA = W0, bA = W1, cA = exact ? W2 | (0xFFFFFFFFu >> gapB) : W2;
-                uint32_t aB = W2, bB = W3, cB = exact ? W4 | (0xFFFFFFFFu >> gapC) : W4;
-                shift96_ones(aA, bA, cA, gapA);
-                shift96_ones(aB, bB, cB, gapB);
-                uint32_t xA = kXEnd - limA, xB = kXEnd - limB;   // see kXEnd
-                Slot oA, oB;
-                slot_init(oA, slotA);
-                slot_init(oB, slotB);
-                uint32_t hA = 1, hB = 1;
-                auto step = [&]() {
-                    uint32_t lA, lB;
-                    lds64(t12_addr(aA, tab, K_ROW, K_TOP, K_ENT), lA, hA);
-                    lds64(t12_addr(aB, tab, K_ROW, K_TOP, K_ENT), lB, hB);
-                    pack(oA, lA, hA, K_S24);
-                    pack(oB, lB, hB, K_S24);
-                    xA += hA;
-                    xB += hB;
-                    shift96_ones(aA, bA, cA, hA);
-                    shift96_ones(aB, bB, cB, hB);
-                };
-#pragma unroll
-                for (int u = 0; u < kFirst; u++) step();
-                for (;;) {
-                    const bool actA = (xA & kXEnd) == 0, actB = (xB & kXEnd) == 0;
-                    if (!__any_sync(FULL, actA || actB)) break;
-                    // an escape row (a code longer than 12 bits) has hi == 0
-                    const bool escA = actA && hA == 0, escB = actB && hB == 0;
-                    if (__any_sync(FULL, escA || escB)) {
-                        if (escA) {
-                            uint32_t len;
-                            const uint32_t r = rot8(walk(aA, len));
-                            pack(oA, r & 0xFFu, 8u << 24, K_S24);
-                            xA += len;
-                            shift96_long_ones(aA, bA, cA, len);
+            if constexpr (kNB == 8) {
+                if (!safe) {
+                    // ---- single decode pass into the private slots (chains A: [gapA, 64), B: [64+gapB, 128))
+                    // exact chain ends when the next chunk's gap marks a code start (every tile but the
+                    // one holding the tensor's last code): A = [gapA, 64 + gapB), B = [64 + gapB, 128 + gapC),
+                    // enforced by one-bits after the end; otherwise [.., 64) / [.., 128) + walk back
+                    const bool exact = long_codes && hi < N;
+                    const uint32_t limA = exact ? 64u + gapB - gapA : 64u - gapA;
+                    const uint32_t limB = exact ? 64u + gapC - gapB : 64u - gapB;
+                    uint32_t aA = W0, bA = W1, cA = exact ? W2 | (0xFFFFFFFFu >> gapB) : W2;
+                    uint32_t aB = W2, bB = W3, cB = exact ? W4 | (0xFFFFFFFFu >> gapC) : W4;
+                    shift96_ones(aA, bA, cA, gapA);
+                    shift96_ones(aB, bB, cB, gapB);
+                    uint32_t xA = kXEnd - limA, xB = kXEnd - limB;   // see kXEnd
+                    Slot oA, oB;
+                    slot_init(oA, slotA);
+                    slot_init(oB, slotB);
+                    uint32_t hA = 1, hB = 1;
+                    auto step = [&]() {
+                        uint32_t lA, lB;
+                        lds64(t12_addr(aA, tab, K_ROW, K_TOP, K_ENT), lA, hA);
+                        lds64(t12_addr(aB, tab, K_ROW, K_TOP, K_ENT), lB, hB);
+                        pack(oA, lA, hA, K_S24);
+                        pack(oB, lB, hB, K_S24);
+                        xA += hA;
+                        xB += hB;
+                        shift96_ones(aA, bA, cA, hA);
+                        shift96_ones(aB, bB, cB, hB);
+                    };
+    #pragma unroll
+                    for (int u = 0; u < kFirst; u++) step();
+                    for (;;) {
+                        const bool actA = (xA & kXEnd) == 0, actB = (xB & kXEnd) == 0;
+                        if (!__any_sync(FULL, actA || actB)) break;
+                        // an escape row (a code longer than 12 bits) has hi == 0
+                        const bool escA = actA && hA == 0, escB = actB && hB == 0;
+                        if (__any_sync(FULL, escA || escB)) {
+                            if (escA) {
+                                uint32_t len;
+                                const uint32_t r = rot8(walk(aA, len));
+                                pack(oA, r & 0xFFu, 8u << 24, K_S24);
+                                xA += len;
+                                shift96_long_ones(aA, bA, cA, len);
+                            }
+                            if (escB) {
+                                uint32_t len;
+                                const uint32_t r = rot8(walk(aB, len));
+                                pack(oB, r & 0xFFu, 8u << 24, K_S24);
+                                xB += len;
+                                shift96_long_ones(aB, bB, cB, len);
+                            }
                         }
-                        if (escB) {
-                            uint32_t len;
-                            const uint32_t r = rot8(walk(aB, len));
-                            pack(oB, r & 0xFFu, 8u << 24, K_S24);
-                            xB += len;
-                            shift96_long_ones(aB, bB, cB, len);
+                        // one step; a chain past its end skips the lookup: lo = hi = 0 leave its state unchanged
+                        uint32_t lA = 0, lB = 0;
+                        hA = 0;
+                        hB = 0;
+                        lds64_if(t12_addr(aA, tab, K_ROW, K_TOP, K_ENT), lA, hA, actA);
+                        lds64_if(t12_addr(aB, tab, K_ROW, K_TOP, K_ENT), lB, hB, actB);
+                        pack(oA, lA, hA, K_S24);
+                        pack(oB, lB, hB, K_S24);
+                        xA += hA;
+                        xB += hB;
+                        shift96_ones(aA, bA, cA, hA);
+                        shift96_ones(aB, bB, cB, hB);
+                    }
+                    slot_flush(oA);                                               // the last partial word
+                    slot_flush(oB);
+                    uint32_t nA = slot_bytes(oA);
+                    uint32_t nB = slot_bytes(oB);
+                    // drop the codes decoded past each chain's end (they start at or after it)
+                    if (!exact) {
+                        uint32_t offA = xA & kXMask;   // kXEnd - limA + consumed
+                        while (nA > 0) {
+                            const uint32_t j = nA - 1;
+                            const uint32_t l = ld8(rlenb + ld8(slotA + (j >> 2) * 128u + (j & 3u)));
+                            if (offA - l < kXEnd) break;
+                            offA -= l;
+                            nA--;
+                        }
+                        uint32_t offB = xB & kXMask;
+                        while (nB > 0) {
+                            const uint32_t j = nB - 1;
+                            const uint32_t l = ld8(rlenb + ld8(slotB + (j >> 2) * 128u + (j & 3u)));
+                            if (offB - l < kXEnd) break;
+                            offB -= l;
+                            nB--;
                         }
                     }
-                    // one step; a chain past its end skips the lookup: lo = hi = 0 leave its state unchanged
-                    uint32_t lA = 0, lB = 0;
-                    hA = 0;
-                    hB = 0;
-                    lds64_if(t12_addr(aA, tab, K_ROW, K_TOP, K_ENT), lA, hA, actA);
-                    lds64_if(t12_addr(aB, tab, K_ROW, K_TOP, K_ENT), lB, hB, actB);
-                    pack(oA, lA, hA, K_S24);
-                    pack(oB, lB, hB, K_S24);
-                    xA += hA;
-                    xB += hB;
-                    shift96_ones(aA, bA, cA, hA);
-                    shift96_ones(aB, bB, cB, hB);
+                    cntA = nA;
+                    cntB = nB;
+                } else {
+                    // ---- count-only pass, one code at a time (1-bit codewords)
+                    auto count_chain = [&](uint32_t a, uint32_t bb, uint32_t c, uint32_t off, uint32_t lim) {
+                        uint32_t n = 0;
+                        while (off < lim) {
+                            uint32_t el, eh, len;
+                            lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
+                            if ((eh & 0xFFFFu) != 0) len = ld8(rlenb + (el & 0xFFu));
+                            else walk(a, len);
+                            n++;
+                            off += len;
+                            shift96_long(a, bb, c, len);
+                        }
+                        return n;
+                    };
+                    uint32_t a = W0, bb = W1, c = W2;
+                    shift96(a, bb, c, gapA);
+                    cntA = count_chain(a, bb, c, gapA, 64u);
+                    a = W2; bb = W3; c = W4;
+                    shift96(a, bb, c, gapB);
+                    cntB = count_chain(a, bb, c, 64u + gapB, 128u);
                 }
-                slot_flush(oA);                                               // the last partial word
-                slot_flush(oB);
+            } else if (!safe) {
+                // ---- one chain per lane: [gapA, 128 + gapB) exact, else [gapA, 128) + walk back
+                const bool exact = long_codes && hi < N;
+                const uint32_t limA = exact ? 128u + gapB - gapA : 128u - gapA;
+                uint32_t a = W0, b1 = W1, c = W2, d = W3, e = exact ? W4 | (0xFFFFFFFFu >> gapB) : W4;
+                shift160_ones(a, b1, c, d, e, gapA);
+                uint32_t xA = kXEnd - limA;
+                Slot oA;
+                slot_init(oA, slotA);
+                uint32_t hA = 1;
+                auto step = [&]() {
+                    uint32_t lA;
+                    lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), lA, hA);
+                    pack(oA, lA, hA, K_S24);
+                    xA += hA;
+                    shift160_ones(a, b1, c, d, e, hA);
+                };
+#pragma unroll
+                for (int u = 0; u < 2 * kFirst; u++) step();
+                for (;;) {
+                    const bool actA = (xA & kXEnd) == 0;
+                    if (!__any_sync(FULL, actA)) break;
+                    const bool escA = actA && hA == 0;           // an escape row (a code > 12 bits)
+                    if (__any_sync(FULL, escA)) {
+                        if (escA) {
+                            uint32_t len;
+                            const uint32_t r = rot8(walk(a, len));
+                            pack(oA, r & 0xFFu, 8u << 24, K_S24);
+                            xA += len;
+                            shift160_long_ones(a, b1, c, d, e, len);
+                        }
+                    }
+                    uint32_t lA = 0;
+                    hA = 0;
+                    lds64_if(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), lA, hA, actA);
+                    pack(oA, lA, hA, K_S24);
+                    xA += hA;
+                    shift160_ones(a, b1, c, d, e, hA);
+                }
+                slot_flush(oA);
                 uint32_t nA = slot_bytes(oA);
-                uint32_t nB = slot_bytes(oB);
-                // drop the codes decoded past each chain's end (they start at or after it)
                 if (!exact) {
                     uint32_t offA = xA & kXMask;   // kXEnd - limA + consumed
                     while (nA > 0) {
@@ -271,38 +372,25 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                         offA -= l;
                         nA--;
                     }
-                    uint32_t offB = xB & kXMask;
-                    while (nB > 0) {
-                        const uint32_t j = nB - 1;
-                        const uint32_t l = ld8(rlenb + ld8(slotB + (j >> 2) * 128u + (j & 3u)));
-                        if (offB - l < kXEnd) break;
-                        offB -= l;
-                        nB--;
-                    }
                 }
                 cntA = nA;
-                cntB = nB;
+                cntB = 0;
             } else {
                 // ---- count-only pass, one code at a time (1-bit codewords)
-                auto count_chain = [&](uint32_t a, uint32_t bb, uint32_t c, uint32_t off, uint32_t lim) {
-                    uint32_t n = 0;
-                    while (off < lim) {
-                        uint32_t el, eh, len;
-                        lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
-                        if ((eh & 0xFFFFu) != 0) len = ld8(rlenb + (el & 0xFFu));
-                        else walk(a, len);
-                        n++;
-                        off += len;
-                        shift96_long(a, bb, c, len);
-                    }
-                    return n;
-                };
-                uint32_t a = W0, bb = W1, c = W2;
-                shift96(a, bb, c, gapA);
-                cntA = count_chain(a, bb, c, gapA, 64u);
-                a = W2; bb = W3; c = W4;
-                shift96(a, bb, c, gapB);
-                cntB = count_chain(a, bb, c, 64u + gapB, 128u);
+                uint32_t a = W0, b1 = W1, c = W2, d = W3, e = W4, off = gapA;
+                shift160_long_ones(a, b1, c, d, e, gapA);
+                uint32_t n = 0;
+                while (off < 128u) {
+                    uint32_t el, eh, len;
+                    lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
+                    if ((eh & 0xFFFFu) != 0) len = ld8(rlenb + (el & 0xFFu));
+                    else walk(a, len);
+                    n++;
+                    off += len;
+                    shift160_long_ones(a, b1, c, d, e, len);
+                }
+                cntA = n;
+                cntB = 0;
             }
             const uint32_t cnt = cntA + cntB;
 
@@ -317,7 +405,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             if (lane == 31) sts32(ws + wig * 4, incl);
             group_bar(g);                          // also: every thread has read this tile's stage
             parity ^= 1u;
-            if (t == 0 && has_next) issue_tile(ts, b + kGroups12, stage, mbar);
+            if (t == 0 && has_next) {
+                if constexpr (kNB == 8) issue_tile(ts, b + kGroups12, stage, mbar);
+                else issue_tile16(ts, b + kGroups12, stage, mbar);
+            }
             uint32_t wpre = 0;
             {
                 uint4 v;
@@ -332,14 +423,29 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 // direct mode: compose and store to HBM per code
                 uint32_t p = wbeg + lpos;
                 const uint32_t pend = min(p + cnt, hi);
+                if constexpr (kNB == 8) {
 #pragma unroll 1
-                for (int sub = 0; sub < 2; sub++) {
-                    uint32_t a, bb, c;
-                    if (sub) { a = W2; bb = W3; c = W4; shift96(a, bb, c, gapB); }
-                    else { a = W0; bb = W1; c = W2; shift96(a, bb, c, gapA); }
-                    uint32_t off = sub ? 64u + gapB : gapA;
-                    const uint32_t lim_off = sub ? 128u : 64u;
-                    while (p < pend && off < lim_off) {
+                    for (int sub = 0; sub < 2; sub++) {
+                        uint32_t a, bb, c;
+                        if (sub) { a = W2; bb = W3; c = W4; shift96(a, bb, c, gapB); }
+                        else { a = W0; bb = W1; c = W2; shift96(a, bb, c, gapA); }
+                        uint32_t off = sub ? 64u + gapB : gapA;
+                        const uint32_t lim_off = sub ? 128u : 64u;
+                        while (p < pend && off < lim_off) {
+                            uint32_t el, eh, len, sym;
+                            lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
+                            if ((eh & 0xFFFFu) != 0) { sym = unrot8(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
+                            else sym = walk(a, len);
+                            out[p] = compose(sym, __ldg(ts.packed_sign_mantissa + p));
+                            p++;
+                            off += len;
+                            shift96_long(a, bb, c, len);
+                        }
+                    }
+                } else {
+                    uint32_t a = W0, b1 = W1, c = W2, d = W3, e = W4, off = gapA;
+                    shift160_long_ones(a, b1, c, d, e, gapA);
+                    while (p < pend && off < 128u) {
                         uint32_t el, eh, len, sym;
                         lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
                         if ((eh & 0xFFFFu) != 0) { sym = unrot8(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
@@ -347,7 +453,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                         out[p] = compose(sym, __ldg(ts.packed_sign_mantissa + p));
                         p++;
                         off += len;
-                        shift96_long(a, bb, c, len);
+                        shift160_long_ones(a, b1, c, d, e, len);
                     }
                 }
                 continue;
@@ -364,40 +470,60 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             const bool edge = vec_out && (lane < 16 ? es < ha : es < rb);
 
             // ---- compaction of the slots into [F, ...) of the warp region (in place: load all first)
-            {
-                uint32_t wa[8], wb[8];
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    wa[k] = lds32(slotA + 128u * k);
-                    wb[k] = lds32(slotB + 128u * k);
+            if constexpr (kNB == 8) {
+                {
+                    uint32_t wa[8], wb[8];
+    #pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        wa[k] = lds32(slotA + 128u * k);
+                        wb[k] = lds32(slotB + 128u * k);
+                    }
+                    __syncwarp();
+                    const uint32_t dA = wreg + (wbeg - F) + lpos, dB = dA + cntA;
+                    compact_words(dA, wa, cntA);
+                    compact_words(dB, wb, cntB);
+                    __syncwarp();
+    #ifndef SP12_BYTE_HEADS
+                    // first partial word of a chain: its low bytes already hold the previous chain's tail
+                    // (that chain's last word, written above), so one read-modify-write completes it when
+                    // every chain of the warp has >= 4 codes (then no word holds bytes of 3 chains)
+                    if (!__any_sync(FULL, cntA < 4u || cntB < 4u)) {
+                        const uint32_t rA = dA & 3u, rB = dB & 3u;
+                        if (rA) {
+                            const uint32_t o = lds32(dA - rA);
+                            sts32(dA - rA, (o & ((1u << (8 * rA)) - 1u)) | (wa[0] << (8 * rA)));
+                        }
+                        if (rB) {
+                            const uint32_t o = lds32(dB - rB);
+                            sts32(dB - rB, (o & ((1u << (8 * rB)) - 1u)) | (wb[0] << (8 * rB)));
+                        }
+                    } else
+    #endif
+                    {
+                        compact_head(dA, wa[0], cntA);
+                        compact_head(dB, wb[0], cntB);
+                    }
                 }
                 __syncwarp();
-                const uint32_t dA = wreg + (wbeg - F) + lpos, dB = dA + cntA;
-                compact_words(dA, wa, cntA);
-                compact_words(dB, wb, cntB);
+            } else {
+                uint32_t wa[16];
+#pragma unroll
+                for (int k = 0; k < 16; k++) wa[k] = lds32(slotA + 128u * k);
                 __syncwarp();
-#ifndef SP12_BYTE_HEADS
-                // first partial word of a chain: its low bytes already hold the previous chain's tail
-                // (that chain's last word, written above), so one read-modify-write completes it when
-                // every chain of the warp has >= 4 codes (then no word holds bytes of 3 chains)
-                if (!__any_sync(FULL, cntA < 4u || cntB < 4u)) {
-                    const uint32_t rA = dA & 3u, rB = dB & 3u;
+                const uint32_t dA = wreg + (wbeg - F) + lpos;
+                compact_words16(dA, wa, cntA);
+                __syncwarp();
+                if (!__any_sync(FULL, cntA < 4u)) {
+                    const uint32_t rA = dA & 3u;
                     if (rA) {
                         const uint32_t o = lds32(dA - rA);
                         sts32(dA - rA, (o & ((1u << (8 * rA)) - 1u)) | (wa[0] << (8 * rA)));
                     }
-                    if (rB) {
-                        const uint32_t o = lds32(dB - rB);
-                        sts32(dB - rB, (o & ((1u << (8 * rB)) - 1u)) | (wb[0] << (8 * rB)));
-                    }
-                } else
-#endif
-                {
+                } else {
                     compact_head(dA, wa[0], cntA);
-                    compact_head(dB, wb[0], cntB);
                 }
+                __syncwarp();
             }
-            __syncwarp();
 
             // ---- per-warp merge of [ra, rb): compose BF16 and store
             uint32_t a0, a1;
@@ -520,30 +646,35 @@ uint32_t fast_grid(uint32_t total_tiles, int num_sms) {
     return min((uint32_t)num_sms, (total_tiles + kGroups12 - 1) / kGroups12);
 }
 
-// Tensors the product kernel decodes: the paper's format parameters (T = 256, n = 8) and the
-// alignment its bulk copies need (stream, gaps and PackedSignMantissa 16-byte aligned, BF16 output
-// 2-byte aligned); df11_decompress_block_ex sends every other tensor to the Algorithm 1 kernel.
+// Tensors the product kernel decodes: the paper's format parameters (T = 256, n = 8) or
+// T = 128, n = 16 (NEXT-4), and the alignment its bulk copies need (stream, gaps and
+// PackedSignMantissa 16-byte aligned, BF16 output 2-byte aligned); df11_decompress_block_ex sends
+// every other tensor to the Algorithm 1 kernel.
 bool fast_supports(const df11_device_tensor &t) {
-    return t.T == kT && t.n == kN &&
+    return ((t.T == kT && t.n == kN) || (t.T == 128 && t.n == 16)) &&
            (reinterpret_cast<uintptr_t>(t.encoded_exponent) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.gaps) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.packed_sign_mantissa) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.out) & 1) == 0;
 }
 
+// Launch for a batch whose tensors all have n = 8 (T = 256) or all n = 16 (T = 128).
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches) {
     if (bt.total_tiles == 0) return cudaSuccess;
     int num_sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    if (device >= 0 && device < 64 && !g_sp12_attr_set[device]) {
-        e = cudaFuncSetAttribute(sp12_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem12);
+    const bool n16 = bt.t[0].n == 16;
+    if (device >= 0 && device < 64 && !(g_sp12_attr_set[device] & (n16 ? 2 : 1))) {
+        e = n16 ? cudaFuncSetAttribute(sp12_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem12)
+                : cudaFuncSetAttribute(sp12_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem12);
         if (e != cudaSuccess) return e;
-        g_sp12_attr_set[device] = 1;
+        g_sp12_attr_set[device] |= n16 ? 2 : 1;
     }
     const uint32_t grid = bt.grid ? bt.grid
                                   : min((uint32_t)num_sms, (bt.total_tiles + kGroups12 - 1) / kGroups12);
-    sp12_kernel<<<grid, kCta12, kSmem12, stream>>>(bt);
+    if (n16) sp12_kernel<16><<<grid, kCta12, kSmem12, stream>>>(bt);
+    else sp12_kernel<8><<<grid, kCta12, kSmem12, stream>>>(bt);
     if (launches) (*launches)++;
     return cudaGetLastError();
 }

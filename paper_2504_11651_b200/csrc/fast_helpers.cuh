@@ -119,6 +119,13 @@ __device__ __forceinline__ void issue_tile(const df11_device_tensor &ts, uint32_
     tma_g2s(stage, ts.encoded_exponent + (size_t)b * (kT * kN), kChunkBytes, bar);
     tma_g2s(stage + kChunkBytes, ts.gaps + (size_t)b * (kT * 5 / 8), kGapBytes, bar);
 }
+// The same for the format T = 128, n = 16 (a format block of the same 2 048 stream bytes, half the
+// gaps: 80 bytes, + 16 read past).
+__device__ __forceinline__ void issue_tile16(const df11_device_tensor &ts, uint32_t b, uint32_t stage, uint32_t bar) {
+    mbar_expect_tx(bar, kChunkBytes + 128 * 5 / 8 + 16);
+    tma_g2s(stage, ts.encoded_exponent + (size_t)b * (kT * kN), kChunkBytes, bar);
+    tma_g2s(stage + kChunkBytes, ts.gaps + (size_t)b * (128 * 5 / 8), 128 * 5 / 8 + 16, bar);
+}
 
 // Paper's hierarchical LUT walk over the format tables in global memory; returns the
 // exponent and its code length.  Bounded: <= 4 levels, child < k, zero length -> 32.

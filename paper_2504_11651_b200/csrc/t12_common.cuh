@@ -130,6 +130,35 @@ __device__ __forceinline__ void compact_words(uint32_t d, const uint32_t (&w)[8]
         sts32_if(db + 4u * k, v, (uint32_t)k < nw && (k > 0 || r == 0));
     }
 }
+// compact_words for runs of up to 64 bytes held in w[0..15] (one chain of a 16-byte chunk)
+__device__ __forceinline__ void compact_words16(uint32_t d, const uint32_t (&w)[16], uint32_t n) {
+    const uint32_t r = d & 3u, db = d - r, sh = r * 8u;
+    const uint32_t nw = (r + n + 3u) >> 2;                 // <= 17
+#pragma unroll
+    for (int k = 0; k < 17; k++) {
+        const uint32_t v = k == 0 ? w[0] : __funnelshift_l(w[k - 1], k < 16 ? w[k] : 0u, sh);
+        sts32_if(db + 4u * k, v, (uint32_t)k < nw && (k > 0 || r == 0));
+    }
+}
+// 160-bit buffer (a:b:c:d:e) shifts for one chain over a 16-byte chunk (n = 16), pulling in one-bits
+__device__ __forceinline__ void shift160_ones(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d, uint32_t &e,
+                                              uint32_t s) {
+    a = __funnelshift_l(b, a, s);
+    b = __funnelshift_l(c, b, s);
+    c = __funnelshift_l(d, c, s);
+    d = __funnelshift_l(e, d, s);
+    e = __funnelshift_l(0xFFFFFFFFu, e, s);
+}
+__device__ __forceinline__ void shift160_long_ones(uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d, uint32_t &e,
+                                                   uint32_t s) {
+    const bool w = s >= 32;
+    a = w ? b : a;
+    b = w ? c : b;
+    c = w ? d : c;
+    d = w ? e : d;
+    e = w ? 0xFFFFFFFFu : e;
+    shift160_ones(a, b, c, d, e, s);
+}
 __device__ __forceinline__ void compact_head(uint32_t d, uint32_t w0, uint32_t n) {
     const uint32_t r = d & 3u, db = d - r;
     if (r == 0) return;

@@ -25,7 +25,7 @@ def df11():
 
 
 def _fast_ok(df11, meta):
-    return meta["T"] == 256 and meta["n"] == 8
+    return (meta["T"], meta["n"]) in ((256, 8), (128, 16))
 
 
 def _gpu_decode_arrays(df11, meta, arrays, kernel, shape=None):
@@ -50,13 +50,26 @@ def _check_oracle_format(df11, oracle_mod, w, kernel, **kw):
         assert np.array_equal(got[: w.size], oracle_mod.decode_sequential(fmt))
 
 
+CASES = ["gauss_1m", "gauss_ragged", "constant_1bit", "two_symbol", "all_patterns_wide", "overflow_wide",
+         "fibonacci_32bit", "one_element", "tiny_17", "sigma_large", "random_bits", "escape_heavy", "escape_deep",
+         "uniform8_short_codes", "one_bit_with_tail", "maxlen_12", "maxlen_13", "four_symbol_2bit", "student_t5",
+         "sigma_loguniform"]
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("case", ["gauss_1m", "gauss_ragged", "constant_1bit", "two_symbol", "all_patterns_wide",
-                                  "overflow_wide", "fibonacci_32bit", "one_element", "tiny_17", "sigma_large",
-                                  "random_bits", "escape_heavy", "escape_deep", "uniform8_short_codes",
-                                  "one_bit_with_tail", "maxlen_12", "maxlen_13", "four_symbol_2bit",
-                                  "student_t5", "sigma_loguniform"])
+@pytest.mark.parametrize("case", CASES)
 def test_parity_cases(df11, oracle_mod, kernel, case):
+    _check_oracle_format(df11, oracle_mod, _case_weights(case), kernel)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_parity_cases_n16_fast(df11, oracle_mod, case):
+    """NEXT-4: the product kernel on the format T = 128, n = 16 (half the gap bits), every
+    parity case, oracle-encoded arrays: GPU == original == oracle D1."""
+    _check_oracle_format(df11, oracle_mod, _case_weights(case), "fast", T=128, n=16)
+
+
+def _case_weights(case):
     if case == "gauss_1m":
         w = workloads.gaussian_bf16((1 << 20,), seed=1)
     elif case == "gauss_ragged":
@@ -128,7 +141,7 @@ def test_parity_cases(df11, oracle_mod, kernel, case):
         w = workloads.from_exponent_histogram(counts, seed=8)
     else:
         w = np.random.default_rng(5).integers(0, 1 << 16, size=400001, dtype=np.uint32).astype(np.uint16)
-    _check_oracle_format(df11, oracle_mod, w, kernel)
+    return w
 
 
 @pytest.mark.parametrize("T,n", [(32, 4), (64, 8), (128, 16), (256, 8), (512, 8), (1024, 8), (96, 5), (1024, 32)])
@@ -276,7 +289,7 @@ def test_auto_splits_a_mixed_batch(df11):
     the block to ONE product-kernel launch; the Alg. 1 kernel takes one launch per distinct T (3
     launches in all here); every output is the original."""
     ws = [workloads.gaussian_bf16((n,), seed=30 + i) for i, n in enumerate((300001, 65536, 123457))]
-    hs = [df11.encode(ws[0]), df11.encode(ws[1], T=128, n=16), df11.encode(ws[2])]
+    hs = [df11.encode(ws[0]), df11.encode(ws[1], T=64, n=8), df11.encode(ws[2])]
     dts = [df11.to_device(h) for h in hs]
     psm = dts[2].packed_sign_mantissa
     big = torch.zeros(psm.numel() + 16, dtype=torch.uint8, device=psm.device)
@@ -291,3 +304,30 @@ def test_auto_splits_a_mixed_batch(df11):
         assert np.array_equal(o.view(torch.int16).cpu().numpy().view(np.uint16), w)
     df11.decompress_block([dts[0]])
     assert df11.last_kernels() == {"fast"}
+
+
+def test_full_size_llama8b_block_n16(df11, oracle_mod):
+    """NEXT-4: the Llama-3.1-8B block encoded with T = 128, n = 16 decodes in ONE product-kernel
+    launch, every element bit-exact, oracle D2 on sampled blocks; a mixed n = 8 / n = 16 batch takes
+    one launch per chunk size."""
+    ts = workloads.config_tensors("llama8b_block")
+    hs = [df11.encode(w, T=128, n=16) for _, w in ts]
+    dts = [df11.to_device(h) for h in hs]
+    before = df11.launch_count()
+    outs = df11.decompress_block(dts)
+    assert df11.launch_count() - before == 1 and df11.last_kernels() == {"fast"}
+    torch.cuda.synchronize()
+    for (name, w), o, h in zip(ts, outs, hs):
+        got = o.view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(got, w), name
+        fmt_like = dict(h.arrays(), num_elements=h.num_elements, T=h.T, n=h.n, B=h.B, k=h.k,
+                        lut_entry_bytes=h.lut_entry_bytes)
+        for b, (lo, vals) in oracle_mod.decode_alg1_blocks(fmt_like, [0, 1, h.B // 2, h.B - 1]).items():
+            assert np.array_equal(got.reshape(-1)[lo:lo + vals.size], vals), (name, b)
+    mixed = [df11.to_device(df11.encode(ts[1][1])), dts[2]]
+    before = df11.launch_count()
+    outs = df11.decompress_block(mixed)
+    assert df11.launch_count() - before == 2
+    torch.cuda.synchronize()
+    for (name, w), o in zip([ts[1], ts[2]], outs):
+        assert np.array_equal(o.view(torch.int16).cpu().numpy().view(np.uint16), w), name
