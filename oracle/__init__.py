@@ -10,7 +10,8 @@ Pins: every function here is checked by tests/test_oracle_*.py against the paper
 (tests/golden/), brute force on tiny inputs, closed forms and invariants.  Parity status per function
 is listed in DESIGN.md §4.
 """
-from .oracle import (FormatError, build_oracle, compose, compressed_bytes, decode_alg1,  # noqa: F401
-                     decode_alg1_blocks, decode_alg1_range, decode_sequential, encode, entropy_bits,
-                     histogram, split)
+from .oracle import (FormatError, VALUE_FORMATS, WORD_DTYPE, build_oracle, compose,  # noqa: F401
+                     compose_v, compressed_bytes, decode_alg1, decode_alg1_blocks, decode_alg1_range,
+                     decode_sequential, encode, entropy_bits, histogram, residual_array_bytes, residual_bits,
+                     split, split_v, vf_code)
 from . import huffman  # noqa: F401

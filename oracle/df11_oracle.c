@@ -6,7 +6,7 @@
  * does, and this file shares no code, header, table or constant generator with it.
  *
  * Citations: "P:n" = PAPER.md line n (section / algorithm in brackets).  Readings where the paper is
- * silent are numbered R1..R24 and listed in DESIGN.md §3 ("Readings").
+ * silent are numbered R1..R28 and listed in DESIGN.md §3 ("Readings").
  *
  * Contents (bulk loops only; the small per-codebook steps E3-E5 are pure Python in huffman.py):
  *   E1 split                 P:50-52 [§2.1, Eq. 1]; inverse of Alg. 1 compose P:429-434
@@ -19,6 +19,9 @@
  *   D1 sequential decoder    P:108 [§2.3] / P:533-546 [App. I.1]: canonical bit-by-bit decode that uses
  *                            only CodeLengths, the stream and PackedSignMantissa
  *   D2 Alg. 1 emulator       P:376-446 [App. Alg. 1 DF11ToBF16], block by block, thread by thread
+ *   format variants (NEXT-4) value formats FP16 / FP8 beside BF16 (P:609 names them as the limitation;
+ *                            readings R25-R27) and b-bit LUTs (App. I.2, generic b; b = L is
+ *                            the monolithic table of App. I.1; R28)
  *
  * Every function is single-threaded scalar C with no blocking, fusion or reordering beyond the
  * definition it follows.
@@ -52,6 +55,61 @@ uint16_t df11o_compose(uint8_t exponent, uint8_t packed_sign_mantissa)
     return (uint16_t)((sign << 8) | ((uint16_t)exponent << 7) | mant);
 }
 
+/* ---------------------------------------------------------------- value formats (NEXT-4, R25-R27)
+ * A value of format vf is split exactly like BF16: its exponent field becomes the Huffman symbol and
+ * the remaining bits (sign, then mantissa) are kept raw.
+ *   vf 0 BF16        16 bits: sign 15, exponent 14..7  (8 bits), mantissa 6..0 (7 bits)
+ *   vf 1 FP16 (IEEE binary16)  16 bits: sign 15, exponent 14..10 (5 bits), mantissa 9..0 (10 bits)
+ *   vf 2 FP8 E4M3              8 bits:  sign 7,  exponent 6..3   (4 bits), mantissa 2..0 (3 bits)
+ *   vf 3 FP8 E5M2              8 bits:  sign 7,  exponent 6..2   (5 bits), mantissa 1..0 (2 bits)
+ * Residual of element i: r = sign << M | mantissa (R = 1 + M bits), stored MSB-first at bits
+ * [R*i, R*i + R) of PackedSignMantissa (R25).  For BF16, R = 8 and byte i is sign << 7 | mantissa:
+ * the paper's layout. */
+static const int VF_WORD_BITS[4] = {16, 16, 8, 8};
+static const int VF_EXP_BITS[4] = {8, 5, 4, 5};
+static const int VF_MAN_BITS[4] = {7, 10, 3, 2};
+
+int df11o_vf_residual_bits(int vf) { return 1 + VF_MAN_BITS[vf]; }
+
+static uint32_t word_at(const void *w, int vf, uint64_t i)
+{
+    if (VF_WORD_BITS[vf] == 16) return ((const uint16_t *)w)[i];
+    return ((const uint8_t *)w)[i];
+}
+
+/* residual stream (MSB-first, R1 order) */
+static void put_bits(uint8_t *buf, uint64_t bit, uint32_t v, int nbits);
+static uint32_t get_bits(const uint8_t *buf, uint64_t nbytes, uint64_t bit, int nbits);
+
+/* `residual` must be zeroed and hold ceil(R*n/8) bytes. */
+void df11o_split_v(const void *w, uint64_t n, int vf, uint8_t *exponent, uint8_t *residual)
+{
+    int M = VF_MAN_BITS[vf], E = VF_EXP_BITS[vf], R = 1 + M;
+    for (uint64_t i = 0; i < n; i++) {
+        uint32_t word = word_at(w, vf, i);
+        uint32_t sign = (word >> (E + M)) & 1u;
+        uint32_t expo = (word >> M) & ((1u << E) - 1u);
+        uint32_t mant = word & ((1u << M) - 1u);
+        exponent[i] = (uint8_t)expo;
+        put_bits(residual, (uint64_t)R * i, (sign << M) | mant, R);
+    }
+}
+
+/* Inverse: sign << (E + M) | exponent << M | mantissa (for BF16 this is Alg. 1's compose). */
+uint32_t df11o_compose_v(int vf, uint32_t exponent, uint32_t residual)
+{
+    int M = VF_MAN_BITS[vf], E = VF_EXP_BITS[vf];
+    uint32_t sign = (residual >> M) & 1u;
+    uint32_t mant = residual & ((1u << M) - 1u);
+    return (sign << (E + M)) | (exponent << M) | mant;
+}
+
+static void store_word(void *out, int vf, uint64_t i, uint32_t v)
+{
+    if (VF_WORD_BITS[vf] == 16) ((uint16_t *)out)[i] = (uint16_t)v;
+    else ((uint8_t *)out)[i] = (uint8_t)v;
+}
+
 /* ---------------------------------------------------------------- E2: histogram */
 void df11o_histogram(const uint8_t *exponent, uint64_t n, uint64_t *hist /*256*/)
 {
@@ -71,6 +129,22 @@ static int get_bit(const uint8_t *buf, uint64_t nbytes, uint64_t bit)
 static void set_bit(uint8_t *buf, uint64_t bit)
 {
     buf[bit >> 3] |= (uint8_t)(1u << (7 - (bit & 7)));
+}
+
+/* nbits of v, most significant first, at stream bits [bit, bit + nbits) (buffer zeroed) */
+static void put_bits(uint8_t *buf, uint64_t bit, uint32_t v, int nbits)
+{
+    for (int j = nbits - 1; j >= 0; j--) {
+        if ((v >> j) & 1u) set_bit(buf, bit);
+        bit++;
+    }
+}
+
+static uint32_t get_bits(const uint8_t *buf, uint64_t nbytes, uint64_t bit, int nbits)
+{
+    uint32_t v = 0;
+    for (int j = 0; j < nbits; j++) v = (v << 1) | (uint32_t)get_bit(buf, nbytes, bit + (uint64_t)j);
+    return v;
 }
 
 /* ---------------------------------------------------------------- E6: bit packing
@@ -152,14 +226,18 @@ static uint32_t read_gap(const uint8_t *gaps, uint64_t gaps_bytes, uint64_t g)
 }
 
 /* ---------------------------------------------------------------- D1: sequential canonical decoder
- * Uses only CodeLengths (canonical reconstruction, R3/E4), the stream, PackedSignMantissa and N.
+ * Uses only CodeLengths (canonical reconstruction, R3/E4), the stream, PackedSignMantissa and N;
+ * value format vf (R25): element i = compose_v(symbol, residual bits [R*i, R*i + R)), written as a
+ * 16-bit (BF16, FP16) or 8-bit (FP8) word.
  * Canonical codes: symbols sorted by (length, symbol); code_0 = 0, code_i = (code_{i-1}+1) << (l_i - l_{i-1}).
  * Bit by bit: append the next stream bit to `code`; after l bits, if code - first_code[l] < count[l]
  * the codeword is complete and names symbol sorted[offset[l] + code - first_code[l]].
  * Returns 0 on success, -1 if the stream runs out (corrupt), -2 on a malformed codebook. */
 int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const uint8_t *code_len /*256*/,
-                            const uint8_t *packed_sign_mantissa, uint64_t n, uint16_t *out)
+                            const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t n, int vf,
+                            void *out)
 {
+    const int R = 1 + VF_MAN_BITS[vf];
     uint32_t count[33] = {0};
     uint32_t first_code[33] = {0};
     uint32_t offset[33] = {0};
@@ -171,6 +249,7 @@ int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const 
             if (code_len[s] == l) { sorted[nsym++] = (uint8_t)s; count[l]++; }
     }
     for (int s = 0; s < 256; s++) if (code_len[s] > 32) return -2;
+    for (int s = 1 << VF_EXP_BITS[vf]; s < 256; s++) if (code_len[s]) return -2;   /* not an exponent */
     if (n > 0 && nsym == 0) return -2;
     /* first canonical code of each length */
     uint64_t code = 0;
@@ -202,7 +281,8 @@ int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const 
             if (count[l] && c >= first_code[l] && c - first_code[l] < count[l])
                 found = sorted[offset[l] + (uint32_t)(c - first_code[l])];
         }
-        out[i] = df11o_compose((uint8_t)found, packed_sign_mantissa[i]);
+        store_word(out, vf, i, df11o_compose_v(vf, (uint32_t)found,
+                                               get_bits(packed_sign_mantissa, psm_bytes, (uint64_t)R * i, R)));
     }
     return 0;
 }
@@ -212,7 +292,9 @@ int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const 
  * a big-endian 32-bit window at the absolute stream bit chunk_start + BitOffset (R2), zero-extended
  * past the buffer end (R16).  Exponent >= 240 is a pointer to LUT_{257-Exponent} (1-based), i.e. the
  * 0-based table 256-Exponent (narrow, entry_bytes = 1); wide tables (entry_bytes = 2, R8) use
- * entries >= 256 as pointers to table (entry-256).  Outputs are clipped to [BOP[b], BOP[b+1]) (R15).
+ * entries >= 256 as pointers to table (entry-256).  Tables have 2^b entries (App. I.2, generic b; the
+ * paper's b = 8 reads Byte_1..Byte_4): level i (1-based) is indexed by window bits [b(i-1), bi),
+ * zero-extended past bit 32 (R28).  Outputs are clipped to [BOP[b], BOP[b+1]) (R15).
  * check_counts = 1 additionally asserts that every non-final block decodes exactly
  * BOP[b+1]-BOP[b] elements (returns -3 if not).  Returns 0 on success, -4 on a malformed LUT walk. */
 static uint32_t window32(const uint8_t *stream, uint64_t stream_bytes, uint64_t bit)
@@ -222,10 +304,11 @@ static uint32_t window32(const uint8_t *stream, uint64_t stream_bytes, uint64_t 
     return w;
 }
 
-static int lut_entry(const uint8_t *luts, uint32_t entry_bytes, uint32_t table, uint32_t idx)
+static int lut_entry(const uint8_t *luts, uint32_t entry_bytes, uint32_t b, uint32_t table, uint32_t idx)
 {
-    if (entry_bytes == 1) return luts[(uint64_t)table * 256 + idx];
-    const uint8_t *p = luts + ((uint64_t)table * 256 + idx) * 2;
+    uint64_t off = ((uint64_t)table << b) + idx;
+    if (entry_bytes == 1) return luts[off];
+    const uint8_t *p = luts + off * 2;
     return (int)p[0] | ((int)p[1] << 8);           /* little-endian uint16 entries */
 }
 
@@ -235,29 +318,41 @@ static uint32_t pointer_target(int e, uint32_t entry_bytes)
     return entry_bytes == 1 ? (uint32_t)(256 - e) : (uint32_t)(e - 256);
 }
 
+/* Window bits [b(i-1), bi) as an index (bits past 32 read as zero). */
+static uint32_t level_index(uint32_t window, uint32_t b, int i)
+{
+    uint32_t idx = 0;
+    for (uint32_t j = 0; j < b; j++) {
+        uint32_t bit = b * (uint32_t)(i - 1) + j;
+        idx = (idx << 1) | (bit < 32 ? (window >> (31 - bit)) & 1u : 0u);
+    }
+    return idx;
+}
+
 /* One LUT walk: returns the decoded exponent or -1 on a malformed walk. */
-static int alg1_decode_one(uint32_t window, const uint8_t *luts, uint32_t entry_bytes, uint32_t k)
+static int alg1_decode_one(uint32_t window, const uint8_t *luts, uint32_t entry_bytes, uint32_t k, uint32_t b)
 {
     int i = 1;
-    uint32_t byte_i = (window >> 24) & 0xFFu;
-    int e = lut_entry(luts, entry_bytes, 0, byte_i);        /* LUT_1 = root */
+    const int levels = (int)((32 + b - 1) / b);              /* a code of <= 32 bits */
+    int e = lut_entry(luts, entry_bytes, b, 0, level_index(window, b, 1));   /* LUT_1 = root */
     while (is_pointer(e, entry_bytes)) {
         i = i + 1;
-        if (i > 4) return -1;
+        if (i > levels) return -1;
         uint32_t table = pointer_target(e, entry_bytes);
         if (table >= k) return -1;
-        byte_i = (window >> (8 * (4 - i))) & 0xFFu;
-        e = lut_entry(luts, entry_bytes, table, byte_i);
+        e = lut_entry(luts, entry_bytes, b, table, level_index(window, b, i));
     }
     return e;
 }
 
-int df11o_decode_alg1(const uint8_t *luts, uint32_t entry_bytes, uint32_t k, const uint8_t *code_len,
-                      const uint8_t *stream, uint64_t stream_bytes,
+int df11o_decode_alg1(const uint8_t *luts, uint32_t entry_bytes, uint32_t k, uint32_t lut_bits,
+                      const uint8_t *code_len, const uint8_t *stream, uint64_t stream_bytes,
                       const uint8_t *gaps, uint64_t gaps_bytes, const uint32_t *bop,
-                      const uint8_t *packed_sign_mantissa, uint32_t B, uint32_t T, uint32_t n_bytes,
-                      uint64_t N, int check_counts, uint16_t *out)
+                      const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint32_t B, uint32_t T,
+                      uint32_t n_bytes, uint64_t N, int vf, int check_counts, void *out)
 {
+    const int R = 1 + VF_MAN_BITS[vf];
+    if (lut_bits < 1 || lut_bits > 16) return -4;
     uint64_t chunk_bits = 8ull * n_bytes;
     uint32_t *num_elements = (uint32_t *)calloc(T ? T : 1, sizeof(uint32_t));
     uint64_t *thread_output_pos = (uint64_t *)calloc(T ? T : 1, sizeof(uint64_t));
@@ -272,7 +367,7 @@ int df11o_decode_alg1(const uint8_t *luts, uint32_t entry_bytes, uint32_t k, con
             num_elements[t] = 0;
             while (bit_offset < chunk_bits) {
                 uint32_t w = window32(stream, stream_bytes, chunk_start + bit_offset);
-                int e = alg1_decode_one(w, luts, entry_bytes, k);
+                int e = alg1_decode_one(w, luts, entry_bytes, k, lut_bits);
                 if (e < 0 || code_len[e] == 0) { rc = -4; break; }
                 bit_offset += code_len[e];
                 num_elements[t]++;
@@ -292,10 +387,12 @@ int df11o_decode_alg1(const uint8_t *luts, uint32_t entry_bytes, uint32_t k, con
             uint64_t pos = thread_output_pos[t];
             while (bit_offset < chunk_bits) {
                 uint32_t w = window32(stream, stream_bytes, chunk_start + bit_offset);
-                int e = alg1_decode_one(w, luts, entry_bytes, k);
-                if (e < 0 || code_len[e] == 0) { rc = -4; break; }
+                int e = alg1_decode_one(w, luts, entry_bytes, k, lut_bits);
+                if (e < 0 || code_len[e] == 0 || e >= (1 << VF_EXP_BITS[vf])) { rc = -4; break; }
                 if (pos < bop[b + 1] && pos < N)
-                    out[pos] = df11o_compose((uint8_t)e, packed_sign_mantissa[pos]);
+                    store_word(out, vf, pos, df11o_compose_v(vf, (uint32_t)e,
+                                                             get_bits(packed_sign_mantissa, psm_bytes,
+                                                                      (uint64_t)R * pos, R)));
                 bit_offset += code_len[e];
                 pos++;
             }

@@ -8,11 +8,13 @@ The bulk loops live in plain C (df11_oracle.c, compiled to liboracle.so by build
 per-codebook steps live in huffman.py.  Citations "P:n" = PAPER.md line n; R-numbers = DESIGN.md §3.
 
 Format produced ("DF11 format"):
-    num_elements N, encoded_bits, T, n, B, k, lut_entry_bytes (1 narrow | 2 wide), max_code_len
+    num_elements N, encoded_bits, T, n, B, k, lut_entry_bytes (1 narrow | 2 wide), max_code_len,
+    value_format (bf16 | fp16 | fp8_e4m3 | fp8_e5m2, R25), lut_bits b (8 = the paper; R28)
     code_lengths          uint8[256]
-    luts                  uint8[k*256*lut_entry_bytes]
+    luts                  uint8[k*2^b*lut_entry_bytes]          (App. I.2)
     encoded_exponent      uint8[B*T*n + 16], MSB-first stream
-    packed_sign_mantissa  uint8[roundup(N,16) + 16]
+    packed_sign_mantissa  uint8[roundup(R*roundup(N,16)/8,16) + 16], R-bit residuals MSB-first
+                          (R = 8 for BF16: one byte per element)
     gaps                  uint8[roundup(ceil(5BT/8),16) + 16]
     block_output_pos      uint32[B+1]
 """
@@ -50,15 +52,21 @@ def _load():
         lib.df11o_split.argtypes = [P, U64, P, P]
         lib.df11o_compose.argtypes = [ctypes.c_uint8, ctypes.c_uint8]
         lib.df11o_compose.restype = ctypes.c_uint16
+        lib.df11o_split_v.argtypes = [P, U64, I, P, P]
+        lib.df11o_compose_v.argtypes = [I, U32, U32]
+        lib.df11o_compose_v.restype = U32
+        lib.df11o_vf_residual_bits.argtypes = [I]
+        lib.df11o_vf_residual_bits.restype = I
         lib.df11o_histogram.argtypes = [P, U64, P]
         lib.df11o_pack_bits.argtypes = [P, U64, P, P, P]
         lib.df11o_pack_bits.restype = U64
         lib.df11o_gaps_bop.argtypes = [P, U64, P, U32, U32, U32, P, P]
         lib.df11o_gaps_bop.restype = I
         lib.df11o_pack_gaps.argtypes = [P, U64, P]
-        lib.df11o_decode_sequential.argtypes = [P, U64, P, P, U64, P]
+        lib.df11o_decode_sequential.argtypes = [P, U64, P, P, U64, U64, I, P]
         lib.df11o_decode_sequential.restype = I
-        lib.df11o_decode_alg1.argtypes = [P, U32, U32, P, P, U64, P, U64, P, P, U32, U32, U32, U64, I, P]
+        lib.df11o_decode_alg1.argtypes = [P, U32, U32, U32, P, P, U64, P, U64, P, P, U64, U32, U32, U32, U64, I, I,
+                                          P]
         lib.df11o_decode_alg1.restype = I
         _lib = lib
     return _lib
@@ -70,6 +78,40 @@ def _ptr(a: np.ndarray):
 
 def _roundup(x: int, m: int) -> int:
     return (x + m - 1) // m * m
+
+
+# --------------------------------------------------------------------------- value formats (R25)
+VALUE_FORMATS = {"bf16": 0, "fp16": 1, "fp8_e4m3": 2, "fp8_e5m2": 3}
+WORD_DTYPE = {0: np.uint16, 1: np.uint16, 2: np.uint8, 3: np.uint8}
+
+
+def vf_code(vf) -> int:
+    return VALUE_FORMATS[vf] if isinstance(vf, str) else int(vf)
+
+
+def residual_bits(vf) -> int:
+    """R = 1 + mantissa bits: BF16 8, FP16 11, FP8 E4M3 4, FP8 E5M2 3."""
+    return int(_load().df11o_vf_residual_bits(vf_code(vf)))
+
+
+def residual_array_bytes(N: int, vf) -> int:
+    R = residual_bits(vf)
+    return _roundup(R * _roundup(N, 16) // 8, 16) + 16
+
+
+def split_v(w: np.ndarray, vf):
+    """E1 for value format vf (R25): words -> (exponent symbols, R-bit residuals packed MSB-first)."""
+    v = vf_code(vf)
+    w = np.ascontiguousarray(w, dtype=WORD_DTYPE[v]).reshape(-1)
+    exp = np.empty(w.size, np.uint8)
+    res = np.zeros(residual_array_bytes(w.size, v), np.uint8)
+    if w.size:
+        _load().df11o_split_v(_ptr(w), w.size, v, _ptr(exp), _ptr(res))
+    return exp, res
+
+
+def compose_v(vf, exponent: int, residual: int) -> int:
+    return int(_load().df11o_compose_v(vf_code(vf), exponent, residual))
 
 
 # --------------------------------------------------------------------------- E1, E2
@@ -114,16 +156,21 @@ class FormatError(ValueError):
         self.kind = kind
 
 
-def encode(w: np.ndarray, T: int = 256, n: int = 8, lut_mode: str = "auto", codebook_hist=None) -> dict:
+def encode(w: np.ndarray, T: int = 256, n: int = 8, lut_mode: str = "auto", codebook_hist=None,
+           vf="bf16", lut_bits=8) -> dict:
     """E1..E8 for one tensor.  Codebook scope (R5): the tensor's own histogram, or `codebook_hist`
     (e.g. the summed histogram of a group sharing "a Huffman tree based on the distribution of
-    exponents in model weights"); it must give every exponent of `w` a code."""
-    w = np.ascontiguousarray(w, dtype=np.uint16).reshape(-1)
+    exponents in model weights"); it must give every exponent of `w` a code.
+    vf: value format (R25; words are uint16 for bf16/fp16, uint8 for the fp8 formats).  lut_bits: b of
+    the b-bit hierarchical tables (App. I.2; 8 = the paper), or "mono" for the monolithic table of
+    App. I.1 (b = L, L <= 16; R28)."""
+    v = vf_code(vf)
+    w = np.ascontiguousarray(w, dtype=WORD_DTYPE[v]).reshape(-1)
     N = int(w.size)
     if N >= 1 << 32:
         raise FormatError("too_large", "N >= 2^32 (BlockOutputPos is uint32, P:387)")
     lib = _load()
-    exp, psm = split(w)
+    exp, psm = split_v(w, v)
     hist = histogram(exp)
     cb_hist = hist if codebook_hist is None else np.asarray(codebook_hist)
     lengths = huffman.code_lengths([int(h) for h in cb_hist])
@@ -133,7 +180,15 @@ def encode(w: np.ndarray, T: int = 256, n: int = 8, lut_mode: str = "auto", code
     L = max(lengths)
     if L > 8 * n:
         raise FormatError("invalid_argument", "max code length exceeds the 8n-bit chunk")
-    tables, _depth = huffman.hierarchical_luts(lengths, codes, b=8)
+    if lut_bits == "mono":
+        if L > 16:
+            raise FormatError("invalid_argument", "monolithic LUT needs L <= 16")
+        b = max(L, 1)
+    else:
+        b = int(lut_bits)
+        if not 1 <= b <= 16:
+            raise FormatError("invalid_argument", "lut_bits must be in [1, 16]")
+    tables, _depth = huffman.hierarchical_luts(lengths, codes, b=b)
     narrow_ok = huffman.narrow_is_legal(lengths, tables)
     if lut_mode == "narrow":
         if any(lengths[s] for s in range(240, 256)):
@@ -167,13 +222,11 @@ def encode(w: np.ndarray, T: int = 256, n: int = 8, lut_mode: str = "auto", code
     gaps = np.zeros(_roundup((5 * B * T + 7) // 8, 16) + 16, np.uint8)
     if B:
         lib.df11o_pack_gaps(_ptr(gap_values), B * T, _ptr(gaps))
-    psm_padded = np.zeros(_roundup(N, 16) + 16, np.uint8)
-    psm_padded[:N] = psm
     return dict(
         num_elements=N, encoded_bits=encoded_bits, T=T, n=n, B=B, k=len(tables),
-        lut_entry_bytes=2 if wide else 1, max_code_len=L,
+        lut_entry_bytes=2 if wide else 1, max_code_len=L, value_format=v, lut_bits=b,
         code_lengths=code_len, luts=luts, encoded_exponent=stream,
-        packed_sign_mantissa=psm_padded, gaps=gaps, block_output_pos=bop,
+        packed_sign_mantissa=psm, gaps=gaps, block_output_pos=bop,
         # oracle-side extras for tests
         histogram=hist, codes=code_arr, gap_values=gap_values[: B * T],
     )
@@ -181,22 +234,30 @@ def encode(w: np.ndarray, T: int = 256, n: int = 8, lut_mode: str = "auto", code
 
 def compressed_bytes(fmt: dict) -> int:
     """Bytes of the DF11 representation that the method must store/read (excluding alignment pad):
-    encoded stream + sign/mantissa + 5-bit gaps + 32-bit BlockOutputPos + LUTs + CodeLengths."""
+    encoded stream + sign/mantissa (R bits per element) + 5-bit gaps + 32-bit BlockOutputPos + LUTs +
+    CodeLengths."""
     B, T = fmt["B"], fmt["T"]
-    return ((fmt["encoded_bits"] + 7) // 8 + fmt["num_elements"] + (5 * B * T + 7) // 8
+    R = residual_bits(fmt.get("value_format", 0))
+    return ((fmt["encoded_bits"] + 7) // 8 + (R * fmt["num_elements"] + 7) // 8 + (5 * B * T + 7) // 8
             + 4 * (B + 1) + len(fmt["luts"]) + 256)
 
 
 # --------------------------------------------------------------------------- decoders
+def _vf(fmt) -> int:
+    return int(fmt.get("value_format", 0))
+
+
 def decode_sequential(fmt: dict) -> np.ndarray:
     """D1: canonical bit-by-bit decode (CodeLengths + stream + PackedSignMantissa only)."""
     N = fmt["num_elements"]
-    out = np.zeros(N, np.uint16)
+    v = _vf(fmt)
+    out = np.zeros(N, WORD_DTYPE[v])
     if N == 0:
         return out
     s = fmt["encoded_exponent"]
-    rc = _load().df11o_decode_sequential(_ptr(s), s.size, _ptr(fmt["code_lengths"]),
-                                         _ptr(fmt["packed_sign_mantissa"]), N, _ptr(out))
+    psm = fmt["packed_sign_mantissa"]
+    rc = _load().df11o_decode_sequential(_ptr(s), s.size, _ptr(fmt["code_lengths"]), _ptr(psm), psm.size, N, v,
+                                         _ptr(out))
     if rc != 0:
         raise FormatError("corrupt", f"sequential decode failed ({rc})")
     return out
@@ -205,14 +266,15 @@ def decode_sequential(fmt: dict) -> np.ndarray:
 def decode_alg1(fmt: dict, check_counts: bool = True) -> np.ndarray:
     """D2: Algorithm 1 emulated block by block, thread by thread."""
     N = fmt["num_elements"]
-    out = np.zeros(N, np.uint16)
+    v = _vf(fmt)
+    out = np.zeros(N, WORD_DTYPE[v])
     if N == 0:
         return out
-    s, g = fmt["encoded_exponent"], fmt["gaps"]
+    s, g, psm = fmt["encoded_exponent"], fmt["gaps"], fmt["packed_sign_mantissa"]
     rc = _load().df11o_decode_alg1(
-        _ptr(fmt["luts"]), fmt["lut_entry_bytes"], fmt["k"], _ptr(fmt["code_lengths"]),
+        _ptr(fmt["luts"]), fmt["lut_entry_bytes"], fmt["k"], int(fmt.get("lut_bits", 8)), _ptr(fmt["code_lengths"]),
         _ptr(s), s.size, _ptr(g), g.size, _ptr(fmt["block_output_pos"]),
-        _ptr(fmt["packed_sign_mantissa"]), fmt["B"], fmt["T"], fmt["n"], N,
+        _ptr(psm), psm.size, fmt["B"], fmt["T"], fmt["n"], N, v,
         1 if check_counts else 0, _ptr(out))
     if rc != 0:
         raise FormatError("corrupt", f"Alg. 1 emulation failed ({rc})")
@@ -233,16 +295,17 @@ def decode_alg1_range(fmt: dict, b0: int, b1: int, out: np.ndarray) -> None:
     s = fmt["encoded_exponent"][b0 * T * n:]
     g = fmt["gaps"][(5 * T * b0) // 8:]
     bop = np.ascontiguousarray(fmt["block_output_pos"][b0:b1 + 1])
+    psm = fmt["packed_sign_mantissa"]
     rc = _load().df11o_decode_alg1(
-        _ptr(fmt["luts"]), fmt["lut_entry_bytes"], fmt["k"], _ptr(fmt["code_lengths"]),
+        _ptr(fmt["luts"]), fmt["lut_entry_bytes"], fmt["k"], int(fmt.get("lut_bits", 8)), _ptr(fmt["code_lengths"]),
         _ptr(s), s.size, _ptr(g), g.size, _ptr(bop),
-        _ptr(fmt["packed_sign_mantissa"]), b1 - b0, T, n, fmt["num_elements"], 1, _ptr(out))
+        _ptr(psm), psm.size, b1 - b0, T, n, fmt["num_elements"], _vf(fmt), 1, _ptr(out))
     if rc != 0:
         raise FormatError("corrupt", f"Alg. 1 emulation failed ({rc})")
 
 
 def decode_alg1_blocks(fmt: dict, blocks) -> dict:
-    """D2 restricted to the given format blocks: returns {block b: (start, uint16 values)} for
+    """D2 restricted to the given format blocks: returns {block b: (start, decoded words)} for
     sampled parity checks at full size.  Runs Alg. 1 on a view containing only those blocks."""
     res = {}
     for b in blocks:
@@ -258,8 +321,14 @@ def decode_alg1_blocks(fmt: dict, blocks) -> dict:
         gv = np.array(gap_vals, np.uint8)
         _load().df11o_pack_gaps(_ptr(gv), T, _ptr(gaps))
         bop = np.array([0, hi - lo], np.uint32)
-        psm = np.zeros(_roundup(hi - lo, 16) + 16, np.uint8)
-        psm[: hi - lo] = fmt["packed_sign_mantissa"][lo:hi]
+        R = residual_bits(_vf(fmt))
+        psm = np.zeros(residual_array_bytes(hi - lo, _vf(fmt)), np.uint8)
+        if R == 8:
+            psm[: hi - lo] = fmt["packed_sign_mantissa"][lo:hi]
+        else:                     # the block's residual bits [R lo, R hi), re-aligned to bit 0
+            bits = np.unpackbits(fmt["packed_sign_mantissa"])[R * lo: R * hi]
+            packed = np.packbits(bits)
+            psm[: packed.size] = packed
         sub = dict(fmt, num_elements=hi - lo, B=1, encoded_exponent=stream, gaps=gaps,
                    block_output_pos=bop, packed_sign_mantissa=psm)
         res[b] = (lo, decode_alg1(sub, check_counts=False))

@@ -100,6 +100,39 @@ def gaussian_bf16_torch(shape, seed: int, device, sigma: float = SIGMA):
     return w.view(torch.int16).cpu().numpy().view(np.uint16)
 
 
+# --------------------------------------------------------------------------- other value formats
+# (NEXT-4, R25-R27): the same N(0, sigma^2) weights stored as FP16, or as FP8 with one
+# per-tensor scale that maps the tensor's absolute maximum to the format's largest finite value (the
+# usual FP8 weight recipe).  Inputs only: conversions are numpy's / torch's round-to-nearest-even.
+VALUE_FORMATS = ("bf16", "fp16", "fp8_e4m3", "fp8_e5m2")
+FP8_MAX = {"fp8_e4m3": 448.0, "fp8_e5m2": 57344.0}
+
+
+def word_dtype(vf: str):
+    return np.uint8 if vf.startswith("fp8") else np.uint16
+
+
+def gaussian_values(shape, seed: int, vf: str = "bf16", sigma: float = SIGMA) -> np.ndarray:
+    """N(0, sigma^2) weights as bit patterns of value format vf (uint16 for bf16/fp16, uint8 for fp8)."""
+    if vf == "bf16":
+        return gaussian_bf16(shape, seed, sigma)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = rng.standard_normal(size=int(np.prod(shape)), dtype=np.float32)
+    x *= np.float32(sigma)
+    if vf == "fp16":
+        return x.astype(np.float16).view(np.uint16).reshape(shape)
+    import torch
+    amax = float(np.abs(x).max()) if x.size else 1.0
+    t = torch.from_numpy(x) * (FP8_MAX[vf] / (amax or 1.0))
+    dt = torch.float8_e4m3fn if vf == "fp8_e4m3" else torch.float8_e5m2
+    return t.to(dt).view(torch.uint8).numpy().copy().reshape(shape)
+
+
+def all_patterns(vf: str = "bf16") -> np.ndarray:
+    """Every bit pattern of the format (65 536 or 256 words)."""
+    return np.arange(1 << (8 if vf.startswith("fp8") else 16), dtype=np.uint32).astype(word_dtype(vf))
+
+
 # Whole-model sweeps: units = transformer blocks (+ embedding first, LM head last).
 MODELS = {
     "llama70b_model": dict(block="llama70b_block", blocks=80, vocab=128256, hidden=8192),
@@ -107,14 +140,18 @@ MODELS = {
 }
 
 
-def config_tensors(config: str, layer: int = 0, base_seed: int = 0, sigma: float = SIGMA, dist: str = "gauss"):
+def config_tensors(config: str, layer: int = 0, base_seed: int = 0, sigma: float = SIGMA, dist: str = "gauss",
+                   vf: str = "bf16"):
     """[(name, uint16 array)] for one unit of `config`.  dist: "gauss" (the headline recipe), or the
     realism variants of SURVEY 8(d), reported separately: "t5" (scale * Student-t(5)) and "sigma-lu"
-    (per-tensor sigma log-uniform in [0.01, 0.04], drawn from the tensor's seed)."""
+    (per-tensor sigma log-uniform in [0.01, 0.04], drawn from the tensor's seed).  vf != "bf16": the
+    Gaussian recipe in another value format (gaussian_values; uint8 arrays for fp8)."""
     out = []
     for name, shape in CONFIGS[config]:
         seed = seed_for(config, layer, name, base_seed)
-        if dist == "t5":
+        if vf != "bf16":
+            out.append((name, gaussian_values(shape, seed, vf, sigma)))
+        elif dist == "t5":
             out.append((name, student_t_bf16(shape, seed, 5.0, sigma)))
         elif dist == "sigma-lu":
             s = float(np.exp(np.random.Generator(np.random.PCG64(seed ^ 0x5F5F)).uniform(np.log(0.01), np.log(0.04))))
