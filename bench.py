@@ -41,6 +41,11 @@ def parse():
     p.add_argument("--kernel", choices=["auto", "alg1", "fast"], default="auto")
     p.add_argument("--format", choices=["256x8", "128x16"], default="256x8",
                    help="DF11 format parameters T x n (P:138: n = 8; 128x16 halves the gap bits, NEXT-4)")
+    p.add_argument("--vf", choices=list(workloads.VALUE_FORMATS), default="bf16",
+                   help="value format (NEXT-4, P:609): the paper's BF16, or FP16 / FP8 E4M3 / FP8 E5M2 weights of "
+                        "the same N(0, 0.02) recipe (value = GB/s of decoded words out)")
+    p.add_argument("--lut-bits", default="8",
+                   help="b of the format's b-bit LUTs (App. I.2; 8 = the paper) or 'mono' (App. I.1, b = L)")
     p.add_argument("--dist", choices=["gauss", "t5", "sigma-lu"], default="gauss",
                    help="weight distribution: gauss = the headline recipe; t5 / sigma-lu = realism variants")
     p.add_argument("--no-e2e", action="store_true")
@@ -137,7 +142,11 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def oracle_decode_rate(tensors_np, budget_s: float = 8.0):
+def _word_np(vf):
+    return np.int16 if workloads.word_dtype(vf) is np.uint16 else np.uint8
+
+
+def oracle_decode_rate(tensors_np, budget_s: float = 8.0, vf: str = "bf16", lut_bits=8):
     """Time the CPU oracle on a bounded sample of this workload (whole tensors in config order until
     ~budget_s of single-thread work), two ways (SURVEY 8(d) "CPU oracle timing"):
       D1: the sequential decoder, one thread per tensor (it is sequential by definition);
@@ -152,7 +161,7 @@ def oracle_decode_rate(tensors_np, budget_s: float = 8.0):
     for name, w in tensors_np:
         if fmts and spent + w.size / est_rate > budget_s:
             break
-        fmts.append((name, oracle.encode(w.reshape(-1)), w))
+        fmts.append((name, oracle.encode(w.reshape(-1), vf=vf, lut_bits=lut_bits), w))
         spent += w.size / est_rate
     elems = sum(w.size for _, _, w in fmts)
     host_cores = os.cpu_count() or 1
@@ -168,11 +177,12 @@ def oracle_decode_rate(tensors_np, budget_s: float = 8.0):
             passes += 1
     for (name, _, w), o in zip(fmts, outs):
         assert np.array_equal(o, w.reshape(-1)), name
-    d1 = {"gbs": 2 * elems * passes / dt / 1e9, "threads": d1_threads, "passes": passes, "seconds": round(dt, 2)}
+    wb = np.dtype(workloads.word_dtype(vf)).itemsize
+    d1 = {"gbs": wb * elems * passes / dt / 1e9, "threads": d1_threads, "passes": passes, "seconds": round(dt, 2)}
 
     # D2: every host core on the format blocks of each tensor in turn
     jobs = []
-    outs2 = [np.zeros(w.size, np.uint16) for _, _, w in fmts]
+    outs2 = [np.zeros(w.size, workloads.word_dtype(vf)) for _, _, w in fmts]
     for (name, f, w), o in zip(fmts, outs2):
         B = int(f["B"])
         step = max(1, -(-B // (4 * host_cores)))
@@ -186,7 +196,7 @@ def oracle_decode_rate(tensors_np, budget_s: float = 8.0):
             passes2 += 1
     for (name, _, w), o in zip(fmts, outs2):
         assert np.array_equal(o, w.reshape(-1)), name
-    d2 = {"gbs": 2 * elems * passes2 / dt2 / 1e9, "threads": host_cores, "passes": passes2,
+    d2 = {"gbs": wb * elems * passes2 / dt2 / 1e9, "threads": host_cores, "passes": passes2,
           "seconds": round(dt2, 2)}
     best = d2 if d2["gbs"] >= d1["gbs"] else d1
     sample = (f"{len(fmts)} tensor(s) of the workload ({elems} elements: " + ", ".join(n for n, _, _ in fmts) +
@@ -283,17 +293,22 @@ def main():
         return
 
     # ---- this rank's shard: one transformer block (seeded by rank -> distinct weights per GPU)
-    tensors = workloads.config_tensors(args.config, layer=rank, dist=args.dist)
+    tensors = workloads.config_tensors(args.config, layer=rank, dist=args.dist, vf=args.vf)
+    lut_bits = args.lut_bits if args.lut_bits == "mono" else int(args.lut_bits)
+    wnp = _word_np(args.vf)
+    wtorch = torch.int16 if wnp is np.int16 else torch.uint8
     # host encoder threads: share the host's cores among the ranks of this node
     enc_threads = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", str(world))))
     fT, fn = (int(v) for v in args.format.split("x"))
-    hs = [df11.encode(w, T=fT, n=fn, num_threads=enc_threads) for _, w in tensors]
+    hs = [df11.encode(w, T=fT, n=fn, num_threads=enc_threads, vf=args.vf, lut_bits=lut_bits) for _, w in tensors]
     N = sum(h.num_elements for h in hs)
-    scratch = torch.empty(N + 64, dtype=torch.bfloat16, device=dev)        # reused BF16 scratch
+    wb = df11.VALUE_FORMATS[args.vf][1]                                    # bytes per decoded word
+    upv = 16 // wb                                                         # words per 16 bytes
+    scratch = torch.empty(N + 16 * len(hs) + 64, dtype=df11.out_dtype(args.vf), device=dev)   # reused
     outs, o = [], 0
     for h in hs:
         outs.append(scratch[o:o + h.num_elements])
-        o += (h.num_elements + 7) // 8 * 8                                 # keep views 16-byte aligned
+        o += (h.num_elements + upv - 1) // upv * upv                       # keep views 16-byte aligned
     assert o <= scratch.numel()
     dts = [df11.to_device(h, dev) for h in hs]
     plan = df11.BlockPlan(dts, outs)
@@ -308,11 +323,11 @@ def main():
     plan.run(kernel=kernel_used)
     torch.cuda.synchronize()
     for (name, w), out in zip(tensors, plan.outputs()):
-        ref = torch.from_numpy(w.reshape(-1).view(np.int16)).to(dev)
-        if not torch.equal(out.reshape(-1).view(torch.int16), ref):
+        ref = torch.from_numpy(w.reshape(-1).view(wnp)).to(dev)
+        if not torch.equal(out.reshape(-1).view(wtorch), ref):
             raise SystemExit(f"bit-exact check failed on {name}")
         del ref
-    bf16_bytes = 2 * N
+    bf16_bytes = wb * N                                                    # decoded words written
     algo_bytes = sum(dt.compressed_bytes for dt in dts) + bf16_bytes       # read DF11 + write BF16
     # ---- L2: a step that moves less than 4x L2 would be served partly from L2 when repeated, so the
     # timed steps rotate over device copies of the DF11 arrays and outputs (SURVEY 8(d) timing step 2)
@@ -325,13 +340,13 @@ def main():
         couts, o = [], 0
         for h in hs:
             couts.append(cscratch[o:o + h.num_elements])
-            o += (h.num_elements + 7) // 8 * 8
+            o += (h.num_elements + upv - 1) // upv * upv
         cp = df11.BlockPlan(cdts, couts)
         cp.run(kernel=kernel_used)
         torch.cuda.synchronize()
         for (name, w), out in zip(tensors, cp.outputs()):
-            if not torch.equal(out.reshape(-1).view(torch.int16),
-                               torch.from_numpy(w.reshape(-1).view(np.int16)).to(dev)):
+            if not torch.equal(out.reshape(-1).view(wtorch),
+                               torch.from_numpy(w.reshape(-1).view(wnp)).to(dev)):
                 raise SystemExit(f"bit-exact check failed on copy {c} of {name}")
         plans.append(cp)
     l2_note = (f"inputs larger than L2: {algo_bytes / 1e6:.0f} MB moved per step vs {l2 / 1e6:.0f} MB L2"
@@ -381,17 +396,17 @@ def main():
     # ---- e2e: through the C ABI with host buffers (pinned H2D of the DF11 arrays, decode, D2H of BF16)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(df11, hs, dts, dev, args.e2e_steps, barrier, tensors)
+        e2e = run_e2e(df11, hs, dts, dev, args.e2e_steps, barrier, tensors, args.vf)
 
     # ---- NEXT-2: CPU->GPU transfer of the same BF16 bytes (the paper's comparator)
     transfer = None
     if not args.no_transfer:
-        transfer = run_transfer(tensors, dev, barrier, value)
+        transfer = run_transfer(tensors, dev, barrier, value, wnp)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
-            cpu = oracle_decode_rate(tensors)
+            cpu = oracle_decode_rate(tensors, vf=args.vf, lut_bits=lut_bits)
         except Exception as exc:                                           # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle", "sample": f"failed: {exc}"}
 
@@ -401,9 +416,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": args.config, "dist": args.dist, "tensors": len(hs), "elements_per_gpu": N,
-                       "bf16_bytes_per_gpu": bf16_bytes, "df11_bytes_per_gpu": algo_bytes - bf16_bytes,
+                       ("bf16_bytes_per_gpu" if args.vf == "bf16" else "out_bytes_per_gpu"): bf16_bytes,
+                       "df11_bytes_per_gpu": algo_bytes - bf16_bytes,
                        "bits_per_weight": 8 * (algo_bytes - bf16_bytes) / N, "T": hs[0].T, "n": hs[0].n,
-                       "format": args.format,
+                       "format": args.format, "value_format": args.vf, "lut_bits": hs[0].lut_bits,
                        "kernel": kernel_used, "parallelism": f"shard{world} (one block per GPU, no collective)",
                        "bf16_bytes_all_ranks_per_step": tot_bf16, "l2": l2_note, "l2_copies": copies},
             "roofline": roofline,
@@ -419,12 +435,12 @@ def main():
         dist.destroy_process_group()
 
 
-def run_transfer(tensors, dev, barrier, decode_gbs):
+def run_transfer(tensors, dev, barrier, decode_gbs, wnp=np.int16):
     """Pinned host -> device copy of the block's BF16 weights (what DF11 decode replaces when weights
     are offloaded to CPU memory).  Returns GB/s of BF16 delivered and the decode/transfer ratio."""
     import torch
     import torch.distributed as dist
-    host = [torch.from_numpy(w.reshape(-1).view(np.int16)).pin_memory() for _, w in tensors]
+    host = [torch.from_numpy(w.reshape(-1).view(wnp)).pin_memory() for _, w in tensors]
     dst = [torch.empty_like(h, device=dev) for h in host]
     stream = torch.cuda.current_stream()
     for h, d in zip(host, dst):
@@ -440,7 +456,7 @@ def run_transfer(tensors, dev, barrier, decode_gbs):
     b.record(stream)
     torch.cuda.synchronize()
     from paper_2504_11651_b200 import shard
-    nbytes = sum(h.numel() * 2 for h in host)
+    nbytes = sum(h.numel() * h.element_size() for h in host)
     gbs, _, _ = shard.aggregate_rate(nbytes * reps, a.elapsed_time(b), 1)
     return {"h2d_gbs": gbs, "unit": UNIT, "decode_over_transfer": decode_gbs / gbs,
             "what": "pinned H2D of the block's BF16 weights vs DF11 decode of the same weights on the GPU"}
@@ -578,7 +594,7 @@ def run_model(args, df11, dev, rank, world, nvml, barrier):
         }), flush=True)
 
 
-def run_e2e(df11, hs, dts, dev, steps, barrier, tensors):
+def run_e2e(df11, hs, dts, dev, steps, barrier, tensors, vf="bf16"):
     import torch
 
     from paper_2504_11651_b200 import shard
@@ -602,9 +618,10 @@ def run_e2e(df11, hs, dts, dev, steps, barrier, tensors):
         c.block_output_pos = ctypes.cast(keep["block_output_pos"].data_ptr(), ctypes.POINTER(ctypes.c_uint32))
         pinned_in.append(keep)
         host_views.append(c)
-        host_outs.append(torch.empty(max(h.num_elements, 1), dtype=torch.bfloat16, pin_memory=True))
+        host_outs.append(torch.empty(max(h.num_elements, 1), dtype=df11.out_dtype(vf), pin_memory=True))
+    wb = df11.VALUE_FORMATS[vf][1]
     h2d = sum(dt.staging_bytes() for dt in dts)
-    d2h = sum(2 * h.num_elements for h in hs)
+    d2h = sum(wb * h.num_elements for h in hs)
     N = sum(h.num_elements for h in hs)
 
     import ctypes
@@ -632,10 +649,10 @@ def run_e2e(df11, hs, dts, dev, steps, barrier, tensors):
     torch.cuda.synchronize()
     # the last step's host output must be the original weights
     for ho, h, (name, w) in zip(host_outs, hs, tensors):
-        got = ho[: h.num_elements].view(torch.int16).numpy().view(np.uint16)
-        if not np.array_equal(got, w.reshape(-1)):
+        got = ho[: h.num_elements].view(torch.int16 if wb == 2 else torch.uint8).numpy()
+        if not np.array_equal(got.view(workloads.word_dtype(vf)), w.reshape(-1)):
             raise SystemExit(f"e2e bit-exact check failed on {name}")
-    value, _, _ = shard.aggregate_rate(2 * N, a.elapsed_time(b), steps)
+    value, _, _ = shard.aggregate_rate(wb * N, a.elapsed_time(b), steps)
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "steps": steps, "path": "df11_decompress_host_block (pinned H2D + decode on one stream, D2H overlapped on a second)"}
 

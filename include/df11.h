@@ -13,7 +13,7 @@
  *    host<->device and are CUDA-graph capturable.
  *  - Robustness: malformed device metadata may produce wrong output but never an out-of-bounds
  *    access: every write is clipped to [BlockOutputPos[b], BlockOutputPos[b+1]) ∩ [0, N), LUT walks
- *    are bounded to 4 levels and k tables, and every code step advances at least one bit.
+ *    are bounded to ceil(32/b) levels and k tables, and every code step advances at least one bit.
  *  - Thread safety: no mutable global state except cached device attributes and the last CUDA error.
  */
 #ifndef DF11_H
@@ -39,6 +39,22 @@ typedef enum {
 
 enum { DF11_LUT_AUTO = 0, DF11_LUT_NARROW = 1, DF11_LUT_WIDE = 2 };
 
+/* Value formats (NEXT-4; DESIGN.md §2 and R25-R27).  The paper codes BF16; P:609 names
+ * FP16 and FP8 as its limitation.  Every format is split the same way: the exponent field is the
+ * Huffman symbol, and the residual r = sign << M | mantissa (R = 1 + M bits) is stored raw, MSB-first
+ * at bits [R*i, R*i + R) of PackedSignMantissa (for BF16, R = 8: one byte per element, sign in bit 7,
+ * mantissa in bits 6..0, the paper's layout P:430-431).
+ *   BF16      16-bit words, exponent bits 14..7  (8), R = 8
+ *   FP16      16-bit words, exponent bits 14..10 (5), R = 11
+ *   FP8_E4M3  8-bit words,  exponent bits 6..3   (4), R = 4
+ *   FP8_E5M2  8-bit words,  exponent bits 6..2   (5), R = 3 */
+enum { DF11_VF_BF16 = 0, DF11_VF_FP16 = 1, DF11_VF_FP8_E4M3 = 2, DF11_VF_FP8_E5M2 = 3 };
+
+/* lut_bits (encoder option): b of the b-bit hierarchical LUTs (App. I.2; 0 or 8 = the paper's 256-entry
+ * tables), or DF11_LUT_BITS_MONOLITHIC: one table of 2^L entries (App. I.1),
+ * legal when the longest code L <= 16 (R28). */
+#define DF11_LUT_BITS_MONOLITHIC 255u
+
 /* Kernel selection for df11_decompress_block_ex (AUTO = fast kernel when eligible). */
 enum { DF11_KERNEL_AUTO = 0, DF11_KERNEL_ALG1 = 1, DF11_KERNEL_FAST = 2 };
 
@@ -49,6 +65,8 @@ typedef struct {
     uint32_t bytes_per_thread;     /* n: [4, 32]; default 8 */
     uint32_t lut_mode;             /* DF11_LUT_AUTO | NARROW (paper format) | WIDE */
     uint32_t num_threads;          /* host encoder threads; 0 = all hardware threads */
+    uint32_t value_format;         /* DF11_VF_*; 0 = BF16 (the paper) */
+    uint32_t lut_bits;             /* b in [1, 16], 0 = 8 (the paper), or DF11_LUT_BITS_MONOLITHIC */
 } df11_encode_opts;
 
 /* Host-side DF11 tensor.  All arrays are library-owned, zero-padded as stated. */
@@ -58,18 +76,21 @@ typedef struct {
     uint32_t T, n, B, k;                   /* threads/block, bytes/thread, #blocks, #LUTs */
     uint32_t lut_entry_bytes;              /* 1 = narrow (paper), 2 = wide (R8) */
     uint32_t max_code_len;                 /* L <= 32 */
+    uint32_t value_format;                 /* DF11_VF_* */
+    uint32_t lut_bits;                     /* b: every LUT has 2^b entries (8 = the paper) */
     uint8_t  code_lengths[256];            /* CodeLengths */
-    uint8_t  *luts;              uint64_t luts_bytes;                  /* k*256*lut_entry_bytes; table 0 = root */
+    uint8_t  *luts;              uint64_t luts_bytes;                  /* k*2^b*lut_entry_bytes; table 0 = root */
     uint8_t  *encoded_exponent;  uint64_t encoded_exponent_bytes;      /* B*T*n + 16 */
-    uint8_t  *packed_sign_mantissa; uint64_t packed_sign_mantissa_bytes; /* roundup(N,16) + 16 */
+    uint8_t  *packed_sign_mantissa; uint64_t packed_sign_mantissa_bytes; /* roundup(R*roundup(N,16)/8,16) + 16
+                                                                            (BF16: roundup(N,16) + 16) */
     uint8_t  *gaps;              uint64_t gaps_bytes;                  /* roundup(ceil(5BT/8),16) + 16 */
     uint32_t *block_output_pos;                                        /* B+1 entries, [B] = N */
 } df11_host_tensor;
 
 /* Device view of one DF11 tensor.  Every pointer is a device pointer owned by the caller; arrays
  * must have the sizes of df11_host_tensor (including the zero padding).  `code_lengths` points at
- * 256 device bytes.  `out` receives N BF16 words (16-byte alignment recommended: the fast kernel
- * then writes 128-bit stores). */
+ * 256 device bytes.  `out` receives N words of the value format (16-bit BF16/FP16, 8-bit FP8; 16-byte
+ * alignment recommended: the fast kernel then writes 128-bit stores). */
 typedef struct {
     const uint8_t  *encoded_exponent;
     const uint8_t  *packed_sign_mantissa;
@@ -77,24 +98,27 @@ typedef struct {
     const uint8_t  *luts;
     const uint8_t  *code_lengths;
     const uint32_t *block_output_pos;
-    uint16_t       *out;
+    void           *out;
     uint64_t        num_elements;
     uint32_t        T, n, B, k, lut_entry_bytes;
+    uint32_t        value_format;          /* DF11_VF_* (0 = BF16) */
+    uint32_t        lut_bits;              /* b in [1, 16]; 0 = 8 (the paper) */
     uint32_t        reserved;              /* must be 0 */
 } df11_device_tensor;
 
 /* ---- host encoder --------------------------------------
- * df11_encode: one BF16 tensor (uint16 bit patterns, row-major) -> DF11 with a per-tensor codebook.
- * opts may be NULL (defaults).  N = 0 is legal (B = 0).  Errors: DF11_E_INVALID_ARGUMENT,
- * DF11_E_RESERVED_EXPONENT / DF11_E_LUT_OVERFLOW (NARROW only), DF11_E_TOO_LARGE, DF11_E_ALLOC.
- * On error *out is left zeroed. */
-df11_status df11_encode(const uint16_t *bf16, uint64_t n_elems, const df11_encode_opts *opts,
+ * df11_encode: one tensor of N words of opts->value_format (BF16 by default: uint16 bit patterns;
+ * FP16 uint16; FP8 uint8; row-major) -> DF11 with a per-tensor codebook.  opts may be NULL
+ * (defaults).  N = 0 is legal (B = 0).  Errors: DF11_E_INVALID_ARGUMENT (bad options, or a monolithic
+ * table with L > 16), DF11_E_RESERVED_EXPONENT / DF11_E_LUT_OVERFLOW (NARROW only), DF11_E_TOO_LARGE,
+ * DF11_E_ALLOC.  On error *out is left zeroed. */
+df11_status df11_encode(const void *values, uint64_t n_elems, const df11_encode_opts *opts,
                         df11_host_tensor *out);
 
 /* df11_encode_group: `count` tensors; shared_codebook != 0 builds one codebook from the summed
  * histogram of the group (R5: "a Huffman tree based on the distribution of exponents in model
  * weights") and stores a copy of it in every output; otherwise one codebook per tensor. */
-df11_status df11_encode_group(const uint16_t *const *tensors, const uint64_t *n_elems, uint32_t count,
+df11_status df11_encode_group(const void *const *tensors, const uint64_t *n_elems, uint32_t count,
                               const df11_encode_opts *opts, int shared_codebook, df11_host_tensor *outs);
 
 void df11_host_tensor_free(df11_host_tensor *t);
@@ -131,12 +155,12 @@ void df11_plan_cta_ranges(const uint32_t *entry_start, uint32_t count, uint32_t 
 
 /* ---- end-to-end from host memory --------------------------------------------------------------
  * df11_decompress_host: copies the host arrays of `h` into the caller-provided device staging
- * buffers described by `d` (same sizes as h's arrays), decodes into d->out and copies the BF16
- * result into `host_out` (N words; pinned memory recommended; NULL = leave the result in d->out),
- * all enqueued on `stream`.
+ * buffers described by `d` (same sizes as h's arrays), decodes into d->out and copies the result
+ * into `host_out` (N words of the value format; pinned memory recommended; NULL = leave the result in
+ * d->out), all enqueued on `stream`.
  * Returns after enqueueing; synchronise the stream before reading host_out. */
 df11_status df11_decompress_host(const df11_host_tensor *h, const df11_device_tensor *d,
-                                 uint16_t *host_out, void *stream);
+                                 void *host_out, void *stream);
 
 /* df11_decompress_host_block: df11_decompress_host for `count` tensors (a transformer block),
  * pipelined over two caller-owned streams: the H2D copies and decode of tensor i+1 run on `stream`
@@ -145,7 +169,7 @@ df11_status df11_decompress_host(const df11_host_tensor *h, const df11_device_te
  * host_outs[i] may be NULL for an empty tensor; copy_stream == stream degrades to sequential calls.
  * Errors: as df11_decompress_host; DF11_E_CUDA for stream/event failures. */
 df11_status df11_decompress_host_block(const df11_host_tensor *hs, const df11_device_tensor *ds,
-                                       uint16_t *const *host_outs, uint32_t count, void *stream,
+                                       void *const *host_outs, uint32_t count, void *stream,
                                        void *copy_stream);
 
 /* ---- device encoder (format P:97; Table `time` P:471-486) -------
@@ -170,11 +194,13 @@ typedef struct {
 } df11_device_buffers;
 
 /* Codebook + geometry of one tensor, built on the host.  `luts` is library-owned host memory: free
- * the plan with df11_encode_plan_free. */
+ * the plan with df11_encode_plan_free.  The device encoder codes BF16 (any lut_bits); other value
+ * formats are DF11_E_UNSUPPORTED there (use df11_encode). */
 typedef struct {
     uint64_t num_elements;            /* N = sum of tensor_hist */
     uint64_t encoded_bits;            /* sum over the tensor of code lengths */
     uint32_t T, n, B, k, lut_entry_bytes, max_code_len;
+    uint32_t lut_bits;                /* b (the plan's tables have 2^b entries) */
     uint8_t  code_lengths[256];
     uint32_t codes[256];              /* canonical codes, right-aligned, MSB-first when emitted */
     uint8_t  *luts;             uint64_t luts_bytes;

@@ -57,6 +57,8 @@ df11_status validate(const df11_device_tensor &t, uint32_t idx) {
         return df11_fail(DF11_E_INVALID_ARGUMENT, buf);
     };
     if (t.reserved != 0) return bad("reserved field must be 0");
+    if (t.value_format > DF11_VF_FP8_E5M2) return bad("bad value_format");
+    if (t.lut_bits > 16) return bad("lut_bits must be in [1, 16] (0 = 8)");
     if (t.num_elements >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "N >= 2^32");
     if (t.num_elements == 0) return DF11_OK;                     // empty tensor: no-op (R11)
     if (t.B == 0) return bad("B == 0 with N > 0");
@@ -66,7 +68,7 @@ df11_status validate(const df11_device_tensor &t, uint32_t idx) {
     if (t.k == 0) return bad("k == 0 with N > 0");
     if (t.lut_entry_bytes == 1 && t.k > 17) return bad("narrow LUTs allow at most 17 tables");
     // a codebook of <= 256 symbols has <= 255 internal nodes, so <= 256 tables; the bound also keeps
-    // every LUT byte offset k * 256 * entry_bytes (<= 128 KB) inside 32-bit arithmetic in the kernels
+    // every LUT byte offset k * 2^b * entry_bytes (<= 32 MB) inside 32-bit arithmetic in the kernels
     if (t.k > 256) return bad("at most 256 LUTs");
     if ((uint64_t)t.B * t.T * t.n * 8 > (uint64_t)t.num_elements * 32 + (uint64_t)t.T * t.n * 8)
         return bad("B too large for N (codes are at most 32 bits)");
@@ -226,7 +228,7 @@ extern "C" df11_status df11_decompress_block_budget(const df11_device_tensor *ts
     if (kernel == DF11_KERNEL_FAST && nslow)
         return df11_fail(DF11_E_UNSUPPORTED,
                          "fast kernel: a tensor is outside its parameter range (T=256, n=8 or T=128, n=16; 16-byte "
-                         "aligned buffers)");
+                         "aligned buffers, output aligned to its word size)");
     cudaStream_t stream = (cudaStream_t)stream_v;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -265,10 +267,11 @@ extern "C" df11_status df11_decompress(const df11_device_tensor *t, void *stream
 }
 
 extern "C" df11_status df11_decompress_host(const df11_host_tensor *h, const df11_device_tensor *d,
-                                            uint16_t *host_out, void *stream_v) {
+                                            void *host_out, void *stream_v) {
     if (!h || !d) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL argument");
     if (d->num_elements != h->num_elements || d->B != h->B || d->T != h->T || d->n != h->n || d->k != h->k ||
-        d->lut_entry_bytes != h->lut_entry_bytes)
+        d->lut_entry_bytes != h->lut_entry_bytes || d->value_format != h->value_format ||
+        df11::lut_bits_of(*d) != (h->lut_bits ? h->lut_bits : 8u))
         return df11_fail(DF11_E_INVALID_ARGUMENT, "device descriptor does not match the host tensor");
     if (h->num_elements == 0) return DF11_OK;
     cudaStream_t s = (cudaStream_t)stream_v;
@@ -288,13 +291,14 @@ extern "C" df11_status df11_decompress_host(const df11_host_tensor *h, const df1
     df11_status st = df11_decompress(d, stream_v);
     if (st != DF11_OK) return st;
     if (!host_out) return DF11_OK;                   // decode only: the result stays in d->out
-    cudaError_t e = cudaMemcpyAsync(host_out, d->out, 2ull * h->num_elements, cudaMemcpyDeviceToHost, s);
+    const uint64_t out_bytes = (uint64_t)df11::vf_of(h->value_format).word_bytes * h->num_elements;
+    cudaError_t e = cudaMemcpyAsync(host_out, d->out, out_bytes, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
     return DF11_OK;
 }
 
 extern "C" df11_status df11_decompress_host_block(const df11_host_tensor *hs, const df11_device_tensor *ds,
-                                                  uint16_t *const *host_outs, uint32_t count, void *stream_v,
+                                                  void *const *host_outs, uint32_t count, void *stream_v,
                                                   void *copy_stream_v) {
     if (count && (!hs || !ds || !host_outs)) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL argument");
     cudaStream_t s = (cudaStream_t)stream_v, cs = (cudaStream_t)copy_stream_v;
@@ -320,7 +324,9 @@ extern "C" df11_status df11_decompress_host_block(const df11_host_tensor *hs, co
         st = df11_decompress_host(h, d, nullptr, stream_v);   // H2D + decode
         if (st != DF11_OK || !h->num_elements) continue;
         if ((e = cudaEventRecord(ev, s)) != cudaSuccess || (e = cudaStreamWaitEvent(cs, ev, 0)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(host_outs[i], d->out, 2ull * h->num_elements, cudaMemcpyDeviceToHost, cs)) !=
+            (e = cudaMemcpyAsync(host_outs[i], d->out,
+                                 (uint64_t)df11::vf_of(h->value_format).word_bytes * h->num_elements,
+                                 cudaMemcpyDeviceToHost, cs)) !=
                 cudaSuccess)
             st = cuda_fail(e, "D2H copy");
     }

@@ -1,17 +1,18 @@
 // decode_alg1.cu — the paper's two-phase kernel, Algorithm 1 "DF11ToBF16", written
-// literally for sm_100a.  It is the baseline the fast kernel (decode_fast.cu) is measured against,
-// and the fallback for format parameters the fast kernel does not specialise (any T multiple of 32,
-// any n in [4, 32], narrow or wide LUTs of any size).
+// literally for sm_100a.  It is the baseline the product kernel (decode_sp12.cu) is measured against,
+// and the fallback for format parameters that kernel does not specialise (any T multiple of 32, any n
+// in [4, 32], narrow or wide LUTs of any size and any b, every value format).
 //
 //   one CTA per format block b, blockDim = T
 //   SRAM: EncodedExponent_b (+4 spill bytes), LUT_1..LUT_k, CodeLengths
 //   phase 1: per-thread LUT walk + count, BitOffset from Gaps[bT+t]
 //   Blelloch work-efficient exclusive scan of the counts
 //   phase 2: re-decode, compose with PackedSignMantissa[pos] into a WriteBuffer
+//            (value formats other than BF16: the residual is the R-bit field at bit R*pos, R25)
 //   one batch of coalesced writes of WriteBuffer to Outputs[BOP[b]..BOP[b+1])
 //
 // Robustness (df11.h): positions are clipped to [BOP[b], BOP[b+1]) ∩ [0, N) and to the buffer size;
-// LUT walks stop after 4 levels or on a child index >= k; a zero code length advances 32 bits.
+// LUT walks stop after ceil(32/b) levels or on a child index >= k; a zero code length advances 32 bits.
 #include "decode_common.cuh"
 
 namespace df11 {
@@ -24,12 +25,14 @@ __global__ void __launch_bounds__(1024) alg1_kernel(const __grid_constant__ Batc
     const df11_device_tensor &ts = bt.t[ti];
     const uint32_t b = g_tile - bt.tile_start[ti];
     const uint32_t T = ts.T, n = ts.n, k = ts.k, eb = ts.lut_entry_bytes;
+    const uint32_t lb = lut_bits_of(ts), tsize = 1u << lb;       // b-bit tables (App. I.2)
+    const VF vf = vf_of(ts.value_format);
     const uint32_t t = threadIdx.x;
     const uint64_t N = ts.num_elements;
 
     // ---- SRAM carve-up
-    const uint32_t lut_bytes = kLutInSmem ? k * 256u * eb : 0u;
-    uint8_t *s_lut = smem;                                         // k*256*eb
+    const uint32_t lut_bytes = kLutInSmem ? k * tsize * eb : 0u;
+    uint8_t *s_lut = smem;                                         // k*2^b*eb
     uint8_t *s_len = smem + ((lut_bytes + 15u) & ~15u);            // 256
     uint8_t *s_chunk = s_len + 256;                                // T*n + 4 (rounded to 16)
     uint32_t *s_count = (uint32_t *)(s_chunk + ((T * n + 4u + 15u) & ~15u));  // pow2 >= T
@@ -49,7 +52,7 @@ __global__ void __launch_bounds__(1024) alg1_kernel(const __grid_constant__ Batc
 
     const uint8_t *lut = kLutInSmem ? s_lut : ts.luts;
     auto lut_at = [&](uint32_t table, uint32_t idx) -> uint32_t {
-        uint32_t off = table * 256u + idx;
+        uint32_t off = (table << lb) + idx;
         if (eb == 1) return kLutInSmem ? lut[off] : __ldg(lut + off);
         uint32_t lo = kLutInSmem ? lut[2 * off] : __ldg(lut + 2 * off);
         uint32_t hi = kLutInSmem ? lut[2 * off + 1] : __ldg(lut + 2 * off + 1);
@@ -65,16 +68,22 @@ __global__ void __launch_bounds__(1024) alg1_kernel(const __grid_constant__ Batc
         return (uint32_t)(v >> (8u - (bit_offset & 7u)));
     };
     // LUT walk: Exponent >= 240 is a pointer to LUT_{257-Exponent} (narrow), >= 256 (wide).
+    // Level i reads window bits [b(i-1), bi) (b = 8: Byte_i), zero-extended past bit 32 (R28).
+    const uint32_t levels = (32u + lb - 1u) / lb;
+    auto level_idx = [&](uint32_t w, uint32_t i) -> uint32_t {    // i: 1-based level
+        const uint64_t w64 = (uint64_t)w << 32;
+        return (uint32_t)(w64 >> (64u - lb * i)) & (tsize - 1u);
+    };
     auto decode_one = [&](uint32_t w, uint32_t &len) -> uint32_t {
-        uint32_t e = lut_at(0, w >> 24);
+        uint32_t e = lut_at(0, level_idx(w, 1));
         uint32_t i = 1;
         while (e >= ptr_threshold) {
             i++;
             uint32_t table = eb == 1 ? 256u - e : e - 256u;
-            if (i > 4 || table >= k) { e = 0; break; }             // malformed: bounded
-            e = lut_at(table, (w >> (32u - 8u * i)) & 0xFFu);
+            if (i > levels || table >= k) { e = 0; break; }        // malformed: bounded
+            e = lut_at(table, level_idx(w, i));
         }
-        e &= 0xFFu;
+        e &= vf.emask;                                             // a symbol is an exponent field
         len = s_len[e];
         if (len == 0) len = 32;                                    // malformed: still advances
         return e;
@@ -124,10 +133,9 @@ __global__ void __launch_bounds__(1024) alg1_kernel(const __grid_constant__ Batc
         uint32_t len;
         uint32_t e = decode_one(window(bit_offset), len);
         if (pos < bop_hi) {
-            uint32_t byte = __ldg(ts.packed_sign_mantissa + pos);
-            uint16_t v = compose(e, byte);
+            const uint16_t v = (uint16_t)compose_vf(vf, e, load_residual(vf, ts.packed_sign_mantissa, pos));
             if (kUseWriteBuffer) s_wbuf[pos - bop_lo] = v;
-            else ts.out[pos] = v;
+            else store_word(vf, ts.out, pos, v);
         }
         bit_offset += len;
         pos++;
@@ -136,7 +144,7 @@ __global__ void __launch_bounds__(1024) alg1_kernel(const __grid_constant__ Batc
     if (kUseWriteBuffer) {
         __syncthreads();
         const uint32_t cnt = (uint32_t)(bop_hi - bop_lo);
-        for (uint32_t i = t; i < cnt; i += T) ts.out[bop_lo + i] = s_wbuf[i];
+        for (uint32_t i = t; i < cnt; i += T) store_word(vf, ts.out, bop_lo + i, s_wbuf[i]);
     }
 }
 
@@ -157,7 +165,7 @@ cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream
     for (uint32_t i = 0; i < bt.count; i++) {
         if (bt.t[i].B == 0) continue;
         n_max = max(n_max, bt.t[i].n);
-        lut_max = max(lut_max, (size_t)bt.t[i].k * 256u * bt.t[i].lut_entry_bytes);
+        lut_max = max(lut_max, (size_t)bt.t[i].k * ((size_t)1 << lut_bits_of(bt.t[i])) * bt.t[i].lut_entry_bytes);
     }
     bool lut_smem = true, wbuf = true;
     size_t need = alg1_smem_bytes(T, n_max, lut_max, true, true);

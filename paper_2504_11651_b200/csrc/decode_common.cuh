@@ -42,6 +42,41 @@ __device__ __forceinline__ uint16_t compose(uint32_t exponent, uint32_t psm) {
     return (uint16_t)(((psm & 0x80u) << 8) | (exponent << 7) | (psm & 0x7Fu));
 }
 
+// b of the format's LUTs (0 = 8, the paper's byte tables).
+__host__ __device__ __forceinline__ uint32_t lut_bits_of(const df11_device_tensor &t) {
+    return t.lut_bits ? t.lut_bits : 8u;
+}
+
+// Value formats (df11.h DF11_VF_*, R25): M mantissa bits, E exponent bits, residual R = 1 + M bits at
+// PackedSignMantissa bits [R*i, R*i + R), words of 2 (BF16/FP16) or 1 (FP8) bytes.
+struct VF {
+    uint32_t M, E, R, emask, word_bytes;
+};
+__host__ __device__ constexpr VF vf_of(uint32_t value_format) {
+    switch (value_format) {
+        case DF11_VF_FP16: return {10, 5, 11, 31, 2};
+        case DF11_VF_FP8_E4M3: return {3, 4, 4, 15, 1};
+        case DF11_VF_FP8_E5M2: return {2, 5, 3, 31, 1};
+        default: return {7, 8, 8, 255, 2};
+    }
+}
+// sign << (E + M) | exponent << M | mantissa from the residual r = sign << M | mantissa
+__device__ __forceinline__ uint32_t compose_vf(const VF &f, uint32_t e, uint32_t r) {
+    return ((r >> f.M) << (f.E + f.M)) | ((e & f.emask) << f.M) | (r & ((1u << f.M) - 1u));
+}
+// Residual of element i: R bits MSB-first at bit R*i (R <= 11: inside a 3-byte window).
+__device__ __forceinline__ uint32_t load_residual(const VF &f, const uint8_t *__restrict__ psm, uint64_t i) {
+    if (f.R == 8) return __ldg(psm + i);
+    const uint64_t bit = (uint64_t)f.R * i;
+    const uint8_t *p = psm + (bit >> 3);
+    const uint32_t v = ((uint32_t)__ldg(p) << 16) | ((uint32_t)__ldg(p + 1) << 8) | __ldg(p + 2);
+    return (v >> (24u - (uint32_t)(bit & 7) - f.R)) & ((1u << f.R) - 1u);
+}
+__device__ __forceinline__ void store_word(const VF &f, void *out, uint64_t i, uint32_t v) {
+    if (f.word_bytes == 2) static_cast<uint16_t *>(out)[i] = (uint16_t)v;
+    else static_cast<uint8_t *>(out)[i] = (uint8_t)v;
+}
+
 // 5-bit gap field g, MSB-first at bits [5g, 5g+5) (R12).
 __device__ __forceinline__ uint32_t load_gap(const uint8_t *__restrict__ gaps, uint64_t g) {
     uint64_t bit = 5ull * g;

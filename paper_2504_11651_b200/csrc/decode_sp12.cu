@@ -28,6 +28,8 @@
 //    512 contiguous bytes (4 L1 wavefronts; two 16-byte halves per lane 32 bytes apart took 8).
 //  * A tile's PackedSignMantissa range is staged in SMEM by one TMA bulk copy; the first tile's copies
 //    are issued before the table build; per-CTA tile ranges come from df11_plan_cta_ranges (api.cu).
+#include <type_traits>
+
 #include "t12_common.cuh"
 
 namespace df11 {
@@ -53,30 +55,93 @@ constexpr uint32_t kWarpReg12 = 16 + 2 * kSubW * 128;   // frame pad + lane-colu
 constexpr uint32_t kOffT = 0;                                       // T12 (t12_common.cuh)
 constexpr uint32_t kOffLut = kOffT + kT12Bytes;
 constexpr uint32_t kOffLen = kOffLut + kLutSmem;                    // CodeLengths[e]
-constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengths[unrot(r)]
-constexpr uint32_t kSmCap = 7168;           // PackedSignMantissa bytes of one tile staged in SMEM
+constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengths[stored symbol]
+constexpr uint32_t kOffGrp = kOffRLen + 256;                        // [groups][kGrpBytes]
+// PackedSignMantissa bytes of one tile staged in SMEM: BF16 ~6.3 KB per tile on LLM weights; FP16
+// (11-bit residuals, NEXT-4) ~8.7 KB: it takes the SMEM left over (tiles above the cap read their
+// residuals through L1/L2 instead)
+constexpr uint32_t sm_cap(uint32_t vf) { return vf == DF11_VF_FP16 ? 11200u : 7168u; }
 // one block per group, so that every per-group / per-warp address is one base register plus an
 // immediate offset
-constexpr uint32_t kOffGrp = kOffRLen + 256;                        // [groups][kGrpBytes]
-constexpr uint32_t kGStage = 0;                                     // stream chunk + gaps (TMA)
-constexpr uint32_t kGSm = kGStage + kStageBytes;                    // PackedSignMantissa (TMA)
-constexpr uint32_t kGReg = kGSm + kSmCap;                           // [warps][kWarpReg12] slots / regions
-constexpr uint32_t kGWsum = kGReg + kWarps12 * kWarpReg12;          // [2][warps] warp totals
-constexpr uint32_t kGCnt = kGWsum + 2 * kWarps12 * 4;               // warps done with the merge
-constexpr uint32_t kGMbar = kGCnt + 16;                             // [stage, sign/mantissa] mbarriers
-constexpr uint32_t kGrpBytes = kGMbar + 16;
-constexpr uint32_t kSmem12 = kOffGrp + kGroups12 * kGrpBytes;
-static_assert(kOffGrp % 16 == 0 && kGSm % 16 == 0 && kGReg % 16 == 0 && kWarpReg12 % 16 == 0 &&
-                  kGWsum % 16 == 0 && kGMbar % 8 == 0 && kGrpBytes % 16 == 0,
-              "alignment");
-static_assert(kWarps12 * kWarpReg12 >= 8192, "first-code table scratch fits group 0's warp regions");
-static_assert(kSmem12 <= 232448, "SMEM budget");
+template <uint32_t kVF>
+struct Lay12 {
+    static constexpr uint32_t kSmCap = sm_cap(kVF);
+    static constexpr uint32_t kGStage = 0;                          // stream chunk + gaps (TMA)
+    static constexpr uint32_t kGSm = kGStage + kStageBytes;         // PackedSignMantissa (TMA)
+    static constexpr uint32_t kGReg = kGSm + kSmCap;                // [warps][kWarpReg12] slots / regions
+    static constexpr uint32_t kGWsum = kGReg + kWarps12 * kWarpReg12;   // [2][warps] warp totals
+    static constexpr uint32_t kGCnt = kGWsum + 2 * kWarps12 * 4;    // warps done with the merge
+    static constexpr uint32_t kGMbar = kGCnt + 16;                  // [stage, sign/mantissa] mbarriers
+    static constexpr uint32_t kGrpBytes = kGMbar + 16;
+    static constexpr uint32_t kSmem = kOffGrp + kGroups12 * kGrpBytes;
+    static_assert(kOffGrp % 16 == 0 && kGSm % 16 == 0 && kGReg % 16 == 0 && kWarpReg12 % 16 == 0 &&
+                      kGWsum % 16 == 0 && kGMbar % 8 == 0 && kGrpBytes % 16 == 0,
+                  "alignment");
+    static_assert(kWarps12 * kWarpReg12 >= 8192, "first-code table scratch fits group 0's warp regions");
+    static_assert(kSmem <= 232448, "SMEM budget");
+};
+
+// ---- merge helpers of the value formats other than BF16 (NEXT-4, R25): a unit is 16 output bytes
+// (8 FP16 / 16 FP8 words) and its residuals are R * (unit words) / 8 bytes at SMEM byte address o.
+// Eight FP16 words from 8 exponents (bytes of x0, x1) and eight 11-bit residuals s << 10 | m at o.
+__device__ __forceinline__ uint4 unit_fp16(uint32_t x0, uint32_t x1, uint32_t o) {
+    const uint32_t base = o & ~3u, sh = (o & 3u) * 8u;
+    const uint32_t B0 = bswap32(lds32(base)), B1 = bswap32(lds32(base + 4)), B2 = bswap32(lds32(base + 8));
+    uint32_t B3 = 0;
+    if (sh >= 16) B3 = bswap32(lds32(base + 12));      // 11 bytes from byte 2 or 3 reach a 4th word
+    const uint32_t H0 = __funnelshift_l(B1, B0, sh), H1 = __funnelshift_l(B2, B1, sh),
+                   H2 = __funnelshift_l(B3, B2, sh);   // the 88 residual bits, MSB-first
+    const uint32_t f0 = H0 >> 21, f1 = (H0 >> 10) & 0x7FFu, f2 = __funnelshift_l(H1, H0, 22) >> 21,
+                   f3 = (H1 >> 20) & 0x7FFu, f4 = (H1 >> 9) & 0x7FFu, f5 = __funnelshift_l(H2, H1, 23) >> 21,
+                   f6 = (H2 >> 19) & 0x7FFu, f7 = (H2 >> 8) & 0x7FFu;
+    // a pair: (s << 15 | e << 10 | m) in each 16-bit half
+    auto pair = [](uint32_t fa, uint32_t fb, uint32_t E) {
+        const uint32_t F = fa | (fb << 16);
+        return ((F << 5) & 0x80008000u) | (F & 0x03FF03FFu) | (E << 10);
+    };
+    uint4 r;
+    r.x = pair(f0, f1, prmt(x0, 0u, 0x4140u));
+    r.y = pair(f2, f3, prmt(x0, 0u, 0x4342u));
+    r.z = pair(f4, f5, prmt(x1, 0u, 0x4140u));
+    r.w = pair(f6, f7, prmt(x1, 0u, 0x4342u));
+    return r;
+}
+// Four FP8 E4M3 bytes from 4 exponents E and the nibbles of residual bytes (b_lo, b_hi) of word r
+// (element 2j in the high nibble of byte j): s << 7 | e << 3 | m.
+template <uint32_t kSel>
+__device__ __forceinline__ uint32_t quad_e4m3(uint32_t r, uint32_t E) {
+    const uint32_t P = prmt(r, 0u, kSel);                // [b, b, b', b']
+    const uint32_t N = bitsel<0xFF00FF00u>(P >> 4, P);   // low nibble of byte j = residual of element j
+    return ((N << 4) & 0x80808080u) | (N & 0x07070707u) | (E << 3);
+}
+// Four FP8 E5M2 bytes from 4 exponents E and 12 residual bits u (element 0 in bits 11..9): s << 7 |
+// e << 2 | m.
+__device__ __forceinline__ uint32_t quad_e5m2(uint32_t u, uint32_t E) {
+    const uint32_t W = ((u >> 9) & 7u) | (((u >> 6) & 7u) << 8) | (((u >> 3) & 7u) << 16) | ((u & 7u) << 24);
+    return ((W << 5) & 0x80808080u) | (W & 0x03030303u) | (E << 2);
+}
+// Residual of one element from the SMEM staging: R bits at bit position `bit` of the buffer at `buf`.
+template <uint32_t kR_>
+__device__ __forceinline__ uint32_t res_smem(uint32_t buf, uint32_t bit) {
+    const uint32_t p = buf + (bit >> 3), end = (bit & 7u) + kR_;   // bytes read: only those it spans
+    uint32_t v = ld8(p) << 16;
+    if (end > 8) v |= ld8(p + 1) << 8;
+    if (end > 16) v |= ld8(p + 2);
+    return (v >> (24u - end)) & ((1u << kR_) - 1u);
+}
 
 // kNB = 8: the paper's format (T = 256, n = 8); a lane decodes two 8-byte chunks as two chains.
 // kNB = 16: T = 128, n = 16 (NEXT-4: half the gap bits); a format block has the same 2 048 stream
 // bytes and a lane decodes its one 16-byte chunk as one chain in a 160-bit buffer.
-template <uint32_t kNB>
+// kVF: value format (DF11_VF_*, NEXT-4).  Decode, scan and compaction are the same for every format
+// (the symbols are exponent fields); the merge composes the format's words.
+template <uint32_t kNB, uint32_t kVF>
 __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__ Batch bt) {
+    using L = Lay12<kVF>;
+    constexpr VF kF = vf_of(kVF);
+    constexpr uint32_t kRb = kF.R;                        // residual bits per element
+    constexpr uint32_t kU = 16 / kF.word_bytes;           // words per 16-byte output unit
+    using OutT = typename std::conditional<kF.word_bytes == 2, uint16_t, uint8_t>::type;
     const uint32_t tid = threadIdx.x;
     const uint32_t g = tid / kLanes;
     const uint32_t t = tid % kLanes;
@@ -89,13 +154,13 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     uint8_t *sb = smem_b();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
     const uint32_t tab = sbase + kOffT;
-    const uint32_t gbase = sbase + kOffGrp + g * kGrpBytes;           // this group's block
-    const uint32_t wreg = gbase + kGReg + wig * kWarpReg12;           // this warp's region
-    const uint32_t stage = gbase + kGStage;
-    const uint32_t mbar = gbase + kGMbar;
+    const uint32_t gbase = sbase + kOffGrp + g * L::kGrpBytes;           // this group's block
+    const uint32_t wreg = gbase + L::kGReg + wig * kWarpReg12;           // this warp's region
+    const uint32_t stage = gbase + L::kGStage;
+    const uint32_t mbar = gbase + L::kGMbar;
     const uint32_t smbar = mbar + 8;                        // the tile's PackedSignMantissa has landed
-    const uint32_t smb = gbase + kGSm;
-    const uint32_t mcnt = gbase + kGCnt;
+    const uint32_t smb = gbase + L::kGSm;
+    const uint32_t mcnt = gbase + L::kGCnt;
     const uint32_t slotA = wreg + 16u + lane * 4u, slotB = slotA + kSubW * 128u;
     const uint32_t rlenb = sbase + kOffRLen;
 
@@ -135,24 +200,25 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             }
         }
         bool safe, lut_in_smem;
-        const bool long_codes = build_t12<kCta12>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen, kOffGrp + kGReg, tid,
-                                                  safe, lut_in_smem);
+        const bool long_codes = build_t12<kCta12, kVF>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
+                                                       kOffGrp + L::kGReg, tid, safe, lut_in_smem);
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
 
         const uint32_t N = (uint32_t)ts.num_elements;
         const bool vec_out = ((reinterpret_cast<uintptr_t>(ts.out) & 15) == 0);
         const uint2 *__restrict__ psm2 = reinterpret_cast<const uint2 *>(ts.packed_sign_mantissa);
-        uint16_t *__restrict__ out = ts.out;
+        OutT *__restrict__ out = static_cast<OutT *>(ts.out);
         // PackedSignMantissa of a tile, [a0, a1) = its output range widened to 16 bytes, is staged in
         // SMEM by one TMA bulk copy (issued by the last warp to finish the previous tile's merge) when
         // it fits kSmCap; otherwise it is prefetched into L2 and read with LDG in the merge.
         const bool psm_al = (reinterpret_cast<uintptr_t>(ts.packed_sign_mantissa) & 15) == 0;   // bulk copies
         const bool sm_tma = vec_out && !safe && psm_al;
+        // [a0, a1): bytes of the residuals of outputs [l & ~15, (h + 15) & ~15), widened to 16 bytes
         auto sm_range = [&](uint32_t plo, uint32_t phi, uint32_t &a0, uint32_t &a1) {
             const uint32_t l = min(plo, N), h = min(max(min(phi, N), l), l + 8 * kN * kT);
-            a0 = l & ~15u;
-            a1 = (h + 15u) & ~15u;
-            return sm_tma && a1 > a0 && a1 - a0 <= kSmCap;
+            a0 = ((l & ~15u) / 8u * kRb) & ~15u;
+            a1 = (((h + 15u) & ~15u) / 8u * kRb + 15u) & ~15u;
+            return sm_tma && a1 > a0 && a1 - a0 <= L::kSmCap;
         };
         auto stage_sm = [&](uint32_t plo, uint32_t phi) {
             uint32_t a0, a1;
@@ -166,7 +232,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         if (t == 0 && tile < seg_end) stage_sm(nlo, nhi);
 
         auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
-            if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, len);
+            if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, 8u, len);
             return lut_walk_global(w, ts, len);
         };
 
@@ -249,14 +315,14 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                         if (__any_sync(FULL, escA || escB)) {
                             if (escA) {
                                 uint32_t len;
-                                const uint32_t r = rot8(walk(aA, len));
+                                const uint32_t r = to_stored<kVF>(walk(aA, len));
                                 pack(oA, r & 0xFFu, 8u << 24, K_S24);
                                 xA += len;
                                 shift96_long_ones(aA, bA, cA, len);
                             }
                             if (escB) {
                                 uint32_t len;
-                                const uint32_t r = rot8(walk(aB, len));
+                                const uint32_t r = to_stored<kVF>(walk(aB, len));
                                 pack(oB, r & 0xFFu, 8u << 24, K_S24);
                                 xB += len;
                                 shift96_long_ones(aB, bB, cB, len);
@@ -348,7 +414,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     if (__any_sync(FULL, escA)) {
                         if (escA) {
                             uint32_t len;
-                            const uint32_t r = rot8(walk(a, len));
+                            const uint32_t r = to_stored<kVF>(walk(a, len));
                             pack(oA, r & 0xFFu, 8u << 24, K_S24);
                             xA += len;
                             shift160_long_ones(a, b1, c, d, e, len);
@@ -401,7 +467,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 const uint32_t v = __shfl_up_sync(FULL, incl, d);
                 if (lane >= (uint32_t)d) incl += v;
             }
-            const uint32_t ws = gbase + kGWsum + parity * (kWarps12 * 4);
+            const uint32_t ws = gbase + L::kGWsum + parity * (kWarps12 * 4);
             if (lane == 31) sts32(ws + wig * 4, incl);
             group_bar(g);                          // also: every thread has read this tile's stage
             parity ^= 1u;
@@ -434,9 +500,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                         while (p < pend && off < lim_off) {
                             uint32_t el, eh, len, sym;
                             lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
-                            if ((eh & 0xFFFFu) != 0) { sym = unrot8(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
+                            if ((eh & 0xFFFFu) != 0) { sym = from_stored<kVF>(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
                             else sym = walk(a, len);
-                            out[p] = compose(sym, __ldg(ts.packed_sign_mantissa + p));
+                            out[p] = (OutT)compose_vf(kF, sym, load_residual(kF, ts.packed_sign_mantissa, p));
                             p++;
                             off += len;
                             shift96_long(a, bb, c, len);
@@ -448,9 +514,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     while (p < pend && off < 128u) {
                         uint32_t el, eh, len, sym;
                         lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
-                        if ((eh & 0xFFFFu) != 0) { sym = unrot8(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
+                        if ((eh & 0xFFFFu) != 0) { sym = from_stored<kVF>(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
                         else sym = walk(a, len);
-                        out[p] = compose(sym, __ldg(ts.packed_sign_mantissa + p));
+                        out[p] = (OutT)compose_vf(kF, sym, load_residual(kF, ts.packed_sign_mantissa, p));
                         p++;
                         off += len;
                         shift160_long_ones(a, b1, c, d, e, len);
@@ -462,10 +528,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             // ---- this warp's output range
             const uint32_t F = wbeg & ~15u;                                    // region byte of e: e - F
             const uint32_t ra = min(wbeg, hi), rb = min(wbeg + wtot, hi);
-            // 8-element units [ua, ub) leave with one STG.128 each; head [ra, ha) and tail [tb, rb) (< 8
-            // elements each) one element per lane
-            const uint32_t ua = vec_out ? (ra + 7) >> 3 : 0, ub = vec_out ? max(rb >> 3, ua) : 0;
-            const uint32_t ha = vec_out ? min(ua << 3, rb) : rb, tb = vec_out ? max(ub << 3, ha) : rb;
+            // kU-word units [ua, ub) (16 bytes: 8 BF16/FP16 or 16 FP8 words) leave with one STG.128 each;
+            // head [ra, ha) and tail [tb, rb) (< kU words each) one element per lane
+            const uint32_t ua = vec_out ? (ra + kU - 1) / kU : 0, ub = vec_out ? max(rb / kU, ua) : 0;
+            const uint32_t ha = vec_out ? min(ua * kU, rb) : rb, tb = vec_out ? max(ub * kU, ha) : rb;
             const uint32_t es = lane < 16 ? ra + lane : tb + (lane - 16);
             const bool edge = vec_out && (lane < 16 ? es < ha : es < rb);
 
@@ -525,17 +591,16 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 __syncwarp();
             }
 
-            // ---- per-warp merge of [ra, rb): compose BF16 and store
+            // ---- per-warp merge of [ra, rb): compose the words and store
             uint32_t a0, a1;
             if (sm_range(lo, hi, a0, a1)) {
                 mbar_wait(smbar, qs & 1u);                                     // PackedSignMantissa staged
                 qs++;
-                if (edge) out[es] = compose_r(ld8(wreg + (es - F)), ld8(smb + (es - a0)));
-#ifndef SP12_MERGE_LOOP
                 // lane l stores units u0 + 32k: every STG.128 of the warp covers 512 contiguous bytes.
                 // A warp range has <= 64 * 32 outputs (<= 257 units, <= 9 per lane); the unit stride is
                 // an immediate offset of the loads and stores.
-                {
+                if constexpr (kVF == DF11_VF_BF16) {
+                    if (edge) out[es] = compose_r(ld8(wreg + (es - F)), ld8(smb + (es - a0)));
                     // warp-uniform trip count: every lane stores (ub - ua) / 32 units, lanes below
                     // (ub - ua) % 32 one more
                     const uint32_t nun = ub - ua, nfull = nun >> 5;
@@ -560,31 +625,41 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     }
                     for (; k < nfull; k++) unit(k);
                     if (lane < (nun & 31u)) unit(nfull);
-                }
-#else
-                // lane l stores units u and u + 32 of each 64-unit stretch: every STG.128 of the warp
-                // covers 512 contiguous bytes
-                for (uint32_t u = ua + lane; u < ub; u += 64) {
-                    const bool two = u + 32 < ub;
-                    const uint32_t e0 = u << 3, e1 = e0 + 256;
-                    uint32_t s0, s1, x0, x1, s2 = 0, s3 = 0, x2 = 0, x3 = 0;
-                    lds64(smb + (e0 - a0), s0, s1);
-                    lds64(wreg + (e0 - F), x0, x1);
-                    if (two) {
-                        lds64(smb + (e1 - a0), s2, s3);
-                        lds64(wreg + (e1 - F), x2, x3);
+                } else {
+                    // other value formats (NEXT-4): residual bits of output e at bit kRb * e - 8 * a0
+                    if (edge)
+                        out[es] = (OutT)compose_vf(kF, ld8(wreg + (es - F)), res_smem<kRb>(smb, es * kRb - 8u * a0));
+                    for (uint32_t u = ua + lane; u < ub; u += 32) {
+                        const uint32_t e0 = u * kU;
+                        const uint32_t o = smb + (e0 / 8u * kRb - a0), xa = wreg + (e0 - F);
+                        uint4 v;
+                        if constexpr (kVF == DF11_VF_FP16) {
+                            uint32_t x0, x1;
+                            lds64(xa, x0, x1);
+                            v = unit_fp16(x0, x1, o);
+                        } else {
+                            uint32_t x0, x1, x2, x3;
+                            lds128(xa, x0, x1, x2, x3);
+                            if constexpr (kVF == DF11_VF_FP8_E4M3) {
+                                uint32_t r0, r1;
+                                lds64(o, r0, r1);                               // 16 nibbles
+                                v.x = quad_e4m3<0x1100u>(r0, x0);
+                                v.y = quad_e4m3<0x3322u>(r0, x1);
+                                v.z = quad_e4m3<0x1100u>(r1, x2);
+                                v.w = quad_e4m3<0x3322u>(r1, x3);
+                            } else {                                            // E5M2: 48 bits at o (even)
+                                const uint32_t base = o & ~3u, sh = (o & 3u) * 8u;
+                                const uint32_t B0 = bswap32(lds32(base)), B1 = bswap32(lds32(base + 4));
+                                const uint32_t H0 = __funnelshift_l(B1, B0, sh), H1 = B1 << sh;
+                                v.x = quad_e5m2(H0 >> 20, x0);
+                                v.y = quad_e5m2((H0 >> 8) & 0xFFFu, x1);
+                                v.z = quad_e5m2(__funnelshift_l(H1, H0, 24) >> 20, x2);
+                                v.w = quad_e5m2((H1 >> 16) & 0xFFFu, x3);
+                            }
+                        }
+                        *reinterpret_cast<uint4 *>(out + e0) = v;
                     }
-                    uint4 o0, o1;
-                    compose4r(x0, s0, o0.x, o0.y);
-                    compose4r(x1, s1, o0.z, o0.w);
-                    *reinterpret_cast<uint4 *>(out + e0) = o0;
-                    if (two) {
-                        compose4r(x2, s2, o1.x, o1.y);
-                        compose4r(x3, s3, o1.z, o1.w);
-                        *reinterpret_cast<uint4 *>(out + e1) = o1;
-                    }
                 }
-#endif
 #ifndef SP12_SM_BARRIER
                 // the last warp done with this tile's buffer stages the group's next tile into it.
                 // Ordering: each warp's reads of the buffer are complete before its
@@ -612,20 +687,26 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 }
 #endif
             } else {
-                if (edge) out[es] = compose_r(ld8(wreg + (es - F)), __ldg(ts.packed_sign_mantissa + es));
-                for (uint32_t u = ua + lane; u < ub; u += 32) {
-                    const uint32_t e0 = u << 3;
-                    const uint2 sm = __ldg(psm2 + u);
-                    uint32_t x0, x1;
-                    lds64(wreg + (e0 - F), x0, x1);
-                    uint4 o0;
-                    compose4r(x0, sm.x, o0.x, o0.y);
-                    compose4r(x1, sm.y, o0.z, o0.w);
-                    *reinterpret_cast<uint4 *>(out + e0) = o0;
-                }
-                if (!vec_out)                                                  // unaligned output: scalar
+                if constexpr (kVF == DF11_VF_BF16) {
+                    if (edge) out[es] = compose_r(ld8(wreg + (es - F)), __ldg(ts.packed_sign_mantissa + es));
+                    for (uint32_t u = ua + lane; u < ub; u += 32) {
+                        const uint32_t e0 = u << 3;
+                        const uint2 sm = __ldg(psm2 + u);
+                        uint32_t x0, x1;
+                        lds64(wreg + (e0 - F), x0, x1);
+                        uint4 o0;
+                        compose4r(x0, sm.x, o0.x, o0.y);
+                        compose4r(x1, sm.y, o0.z, o0.w);
+                        *reinterpret_cast<uint4 *>(out + e0) = o0;
+                    }
+                    if (!vec_out)                                              // unaligned output: scalar
+                        for (uint32_t e = ra + lane; e < rb; e += 32)
+                            out[e] = compose_r(ld8(wreg + (e - F)), __ldg(ts.packed_sign_mantissa + e));
+                } else {
+                    // residuals of a tile above the SMEM cap (or an unaligned output): per element
                     for (uint32_t e = ra + lane; e < rb; e += 32)
-                        out[e] = compose_r(ld8(wreg + (e - F)), __ldg(ts.packed_sign_mantissa + e));
+                        out[e] = (OutT)compose_vf(kF, ld8(wreg + (e - F)), load_residual(kF, ts.packed_sign_mantissa, e));
+                }
                 if (t == 0 && has_next) stage_sm(nlo, nhi);
                 __syncwarp();                  // the region's reads are done before the next tile's slots
             }
@@ -638,7 +719,20 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 #undef K_S24
 }
 
-int g_sp12_attr_set[64];
+uint32_t g_sp12_attr_set[64];
+
+template <uint32_t kNB, uint32_t kVF>
+cudaError_t launch_one(const Batch &bt, int device, uint32_t grid, cudaStream_t stream) {
+    constexpr uint32_t bit = 1u << ((kNB == 16 ? 4 : 0) + kVF);
+    if (device >= 0 && device < 64 && !(g_sp12_attr_set[device] & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(sp12_kernel<kNB, kVF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)Lay12<kVF>::kSmem);
+        if (e != cudaSuccess) return e;
+        g_sp12_attr_set[device] |= bit;
+    }
+    sp12_kernel<kNB, kVF><<<grid, kCta12, Lay12<kVF>::kSmem, stream>>>(bt);
+    return cudaGetLastError();
+}
 
 }  // namespace
 
@@ -647,36 +741,39 @@ uint32_t fast_grid(uint32_t total_tiles, int num_sms) {
 }
 
 // Tensors the product kernel decodes: the paper's format parameters (T = 256, n = 8) or
-// T = 128, n = 16 (NEXT-4), and the alignment its bulk copies need (stream, gaps and
-// PackedSignMantissa 16-byte aligned, BF16 output 2-byte aligned); df11_decompress_block_ex sends
-// every other tensor to the Algorithm 1 kernel.
+// T = 128, n = 16 (NEXT-4), any value format and LUT width b, and the alignment its bulk copies need
+// (stream, gaps and PackedSignMantissa 16-byte aligned, output aligned to its word size);
+// df11_decompress_block_ex sends every other tensor to the Algorithm 1 kernel.
 bool fast_supports(const df11_device_tensor &t) {
     return ((t.T == kT && t.n == kN) || (t.T == 128 && t.n == 16)) &&
            (reinterpret_cast<uintptr_t>(t.encoded_exponent) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.gaps) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.packed_sign_mantissa) & 15) == 0 &&
-           (reinterpret_cast<uintptr_t>(t.out) & 1) == 0;
+           (reinterpret_cast<uintptr_t>(t.out) & (vf_of(t.value_format).word_bytes - 1)) == 0;
 }
 
-// Launch for a batch whose tensors all have n = 8 (T = 256) or all n = 16 (T = 128).
+// Launch for a batch whose tensors share n (8 with T = 256, or 16 with T = 128) and the value format.
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches) {
     if (bt.total_tiles == 0) return cudaSuccess;
     int num_sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
     const bool n16 = bt.t[0].n == 16;
-    if (device >= 0 && device < 64 && !(g_sp12_attr_set[device] & (n16 ? 2 : 1))) {
-        e = n16 ? cudaFuncSetAttribute(sp12_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem12)
-                : cudaFuncSetAttribute(sp12_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem12);
-        if (e != cudaSuccess) return e;
-        g_sp12_attr_set[device] |= n16 ? 2 : 1;
-    }
+    const uint32_t vf = bt.t[0].value_format;
     const uint32_t grid = bt.grid ? bt.grid
                                   : min((uint32_t)num_sms, (bt.total_tiles + kGroups12 - 1) / kGroups12);
-    if (n16) sp12_kernel<16><<<grid, kCta12, kSmem12, stream>>>(bt);
-    else sp12_kernel<8><<<grid, kCta12, kSmem12, stream>>>(bt);
-    if (launches) (*launches)++;
-    return cudaGetLastError();
+    switch (vf + (n16 ? 4u : 0u)) {
+        case 0: e = launch_one<8, DF11_VF_BF16>(bt, device, grid, stream); break;
+        case 1: e = launch_one<8, DF11_VF_FP16>(bt, device, grid, stream); break;
+        case 2: e = launch_one<8, DF11_VF_FP8_E4M3>(bt, device, grid, stream); break;
+        case 3: e = launch_one<8, DF11_VF_FP8_E5M2>(bt, device, grid, stream); break;
+        case 4: e = launch_one<16, DF11_VF_BF16>(bt, device, grid, stream); break;
+        case 5: e = launch_one<16, DF11_VF_FP16>(bt, device, grid, stream); break;
+        case 6: e = launch_one<16, DF11_VF_FP8_E4M3>(bt, device, grid, stream); break;
+        default: e = launch_one<16, DF11_VF_FP8_E5M2>(bt, device, grid, stream); break;
+    }
+    if (e == cudaSuccess && launches) (*launches)++;
+    return e;
 }
 
 }  // namespace df11

@@ -2,9 +2,11 @@
 //
 // Produces the bit-exact format of DESIGN.md §2 from the paper's description:
 //   split -> exponent histogram -> Huffman code lengths with the 32-bit
-//   cap (R3 tie rule, R4 package-merge) -> canonical codes -> hierarchical 256-entry LUTs
-//   (App. I.2; R6 breadth-first children, R8 wide fallback) -> MSB-first bit packing of
-//   EncodedExponent (R1) -> Gaps (R12/R13) and BlockOutputPos (R14).
+//   cap (R3 tie rule, R4 package-merge) -> canonical codes -> hierarchical 2^b-entry LUTs
+//   (App. I.2; b = 8 by default, b = L for the monolithic table of App. I.1; R6
+//   breadth-first children, R8 wide fallback, R28) -> MSB-first bit packing of EncodedExponent (P:97,
+//   R1) -> Gaps (R12/R13) and BlockOutputPos (R14).  Value formats FP16 / FP8 (NEXT-4,
+//   R25-R27) split the same way: exponent field -> symbol, sign + mantissa -> R-bit residual stream.
 //
 // Built for speed, not for reading against the paper (that is oracle/'s job): every O(N) pass is
 // split over host threads; the bit packer gives every thread a bit range computed by a prefix sum of
@@ -52,19 +54,39 @@ struct Pool {
 
 inline uint64_t roundup(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 
+// ------------------------------------------------------------------------------------ value formats
+// Word of `word_bytes` bytes: sign | exponent (exp_bits) | mantissa (man_bits); residual R = 1 + M.
+struct VFmt {
+    uint32_t word_bytes, exp_bits, man_bits;
+    uint32_t R() const { return 1 + man_bits; }
+    uint32_t emask() const { return (1u << exp_bits) - 1u; }
+};
+constexpr VFmt kVF[4] = {{2, 8, 7}, {2, 5, 10}, {1, 4, 3}, {1, 5, 2}};   // BF16, FP16, FP8 E4M3, E5M2
+
+inline uint32_t word_at(const void *w, const VFmt &f, uint64_t i) {
+    return f.word_bytes == 2 ? (uint32_t)static_cast<const uint16_t *>(w)[i] : (uint32_t)static_cast<const uint8_t *>(w)[i];
+}
+inline uint32_t symbol_of(uint32_t word, const VFmt &f) { return (word >> f.man_bits) & f.emask(); }
+inline uint32_t residual_of(uint32_t word, const VFmt &f) {
+    return ((word >> (f.exp_bits + f.man_bits)) << f.man_bits) | (word & ((1u << f.man_bits) - 1u));
+}
+inline uint64_t residual_bytes(uint64_t n, const VFmt &f) { return roundup(f.R() * roundup(n, 16) / 8, 16) + 16; }
+
 // ------------------------------------------------------------------------------------ histogram
-void histogram(const uint16_t *w, uint64_t n, const Pool &pool, uint64_t hist[256]) {
+template <typename W>
+void histogram_t(const W *w, uint64_t n, const VFmt &f, const Pool &pool, uint64_t hist[256]) {
     std::vector<uint64_t> part((size_t)pool.nthreads * 256, 0);
+    const uint32_t sh = f.man_bits, m = f.emask();
     pool.run(n, [&](unsigned t, uint64_t b, uint64_t e) {
         uint64_t local[4][256] = {};
         uint64_t i = b;
         for (; i + 4 <= e; i += 4) {                      // 4 sub-histograms hide store-to-load stalls
-            local[0][(w[i] >> 7) & 0xFF]++;
-            local[1][(w[i + 1] >> 7) & 0xFF]++;
-            local[2][(w[i + 2] >> 7) & 0xFF]++;
-            local[3][(w[i + 3] >> 7) & 0xFF]++;
+            local[0][(w[i] >> sh) & m]++;
+            local[1][(w[i + 1] >> sh) & m]++;
+            local[2][(w[i + 2] >> sh) & m]++;
+            local[3][(w[i + 3] >> sh) & m]++;
         }
-        for (; i < e; i++) local[0][(w[i] >> 7) & 0xFF]++;
+        for (; i < e; i++) local[0][(w[i] >> sh) & m]++;
         for (int s = 0; s < 256; s++) part[(size_t)t * 256 + s] = local[0][s] + local[1][s] + local[2][s] + local[3][s];
     });
     for (int s = 0; s < 256; s++) {
@@ -72,6 +94,10 @@ void histogram(const uint16_t *w, uint64_t n, const Pool &pool, uint64_t hist[25
         for (unsigned t = 0; t < pool.nthreads; t++) acc += part[(size_t)t * 256 + s];
         hist[s] = acc;
     }
+}
+void histogram(const void *w, uint64_t n, const VFmt &f, const Pool &pool, uint64_t hist[256]) {
+    if (f.word_bytes == 2) histogram_t(static_cast<const uint16_t *>(w), n, f, pool, hist);
+    else histogram_t(static_cast<const uint8_t *>(w), n, f, pool, hist);
 }
 
 // ------------------------------------------------------------------------------------ code lengths
@@ -176,14 +202,15 @@ void canonical_codes(const uint8_t len[256], uint32_t code[256]) {
 }
 
 // ------------------------------------------------------------------------------------ LUTs
-// Explicit code tree, then every table enumerates the 256 8-bit paths from its subtree root.
+// Explicit code tree, then every table enumerates the 2^b b-bit paths from its subtree root.
 struct Tree {
     std::vector<int> child0, child1, symbol;   // symbol >= 0 at leaves
     int add() { child0.push_back(-1); child1.push_back(-1); symbol.push_back(-1); return (int)symbol.size() - 1; }
 };
 
-df11_status build_luts(const uint8_t len[256], const uint32_t code[256], int lut_mode,
+df11_status build_luts(const uint8_t len[256], const uint32_t code[256], int lut_mode, uint32_t b,
                        std::vector<uint8_t> &out, uint32_t &k, uint32_t &entry_bytes) {
+    const uint32_t size = 1u << b;
     out.clear();
     k = 0;
     entry_bytes = 1;
@@ -211,17 +238,17 @@ df11_status build_luts(const uint8_t len[256], const uint32_t code[256], int lut
     std::vector<int> table_root{root};
     std::vector<int> entries;
     for (size_t t = 0; t < table_root.size(); t++) {
-        for (int idx = 0; idx < 256; idx++) {
+        for (uint32_t idx = 0; idx < size; idx++) {
             int v = table_root[t];
             int val = INT32_MIN;
-            for (int bit = 7; bit >= 0 && val == INT32_MIN; bit--) {
-                int b = (idx >> bit) & 1;
-                int nv = b ? tree.child1[v] : tree.child0[v];
+            for (int bit = (int)b - 1; bit >= 0 && val == INT32_MIN; bit--) {
+                int bb = (idx >> bit) & 1;
+                int nv = bb ? tree.child1[v] : tree.child0[v];
                 if (nv < 0) { val = only; break; }           // unreachable: only when |S| = 1 (R7)
                 v = nv;
                 if (tree.symbol[v] >= 0) val = tree.symbol[v];
             }
-            if (val == INT32_MIN) {                          // still inside the tree after 8 bits
+            if (val == INT32_MIN) {                          // still inside the tree after b bits
                 int j = -1;
                 for (size_t q = t + 1; q < table_root.size(); q++) if (table_root[q] == v) { j = (int)q; break; }
                 if (j < 0) { table_root.push_back(v); j = (int)table_root.size() - 1; }
@@ -243,7 +270,7 @@ df11_status build_luts(const uint8_t len[256], const uint32_t code[256], int lut
         wide = !narrow_ok;
     }
     entry_bytes = wide ? 2 : 1;
-    out.resize((size_t)k * 256 * entry_bytes);
+    out.resize((size_t)k * size * entry_bytes);
     for (size_t i = 0; i < entries.size(); i++) {
         int e = entries[i];
         uint32_t v = e >= 0 ? (uint32_t)e : (wide ? 256u + (uint32_t)(-e) : 256u - (uint32_t)(-e));
@@ -259,10 +286,11 @@ struct Codebook {
     uint32_t code[256];
     uint32_t max_len;
     std::vector<uint8_t> luts;
-    uint32_t k, entry_bytes;
+    uint32_t k, entry_bytes, lut_bits;
 };
 
-df11_status make_codebook(const uint64_t hist[256], int lut_mode, Codebook &cb) {
+// lut_bits: 1..16, or DF11_LUT_BITS_MONOLITHIC (b = L, one table; L <= 16)
+df11_status make_codebook(const uint64_t hist[256], int lut_mode, uint32_t lut_bits, Codebook &cb) {
     std::vector<int> ranked = ranked_symbols(hist);
     huffman_lengths(hist, ranked, cb.len);
     cb.max_len = 0;
@@ -273,14 +301,24 @@ df11_status make_codebook(const uint64_t hist[256], int lut_mode, Codebook &cb) 
         for (int s = 0; s < 256; s++) cb.max_len = std::max<uint32_t>(cb.max_len, cb.len[s]);
     }
     canonical_codes(cb.len, cb.code);
-    return build_luts(cb.len, cb.code, lut_mode, cb.luts, cb.k, cb.entry_bytes);
+    if (lut_bits == DF11_LUT_BITS_MONOLITHIC) {
+        if (cb.max_len > 16) return df11_fail(DF11_E_INVALID_ARGUMENT, "monolithic LUT needs max code length <= 16");
+        lut_bits = std::max<uint32_t>(cb.max_len, 1);
+    }
+    cb.lut_bits = lut_bits;
+    df11_status st = build_luts(cb.len, cb.code, lut_mode, lut_bits, cb.luts, cb.k, cb.entry_bytes);
+    if (st == DF11_E_RESERVED_EXPONENT) return df11_fail(st, "exponent >= 240 with NARROW LUTs");
+    if (st == DF11_E_LUT_OVERFLOW) return df11_fail(st, "more than 16 child LUTs with NARROW LUTs");
+    return st;
 }
 
 // ------------------------------------------------------------------------------------ packing
 inline void or_byte(uint8_t *p, uint8_t v) { __atomic_fetch_or(p, v, __ATOMIC_RELAXED); }
 
-df11_status encode_with_codebook(const uint16_t *w, uint64_t n, uint32_t T, uint32_t nb, const Codebook &cb,
-                                 const Pool &pool, df11_host_tensor *out) {
+template <typename W>
+df11_status encode_with_codebook(const W *w, uint64_t n, const VFmt &f, uint32_t vf, uint32_t T, uint32_t nb,
+                                 const Codebook &cb, const Pool &pool, df11_host_tensor *out) {
+    const uint32_t sh = f.man_bits, em = f.emask();
     df11_host_tensor r;
     std::memset(&r, 0, sizeof(r));
     r.num_elements = n;
@@ -290,13 +328,15 @@ df11_status encode_with_codebook(const uint16_t *w, uint64_t n, uint32_t T, uint
     r.k = cb.k;
     r.lut_entry_bytes = cb.entry_bytes;
     r.max_code_len = cb.max_len;
+    r.value_format = vf;
+    r.lut_bits = cb.lut_bits;
 
     // per-thread bit totals -> exclusive prefix (bit offset of each segment)
     const unsigned P = pool.nthreads;
     std::vector<uint64_t> seg_bits(P + 1, 0);
     pool.run(n, [&](unsigned t, uint64_t b, uint64_t e) {
         uint64_t acc = 0;
-        for (uint64_t i = b; i < e; i++) acc += cb.len[(w[i] >> 7) & 0xFF];
+        for (uint64_t i = b; i < e; i++) acc += cb.len[(w[i] >> sh) & em];
         seg_bits[t + 1] = acc;
     });
     for (unsigned t = 0; t < P; t++) seg_bits[t + 1] += seg_bits[t];
@@ -310,7 +350,7 @@ df11_status encode_with_codebook(const uint16_t *w, uint64_t n, uint32_t T, uint
 
     r.luts_bytes = cb.luts.size();
     r.encoded_exponent_bytes = (uint64_t)B * T * nb + 16;
-    r.packed_sign_mantissa_bytes = roundup(n, 16) + 16;
+    r.packed_sign_mantissa_bytes = residual_bytes(n, f);
     r.gaps_bytes = roundup((5ull * B * T + 7) / 8, 16) + 16;
     r.luts = (uint8_t *)std::calloc(std::max<uint64_t>(r.luts_bytes, 1), 1);
     r.encoded_exponent = (uint8_t *)std::calloc(r.encoded_exponent_bytes, 1);
@@ -337,13 +377,13 @@ df11_status encode_with_codebook(const uint16_t *w, uint64_t n, uint32_t T, uint
         int nacc = (int)(bit & 7);             // leading bits belong to the previous segment (zeros here)
         bool first_byte = true;
         // gaps/BOP: chunks whose first codeword start lies in this segment
-        uint64_t prev_start = (b == 0) ? 0 : bit - cb.len[(w[b - 1] >> 7) & 0xFF];
+        uint64_t prev_start = (b == 0) ? 0 : bit - cb.len[(w[b - 1] >> sh) & em];
         uint64_t next_chunk = (b == 0) ? 0 : prev_start / chunk_bits + 1;
         uint64_t next_block = (b == 0) ? 0 : prev_start / block_bits + 1;
         for (uint64_t i = b; i < e; i++) {
-            const uint16_t word = w[i];
-            const uint8_t ex = (uint8_t)((word >> 7) & 0xFF);
-            psm[i] = (uint8_t)(((word >> 8) & 0x80) | (word & 0x7F));
+            const uint32_t word = w[i];
+            const uint32_t ex = (word >> sh) & em;
+            if (f.R() == 8) psm[i] = (uint8_t)(((word >> 8) & 0x80) | (word & 0x7F));   // BF16
             // first codeword start at or after chunk / block boundaries
             while (next_chunk < nthreads_fmt && next_chunk * chunk_bits <= bit) {
                 uint64_t gap = bit - next_chunk * chunk_bits;
@@ -369,10 +409,24 @@ df11_status encode_with_codebook(const uint16_t *w, uint64_t n, uint32_t T, uint
     // chunks / blocks past the last codeword start
     {
         // last start = total_bits - len(last)
-        uint64_t last_start = n ? total_bits - cb.len[(w[n - 1] >> 7) & 0xFF] : 0;
+        uint64_t last_start = n ? total_bits - cb.len[(w[n - 1] >> sh) & em] : 0;
         (void)last_start;
         for (uint32_t b = 0; b < B; b++) if (b > 0 && bop[b] == 0 && (uint64_t)b * block_bits > last_start) bop[b] = (uint32_t)n;
         bop[B] = (uint32_t)n;
+    }
+    // residual stream of the other value formats: 8 elements = R bytes, MSB-first (R25)
+    if (f.R() != 8) {
+        const uint32_t R = f.R();
+        pool.run((n + 7) / 8, [&](unsigned, uint64_t qb, uint64_t qe) {
+            for (uint64_t q = qb; q < qe; q++) {
+                unsigned __int128 acc = 0;                 // 8 * R <= 88 bits
+                for (uint64_t j = 0; j < 8; j++) {
+                    const uint64_t i = q * 8 + j;
+                    acc = (acc << R) | (i < n ? residual_of(w[i], f) : 0u);
+                }
+                for (uint32_t j = 0; j < R; j++) psm[q * R + j] = (uint8_t)(acc >> (8 * (R - 1 - j)));
+            }
+        });
     }
     // pack gaps: 8 fields = 40 bits = 5 bytes, MSB-first
     Pool gpool(pool.nthreads, nthreads_fmt);
@@ -399,7 +453,13 @@ df11_status check_opts(const df11_encode_opts *opts, df11_encode_opts &o) {
     o.bytes_per_thread = 8;
     o.lut_mode = DF11_LUT_AUTO;
     o.num_threads = 0;
+    o.value_format = DF11_VF_BF16;
+    o.lut_bits = 8;
     if (opts) o = *opts;
+    if (o.lut_bits == 0) o.lut_bits = 8;
+    if (o.value_format > DF11_VF_FP8_E5M2) return df11_fail(DF11_E_INVALID_ARGUMENT, "bad value_format");
+    if (o.lut_bits > 16 && o.lut_bits != DF11_LUT_BITS_MONOLITHIC)
+        return df11_fail(DF11_E_INVALID_ARGUMENT, "lut_bits must be in [1, 16] or DF11_LUT_BITS_MONOLITHIC");
     if (o.threads_per_block < 32 || o.threads_per_block > 1024 || o.threads_per_block % 32)
         return df11_fail(DF11_E_INVALID_ARGUMENT, "threads_per_block must be a multiple of 32 in [32, 1024]");
     if (o.bytes_per_thread < 4 || o.bytes_per_thread > 32)
@@ -410,11 +470,23 @@ df11_status check_opts(const df11_encode_opts *opts, df11_encode_opts &o) {
 
 }  // namespace
 
-extern "C" df11_status df11_encode(const uint16_t *bf16, uint64_t n_elems, const df11_encode_opts *opts,
+namespace {
+df11_status encode_values(const void *w, uint64_t n, const df11_encode_opts &o, const Codebook &cb, const Pool &pool,
+                          df11_host_tensor *out) {
+    const VFmt &f = kVF[o.value_format];
+    if (f.word_bytes == 2)
+        return encode_with_codebook(static_cast<const uint16_t *>(w), n, f, o.value_format, o.threads_per_block,
+                                    o.bytes_per_thread, cb, pool, out);
+    return encode_with_codebook(static_cast<const uint8_t *>(w), n, f, o.value_format, o.threads_per_block,
+                                o.bytes_per_thread, cb, pool, out);
+}
+}  // namespace
+
+extern "C" df11_status df11_encode(const void *values, uint64_t n_elems, const df11_encode_opts *opts,
                                    df11_host_tensor *out) {
     if (!out) return df11_fail(DF11_E_INVALID_ARGUMENT, "out is NULL");
     std::memset(out, 0, sizeof(*out));
-    if (!bf16 && n_elems) return df11_fail(DF11_E_INVALID_ARGUMENT, "bf16 is NULL");
+    if (!values && n_elems) return df11_fail(DF11_E_INVALID_ARGUMENT, "values is NULL");
     df11_encode_opts o;
     df11_status st = check_opts(opts, o);
     if (st != DF11_OK) return st;
@@ -422,18 +494,17 @@ extern "C" df11_status df11_encode(const uint16_t *bf16, uint64_t n_elems, const
     try {
         Pool pool(o.num_threads, n_elems);
         uint64_t hist[256];
-        histogram(bf16, n_elems, pool, hist);
+        histogram(values, n_elems, kVF[o.value_format], pool, hist);
         Codebook cb;
-        st = make_codebook(hist, (int)o.lut_mode, cb);
-        if (st != DF11_OK) return df11_fail(st, st == DF11_E_RESERVED_EXPONENT ? "exponent >= 240 with NARROW LUTs"
-                                                                          : "more than 16 child LUTs with NARROW LUTs");
-        return encode_with_codebook(bf16, n_elems, o.threads_per_block, o.bytes_per_thread, cb, pool, out);
+        st = make_codebook(hist, (int)o.lut_mode, o.lut_bits, cb);
+        if (st != DF11_OK) return st;
+        return encode_values(values, n_elems, o, cb, pool, out);
     } catch (const std::bad_alloc &) {
         return df11_fail(DF11_E_ALLOC, "host allocation failed");
     }
 }
 
-extern "C" df11_status df11_encode_group(const uint16_t *const *tensors, const uint64_t *n_elems, uint32_t count,
+extern "C" df11_status df11_encode_group(const void *const *tensors, const uint64_t *n_elems, uint32_t count,
                                          const df11_encode_opts *opts, int shared_codebook, df11_host_tensor *outs) {
     if (!outs || (count && (!tensors || !n_elems))) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL argument");
     for (uint32_t i = 0; i < count; i++) std::memset(&outs[i], 0, sizeof(outs[i]));
@@ -458,16 +529,16 @@ extern "C" df11_status df11_encode_group(const uint16_t *const *tensors, const u
             if (n_elems[i] >= (1ull << 32)) return df11_fail(DF11_E_TOO_LARGE, "N >= 2^32");
             Pool pool(o.num_threads, n_elems[i]);
             uint64_t h[256];
-            histogram(tensors[i], n_elems[i], pool, h);
+            histogram(tensors[i], n_elems[i], kVF[o.value_format], pool, h);
             for (int s = 0; s < 256; s++) hist[s] += h[s];
             total += n_elems[i];
         }
         Codebook cb;
-        st = make_codebook(hist, (int)o.lut_mode, cb);
-        if (st != DF11_OK) return df11_fail(st, "shared codebook not representable with NARROW LUTs");
+        st = make_codebook(hist, (int)o.lut_mode, o.lut_bits, cb);
+        if (st != DF11_OK) return st;
         for (uint32_t i = 0; i < count; i++) {
             Pool pool(o.num_threads, n_elems[i]);
-            st = encode_with_codebook(tensors[i], n_elems[i], o.threads_per_block, o.bytes_per_thread, cb, pool, &outs[i]);
+            st = encode_values(tensors[i], n_elems[i], o, cb, pool, &outs[i]);
             if (st != DF11_OK) {
                 for (uint32_t j = 0; j < i; j++) df11_host_tensor_free(&outs[j]);
                 return df11_fail(st, "group encode failed");
@@ -502,11 +573,12 @@ extern "C" df11_status df11_encode_plan_create(const uint64_t *codebook_hist, co
     df11_encode_opts o;
     df11_status st = check_opts(opts, o);
     if (st != DF11_OK) return st;
+    if (o.value_format != DF11_VF_BF16)
+        return df11_fail(DF11_E_UNSUPPORTED, "the device encoder codes BF16 only (use df11_encode)");
     try {
         Codebook cb;
-        st = make_codebook(codebook_hist, (int)o.lut_mode, cb);
-        if (st != DF11_OK) return df11_fail(st, st == DF11_E_RESERVED_EXPONENT ? "exponent >= 240 with NARROW LUTs"
-                                                                          : "more than 16 child LUTs with NARROW LUTs");
+        st = make_codebook(codebook_hist, (int)o.lut_mode, o.lut_bits, cb);
+        if (st != DF11_OK) return st;
         uint64_t n = 0, bits = 0;
         for (int s = 0; s < 256; s++) {
             if (tensor_hist[s] && !cb.len[s])
@@ -529,6 +601,7 @@ extern "C" df11_status df11_encode_plan_create(const uint64_t *codebook_hist, co
         plan->k = cb.k;
         plan->lut_entry_bytes = cb.entry_bytes;
         plan->max_code_len = cb.max_len;
+        plan->lut_bits = cb.lut_bits;
         std::memcpy(plan->code_lengths, cb.len, 256);
         std::memcpy(plan->codes, cb.code, sizeof(plan->codes));
         plan->encoded_exponent_bytes = B * o.threads_per_block * o.bytes_per_thread + 16;

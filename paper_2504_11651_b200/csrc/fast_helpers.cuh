@@ -127,20 +127,27 @@ __device__ __forceinline__ void issue_tile16(const df11_device_tensor &ts, uint3
     tma_g2s(stage + kChunkBytes, ts.gaps + (size_t)b * (128 * 5 / 8), 128 * 5 / 8 + 16, bar);
 }
 
-// Paper's hierarchical LUT walk over the format tables in global memory; returns the
-// exponent and its code length.  Bounded: <= 4 levels, child < k, zero length -> 32.
+// Level i (0-based) of a b-bit LUT walk reads window bits [b*i, b*(i+1)), zero-extended past bit 32
+// (R28: a symbol's entries cover every value of the bits after its code); b = 8 reads byte i.
+__device__ __forceinline__ uint32_t lut_level_idx(uint32_t w, uint32_t lb, uint32_t i) {
+    return shr_c(shl_c(w, lb * i), 32u - lb);          // PTX shifts by >= 32 give 0
+}
+
+// Paper's hierarchical LUT walk over the format's b-bit tables in global memory; returns
+// the exponent and its code length.  Bounded: <= ceil(32/b) levels, child < k, zero length -> 32.
 __device__ __noinline__ uint32_t lut_walk_global(uint32_t w, const df11_device_tensor &ts, uint32_t &len) {
     const uint8_t *__restrict__ luts = ts.luts;
     const uint32_t eb = ts.lut_entry_bytes, thr = eb == 1 ? 240u : 256u;
+    const uint32_t lb = lut_bits_of(ts), levels = (32u + lb - 1u) / lb;
     uint32_t table = 0, e = 0;
 #pragma unroll 1
-    for (int i = 0; i < 4; i++) {
-        const uint32_t off = table * 256u + ((w >> (24 - 8 * i)) & 0xFFu);
+    for (uint32_t i = 0; i < levels; i++) {
+        const uint32_t off = (table << lb) + lut_level_idx(w, lb, i);
         e = eb == 1 ? (uint32_t)__ldg(luts + off)
                     : ((uint32_t)__ldg(luts + 2 * off) | ((uint32_t)__ldg(luts + 2 * off + 1) << 8));
         if (e < thr) break;
         table = eb == 1 ? 256u - e : e - 256u;
-        if (table >= ts.k || i == 3) { e = 0; break; }
+        if (table >= ts.k || i == levels - 1) { e = 0; break; }
     }
     e &= 0xFFu;
     len = __ldg(ts.code_lengths + e);
@@ -150,17 +157,17 @@ __device__ __noinline__ uint32_t lut_walk_global(uint32_t w, const df11_device_t
 
 // The same walk over the SMEM copy of the format tables (narrow or wide).
 __device__ __forceinline__ uint32_t lut_walk_smem(uint32_t w, uint32_t lut, uint32_t clen, uint32_t eb,
-                                                  uint32_t k, uint32_t &len) {
-    const uint32_t thr = eb == 1 ? 240u : 256u;
+                                                  uint32_t k, uint32_t lb, uint32_t &len) {
+    const uint32_t thr = eb == 1 ? 240u : 256u, levels = (32u + lb - 1u) / lb;
     uint32_t e = 0, table = 0;
 #pragma unroll 1
-    for (int i = 0, sh = 24; i < 4; i++, sh -= 8) {
-        const uint32_t idx = table * 256u + ((w >> sh) & 0xFFu);
+    for (uint32_t i = 0; i < levels; i++) {
+        const uint32_t idx = (table << lb) + lut_level_idx(w, lb, i);
         if (eb == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(e) : "r"(lut + idx));
         else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(lut + 2 * idx));
         if (e < thr) break;
         table = eb == 1 ? 256u - e : e - 256u;
-        if (table >= k || i == 3) { e = 0; break; }
+        if (table >= k || i == levels - 1) { e = 0; break; }
     }
     e &= 0xFFu;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(len) : "r"(clen + e));

@@ -29,6 +29,18 @@ __device__ __forceinline__ uint32_t t12_addr(uint32_t a, uint32_t base, uint32_t
 }
 __device__ __forceinline__ uint32_t rot8(uint32_t e) { return ((e >> 1) | (e << 7)) & 0xFFu; }
 __device__ __forceinline__ uint32_t unrot8(uint32_t r) { return ((r << 1) | (r >> 7)) & 0xFFu; }
+// Symbol as stored in T12 / the slots: BF16 exponents rotated (the merge's bit-select trick), the
+// other value formats' exponents as they are.
+template <uint32_t kVF>
+__device__ __forceinline__ uint32_t to_stored(uint32_t e) {
+    if constexpr (kVF == DF11_VF_BF16) return rot8(e);
+    else return e & 0xFFu;
+}
+template <uint32_t kVF>
+__device__ __forceinline__ uint32_t from_stored(uint32_t r) {
+    if constexpr (kVF == DF11_VF_BF16) return unrot8(r);
+    else return r & 0xFFu;
+}
 
 __device__ __forceinline__ void st8(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -186,14 +198,17 @@ __device__ __forceinline__ uint16_t compose_r(uint32_t r, uint32_t psm) {
 // 8 * count << 24.  The format LUTs are staged at lut (if they fit kLutSmem) and
 // CodeLengths at len / rlen (indexed by exponent / by rotated exponent; absent codes: 32 in rlen).
 // fc: 8 KB of scratch for the first-code table.  Returns whether the all-ones row is an escape (some
-// code is longer than 12 bits); `safe` = some code is 1 bit long.
-template <uint32_t kThreads>
+// code is longer than 12 bits); `safe` = some code is 1 bit long.  Symbols are stored as
+// to_stored<kVF>; b-bit tables (lut_bits != 8) are walked row by row.
+template <uint32_t kThreads, uint32_t kVF>
 __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t *sb, uint32_t sbase,
                                           uint32_t off_t, uint32_t off_lut, uint32_t off_len, uint32_t off_rlen,
                                           uint32_t off_fc, uint32_t tid, bool &safe, bool &lut_in_smem) {
+    // the paper's byte tables (b = 8) are staged in SMEM when they fit; b-bit tables of other widths are
+    // walked in global memory (only the table build and codes longer than 12 bits walk them)
     const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
     const uint32_t lut_bytes = kk * 256u * eb_bytes;
-    lut_in_smem = lut_bytes <= kLutSmem;
+    lut_in_smem = (ts.lut_bits == 0 || ts.lut_bits == 8) && lut_bytes <= kLutSmem;
     if (lut_in_smem) {
         if ((reinterpret_cast<uintptr_t>(ts.luts) & 15) == 0) {       // 16-byte loads (k*256*eb bytes)
             for (uint32_t i = tid; i < lut_bytes / 16; i += kThreads)
@@ -206,7 +221,7 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
     if (tid < 256u) {
         len_t = __ldg(ts.code_lengths + tid);
         sb[off_len + tid] = (uint8_t)len_t;
-        sb[off_rlen + rot8(tid)] = (uint8_t)(len_t ? len_t : 32u);
+        sb[off_rlen + to_stored<kVF>(tid)] = (uint8_t)(len_t ? len_t : 32u);
     }
     // a 1-bit codeword allows 64 codes per chain: such tensors take the count + direct path
     safe = __syncthreads_or(len_t == 1) != 0;
@@ -240,7 +255,7 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
                 ok = ok && e < thr;
             }
             const uint32_t len = ok ? (uint32_t)sb[off_len + (e & 0xFFu)] : 0u;
-            v[u] = (len != 0 && len <= kR) ? (rot8(e & 0xFFu) | (len << 8)) : 0u;
+            v[u] = (len != 0 && len <= kR) ? (to_stored<kVF>(e & 0xFFu) | (len << 8)) : 0u;
             fc[fci(r)] = (uint16_t)v[u];
         }
         __syncthreads();
@@ -262,12 +277,12 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
             if (r == kRows - 1) row_esc_last = c2 == 0;
         }
     } else {
+        // b-bit tables other than b = 8, or tables too large for SMEM: one walk of the format LUTs per
+        // row (in global memory / L1: a cold path, kept simple so that it adds no register pressure)
         for (uint32_t row = tid; row < kRows; row += kThreads) {
             uint32_t len;
-            const uint32_t sym = lut_in_smem ? lut_walk_smem(row << (32 - kR), sbase + off_lut, sbase + off_len,
-                                                             eb_bytes, kk, len)
-                                             : lut_walk_global(row << (32 - kR), ts, len);
-            fc[fci(row)] = len <= kR ? (uint16_t)(rot8(sym) | (len << 8)) : (uint16_t)0;
+            const uint32_t sym = lut_walk_global(row << (32 - kR), ts, len);
+            fc[fci(row)] = len <= kR ? (uint16_t)(to_stored<kVF>(sym) | (len << 8)) : (uint16_t)0;
         }
         __syncthreads();
         for (uint32_t row = tid; row < kRows; row += kThreads) {

@@ -20,6 +20,10 @@ DF11_OK = 0
 STATUS = {0: "DF11_OK", 1: "DF11_E_INVALID_ARGUMENT", 2: "DF11_E_RESERVED_EXPONENT", 3: "DF11_E_LUT_OVERFLOW",
           4: "DF11_E_TOO_LARGE", 5: "DF11_E_CORRUPT", 6: "DF11_E_CUDA", 7: "DF11_E_ALLOC", 8: "DF11_E_UNSUPPORTED"}
 LUT_MODES = {"auto": 0, "narrow": 1, "wide": 2}
+# value formats (df11.h DF11_VF_*; NEXT-4): name -> (code, word bytes, residual bits R)
+VALUE_FORMATS = {"bf16": (0, 2, 8), "fp16": (1, 2, 11), "fp8_e4m3": (2, 1, 4), "fp8_e5m2": (3, 1, 3)}
+VF_NAMES = {v[0]: k for k, v in VALUE_FORMATS.items()}
+LUT_BITS_MONOLITHIC = 255
 KERNELS = {"auto": 0, "alg1": 1, "fast": 2}
 MAX_BATCH = 64
 
@@ -40,13 +44,15 @@ class Df11Error(RuntimeError):
 
 class EncodeOpts(ctypes.Structure):
     _fields_ = [("threads_per_block", ctypes.c_uint32), ("bytes_per_thread", ctypes.c_uint32),
-                ("lut_mode", ctypes.c_uint32), ("num_threads", ctypes.c_uint32)]
+                ("lut_mode", ctypes.c_uint32), ("num_threads", ctypes.c_uint32),
+                ("value_format", ctypes.c_uint32), ("lut_bits", ctypes.c_uint32)]
 
 
 class HostTensorC(ctypes.Structure):
     _fields_ = [("num_elements", ctypes.c_uint64), ("encoded_bits", ctypes.c_uint64),
                 ("T", ctypes.c_uint32), ("n", ctypes.c_uint32), ("B", ctypes.c_uint32), ("k", ctypes.c_uint32),
                 ("lut_entry_bytes", ctypes.c_uint32), ("max_code_len", ctypes.c_uint32),
+                ("value_format", ctypes.c_uint32), ("lut_bits", ctypes.c_uint32),
                 ("code_lengths", ctypes.c_uint8 * 256),
                 ("luts", ctypes.POINTER(ctypes.c_uint8)), ("luts_bytes", ctypes.c_uint64),
                 ("encoded_exponent", ctypes.POINTER(ctypes.c_uint8)), ("encoded_exponent_bytes", ctypes.c_uint64),
@@ -62,13 +68,14 @@ class DeviceTensorC(ctypes.Structure):
                 ("block_output_pos", ctypes.c_void_p), ("out", ctypes.c_void_p),
                 ("num_elements", ctypes.c_uint64), ("T", ctypes.c_uint32), ("n", ctypes.c_uint32),
                 ("B", ctypes.c_uint32), ("k", ctypes.c_uint32), ("lut_entry_bytes", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32)]
+                ("value_format", ctypes.c_uint32), ("lut_bits", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class EncodePlanC(ctypes.Structure):
     _fields_ = [("num_elements", ctypes.c_uint64), ("encoded_bits", ctypes.c_uint64),
                 ("T", ctypes.c_uint32), ("n", ctypes.c_uint32), ("B", ctypes.c_uint32), ("k", ctypes.c_uint32),
                 ("lut_entry_bytes", ctypes.c_uint32), ("max_code_len", ctypes.c_uint32),
+                ("lut_bits", ctypes.c_uint32),
                 ("code_lengths", ctypes.c_uint8 * 256), ("codes", ctypes.c_uint32 * 256),
                 ("luts", ctypes.POINTER(ctypes.c_uint8)), ("luts_bytes", ctypes.c_uint64),
                 ("encoded_exponent_bytes", ctypes.c_uint64), ("packed_sign_mantissa_bytes", ctypes.c_uint64),
@@ -174,6 +181,8 @@ class HostTensor:
     k = property(lambda s: int(s._c.k))
     lut_entry_bytes = property(lambda s: int(s._c.lut_entry_bytes))
     max_code_len = property(lambda s: int(s._c.max_code_len))
+    value_format = property(lambda s: int(s._c.value_format))
+    lut_bits = property(lambda s: int(s._c.lut_bits))
 
     @property
     def code_lengths(self):
@@ -200,10 +209,11 @@ class HostTensor:
         return self._arr("block_output_pos", self.B + 1, np.uint32)
 
     def compressed_bytes(self) -> int:
-        """Bytes the method must read to rebuild the tensor (stream + sign/mantissa + 5-bit gaps +
-        BlockOutputPos + LUTs + CodeLengths), excluding alignment padding."""
-        return ((self.encoded_bits + 7) // 8 + self.num_elements + (5 * self.B * self.T + 7) // 8
-                + 4 * (self.B + 1) + self.k * 256 * self.lut_entry_bytes + 256)
+        """Bytes the method must read to rebuild the tensor (stream + sign/mantissa residuals + 5-bit
+        gaps + BlockOutputPos + LUTs + CodeLengths), excluding alignment padding."""
+        R = VALUE_FORMATS[VF_NAMES[self.value_format]][2]
+        return ((self.encoded_bits + 7) // 8 + (R * self.num_elements + 7) // 8 + (5 * self.B * self.T + 7) // 8
+                + 4 * (self.B + 1) + int(self._c.luts_bytes) + 256)
 
     def arrays(self) -> dict:
         return dict(code_lengths=self.code_lengths, luts=self.luts, encoded_exponent=self.encoded_exponent,
@@ -211,47 +221,60 @@ class HostTensor:
                     block_output_pos=self.block_output_pos)
 
 
-def _as_u16(w) -> np.ndarray:
+def _as_words(w, vf: str = "bf16") -> np.ndarray:
+    """Host words of value format vf: uint16 (bf16/fp16) or uint8 (fp8) bit patterns."""
+    wt = np.uint16 if VALUE_FORMATS[vf][1] == 2 else np.uint8
     try:
         import torch
         if isinstance(w, torch.Tensor):
             if w.is_cuda:
                 raise ValueError("df11.encode takes a host tensor")
             w = w.contiguous()
-            if w.dtype == torch.bfloat16:
-                w = w.view(torch.int16)
-            return w.numpy().view(np.uint16)
+            if w.element_size() != VALUE_FORMATS[vf][1]:
+                raise ValueError(f"{vf} words are {VALUE_FORMATS[vf][1]} bytes")
+            w = w.view(torch.int16 if wt is np.uint16 else torch.uint8)
+            return w.numpy().view(wt)
     except ImportError:
         pass
-    return np.ascontiguousarray(w).view(np.uint16)
+    return np.ascontiguousarray(w).view(wt)
 
 
-def _opts(T, n, lut_mode, num_threads):
-    return EncodeOpts(T, n, LUT_MODES[lut_mode], num_threads)
+def _as_u16(w) -> np.ndarray:
+    return _as_words(w, "bf16")
 
 
-def encode(w, T: int = 256, n: int = 8, lut_mode: str = "auto", num_threads: int = 0) -> HostTensor:
-    """df11_encode: BF16 host tensor (torch.bfloat16 or uint16 bit patterns) -> HostTensor."""
-    a = _as_u16(w)
+def _lut_bits(lut_bits) -> int:
+    return LUT_BITS_MONOLITHIC if lut_bits == "mono" else int(lut_bits)
+
+
+def _opts(T, n, lut_mode, num_threads, vf="bf16", lut_bits=8):
+    return EncodeOpts(T, n, LUT_MODES[lut_mode], num_threads, VALUE_FORMATS[vf][0], _lut_bits(lut_bits))
+
+
+def encode(w, T: int = 256, n: int = 8, lut_mode: str = "auto", num_threads: int = 0, vf: str = "bf16",
+           lut_bits=8) -> HostTensor:
+    """df11_encode: host tensor of value format vf (bf16 default: torch.bfloat16 or uint16 bit patterns;
+    fp16; fp8_e4m3 / fp8_e5m2 as uint8 patterns) -> HostTensor.  lut_bits: b in [1, 16] or "mono"."""
+    a = _as_words(w, vf)
     shape = a.shape
     a = a.reshape(-1)
     c = HostTensorC()
-    o = _opts(T, n, lut_mode, num_threads)
+    o = _opts(T, n, lut_mode, num_threads, vf, lut_bits)
     _check(lib().df11_encode(ctypes.c_void_p(a.ctypes.data if a.size else 0), a.size, ctypes.byref(o),
                              ctypes.byref(c)))
     return HostTensor(c, shape)
 
 
 def encode_group(ws, T: int = 256, n: int = 8, lut_mode: str = "auto", shared_codebook: bool = False,
-                 num_threads: int = 0):
-    arrs = [_as_u16(w) for w in ws]
+                 num_threads: int = 0, vf: str = "bf16", lut_bits=8):
+    arrs = [_as_words(w, vf) for w in ws]
     shapes = [a.shape for a in arrs]
     flat = [a.reshape(-1) for a in arrs]
     cnt = len(flat)
     ptrs = (ctypes.c_void_p * cnt)(*[a.ctypes.data if a.size else None for a in flat])
     ns = (ctypes.c_uint64 * cnt)(*[a.size for a in flat])
     outs = (HostTensorC * cnt)()
-    o = _opts(T, n, lut_mode, num_threads)
+    o = _opts(T, n, lut_mode, num_threads, vf, lut_bits)
     _check(lib().df11_encode_group(ptrs, ns, cnt, ctypes.byref(o), 1 if shared_codebook else 0, outs))
     res = []
     for i in range(cnt):
@@ -267,14 +290,15 @@ class DeviceTensor:
 
     def __init__(self, h: HostTensor, device="cuda", out=None):
         m = dict(num_elements=h.num_elements, T=h.T, n=h.n, B=h.B, k=h.k, lut_entry_bytes=h.lut_entry_bytes,
-                 encoded_bits=h.encoded_bits, max_code_len=h.max_code_len)
+                 encoded_bits=h.encoded_bits, max_code_len=h.max_code_len, value_format=h.value_format,
+                 lut_bits=h.lut_bits)
         self._init(m, h.arrays(), h.shape, device, out)
 
     @classmethod
     def from_arrays(cls, meta: dict, arrays: dict, shape=None, device="cuda", out=None) -> "DeviceTensor":
         """Upload DF11 arrays given as numpy (e.g. read from disk): keys code_lengths, luts,
         encoded_exponent, packed_sign_mantissa, gaps, block_output_pos; meta: num_elements, T, n, B, k,
-        lut_entry_bytes, encoded_bits, max_code_len."""
+        lut_entry_bytes, encoded_bits, max_code_len (+ value_format, lut_bits; default BF16, 8)."""
         self = cls.__new__(cls)
         self._init(meta, arrays, shape if shape is not None else (int(meta["num_elements"]),), device, out)
         return self
@@ -286,9 +310,13 @@ class DeviceTensor:
         self.num_elements = int(meta["num_elements"])
         self.meta = {k: int(meta[k]) for k in ("T", "n", "B", "k", "lut_entry_bytes", "encoded_bits",
                                                "max_code_len")}
+        self.meta["value_format"] = int(meta.get("value_format", 0))
+        self.meta["lut_bits"] = int(meta.get("lut_bits", 8))
+        self.vf = VF_NAMES[self.meta["value_format"]]
         B, T = self.meta["B"], self.meta["T"]
-        self.compressed_bytes = ((self.meta["encoded_bits"] + 7) // 8 + self.num_elements + (5 * B * T + 7) // 8
-                                 + 4 * (B + 1) + int(np.asarray(a["luts"]).size) + 256)
+        R = VALUE_FORMATS[self.vf][2]
+        self.compressed_bytes = ((self.meta["encoded_bits"] + 7) // 8 + (R * self.num_elements + 7) // 8
+                                 + (5 * B * T + 7) // 8 + 4 * (B + 1) + int(np.asarray(a["luts"]).size) + 256)
 
         def up(x):
             t = torch.from_numpy(np.ascontiguousarray(x).view(np.uint8).copy())
@@ -301,18 +329,19 @@ class DeviceTensor:
         self.luts = up(luts if luts.size else np.zeros(16, np.uint8))
         self.code_lengths = up(a["code_lengths"])
         self.block_output_pos = up(np.asarray(a["block_output_pos"], np.uint32).view(np.uint8))
-        self.out = out if out is not None else torch.empty(max(self.num_elements, 1), dtype=torch.bfloat16,
+        self.out = out if out is not None else torch.empty(max(self.num_elements, 1), dtype=out_dtype(self.vf),
                                                            device=dev)
 
     def descriptor(self, out=None) -> DeviceTensorC:
         o = self.out if out is None else out
-        if o.numel() < self.num_elements or o.dtype not in _u16_dtypes():
-            raise ValueError("output buffer too small or not 16-bit")
+        if o.numel() < self.num_elements or o.element_size() != VALUE_FORMATS[self.vf][1]:
+            raise ValueError(f"output buffer too small or not {VALUE_FORMATS[self.vf][1]}-byte words")
         m = self.meta
         return DeviceTensorC(self.encoded_exponent.data_ptr(), self.packed_sign_mantissa.data_ptr(),
                              self.gaps.data_ptr(), self.luts.data_ptr(), self.code_lengths.data_ptr(),
                              self.block_output_pos.data_ptr(), o.data_ptr(), self.num_elements,
-                             m["T"], m["n"], m["B"], m["k"], m["lut_entry_bytes"], 0)
+                             m["T"], m["n"], m["B"], m["k"], m["lut_entry_bytes"], m["value_format"],
+                             m["lut_bits"], 0)
 
     def staging_bytes(self) -> int:
         return sum(int(t.numel()) for t in (self.encoded_exponent, self.packed_sign_mantissa, self.gaps,
@@ -333,6 +362,13 @@ def clone_device_tensor(d: "DeviceTensor", out=None) -> "DeviceTensor":
 def _u16_dtypes():
     import torch
     return (torch.bfloat16, torch.int16, torch.uint16)
+
+
+def out_dtype(vf: str):
+    """torch dtype of a decoded tensor of value format vf."""
+    import torch
+    return {"bf16": torch.bfloat16, "fp16": torch.float16, "fp8_e4m3": torch.float8_e4m3fn,
+            "fp8_e5m2": torch.float8_e5m2}[vf]
 
 
 def to_device(h: HostTensor, device="cuda", out=None) -> DeviceTensor:
@@ -419,13 +455,14 @@ def decompress_host_block(hs, dts, host_outs, stream=None, copy_stream=None):
 class EncodePlan:
     """df11_encode_plan: codebook + geometry of one tensor (host); frees its LUT copy on deletion."""
 
-    def __init__(self, codebook_hist, tensor_hist=None, T: int = 256, n: int = 8, lut_mode: str = "auto"):
+    def __init__(self, codebook_hist, tensor_hist=None, T: int = 256, n: int = 8, lut_mode: str = "auto",
+                 lut_bits=8):
         cb = np.ascontiguousarray(codebook_hist, dtype=np.uint64)
         th = None if tensor_hist is None else np.ascontiguousarray(tensor_hist, dtype=np.uint64)
         if cb.shape != (256,) or (th is not None and th.shape != (256,)):
             raise ValueError("histograms have 256 bins")
         self._c = EncodePlanC()
-        o = _opts(T, n, lut_mode, 0)
+        o = _opts(T, n, lut_mode, 0, "bf16", lut_bits)
         _check(lib().df11_encode_plan_create(ctypes.c_void_p(cb.ctypes.data),
                                              None if th is None else ctypes.c_void_p(th.ctypes.data),
                                              ctypes.byref(o), ctypes.byref(self._c)))
@@ -437,7 +474,7 @@ class EncodePlan:
             pass
 
     def __getattr__(self, name):
-        if name in ("num_elements", "encoded_bits", "T", "n", "B", "k", "lut_entry_bytes", "max_code_len",
+        if name in ("num_elements", "encoded_bits", "T", "n", "B", "k", "lut_entry_bytes", "max_code_len", "lut_bits",
                     "luts_bytes", "encoded_exponent_bytes", "packed_sign_mantissa_bytes", "gaps_bytes",
                     "workspace_bytes"):
             return int(getattr(self.__dict__["_c"], name))
@@ -509,7 +546,10 @@ def _encode_device_with_plan(x, plan, stream, out):
     dt = DeviceTensor.__new__(DeviceTensor)
     dt.shape = tuple(x.shape)
     dt.num_elements = plan.num_elements
-    dt.meta = {k: getattr(plan, k) for k in ("T", "n", "B", "k", "lut_entry_bytes", "encoded_bits", "max_code_len")}
+    dt.meta = {k: getattr(plan, k) for k in ("T", "n", "B", "k", "lut_entry_bytes", "encoded_bits", "max_code_len",
+                                             "lut_bits")}
+    dt.meta["value_format"] = 0
+    dt.vf = "bf16"
     dt.encoded_exponent = buf(plan.encoded_exponent_bytes)
     dt.packed_sign_mantissa = buf(plan.packed_sign_mantissa_bytes)
     dt.gaps = buf(plan.gaps_bytes)

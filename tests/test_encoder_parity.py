@@ -164,3 +164,59 @@ def test_plan_cta_ranges_cover_and_balance():
                 work.append(int(out[c + 1]) - int(out[c]) + P * inner)
             if total >= grid * (P + 2):
                 assert max(work) - min(work) <= 2 * P + 2, (work, P)
+
+
+# ---------------------------------------------------------------------------- NEXT-4 format variants
+def _cmp_variant(fmt, h):
+    _cmp(fmt, h)
+    assert h.value_format == fmt["value_format"] and h.lut_bits == fmt["lut_bits"]
+
+
+@pytest.mark.parametrize("vf", ["fp16", "fp8_e4m3", "fp8_e5m2"])
+@pytest.mark.parametrize("case", ["gauss", "patterns", "ragged"])
+def test_encoder_value_formats_equal_oracle(oracle_mod, vf, case):
+    """FP16 / FP8 (R25-R27): the library encoder writes the oracle's bytes (residual stream included),
+    single- and multi-threaded, for Gaussian weights, every bit pattern and ragged sizes."""
+    if case == "gauss":
+        w = workloads.gaussian_values((1 << 19,), 4, vf)
+    elif case == "patterns":
+        rng = np.random.default_rng(8)
+        w = np.tile(workloads.all_patterns(vf), 3 if vf == "fp16" else 300)
+        rng.shuffle(w)
+    else:
+        w = workloads.gaussian_values((300007,), 5, vf)
+    fmt = oracle_mod.encode(w, vf=vf)
+    for threads in (1, 0):
+        _cmp_variant(fmt, df11.encode(w, num_threads=threads, vf=vf))
+
+
+@pytest.mark.parametrize("lut_bits", [1, 3, 5, 8, 11, 12, 16, "mono"])
+def test_encoder_lut_bits_equal_oracle(oracle_mod, lut_bits):
+    """b-bit hierarchical tables (App. I.2) and the monolithic table (b = L, App. I.1): same bytes."""
+    cases = [workloads.gaussian_bf16((1 << 18,), seed=6),
+             workloads.gaussian_values((1 << 18,), 7, "fp8_e4m3"),
+             workloads.from_exponent_histogram(workloads.fibonacci_histogram(34, 80), seed=3)]
+    for i, w in enumerate(cases):
+        vf = "fp8_e4m3" if i == 1 else "bf16"
+        try:
+            fmt = oracle_mod.encode(w, vf=vf, lut_bits=lut_bits)
+        except oracle_mod.FormatError as e:
+            assert lut_bits == "mono" and e.kind == "invalid_argument"
+            with pytest.raises(df11.Df11Error) as ei:
+                df11.encode(w, vf=vf, lut_bits=lut_bits)
+            assert ei.value.kind == "DF11_E_INVALID_ARGUMENT"
+            continue
+        _cmp_variant(fmt, df11.encode(w, vf=vf, lut_bits=lut_bits))
+
+
+def test_encoder_rejects_bad_variant_options():
+    w = workloads.gaussian_bf16((1000,), seed=1)
+    for kw in (dict(lut_bits=17), dict(lut_bits=40)):
+        with pytest.raises(df11.Df11Error):
+            df11.encode(w, **kw)
+    # the device encoder's plan is BF16 only
+    o = df11._opts(256, 8, "auto", 0, "fp16", 8)
+    plan = df11.EncodePlanC()
+    hist = (ctypes.c_uint64 * 256)(*([0] * 100 + [10] + [0] * 155))
+    st = df11.lib().df11_encode_plan_create(hist, None, ctypes.byref(o), ctypes.byref(plan))
+    assert df11.STATUS[st] == "DF11_E_UNSUPPORTED"

@@ -185,6 +185,21 @@ def from_exponent_histogram(counts: dict, seed: int = 0) -> np.ndarray:
     return (((sm & 0x80) << 8) | (exps << 7) | (sm & 0x7F)).astype(np.uint16)
 
 
+def from_exponent_histogram_vf(counts: dict, vf: str, seed: int = 0) -> np.ndarray:
+    """from_exponent_histogram for any value format: words of vf whose exponent field histogram is
+    exactly `counts`, shuffled, with random sign and mantissa bits."""
+    if vf == "bf16":
+        return from_exponent_histogram(counts, seed)
+    E, M = {"fp16": (5, 10), "fp8_e4m3": (4, 3), "fp8_e5m2": (5, 2)}[vf]
+    rng = np.random.Generator(np.random.PCG64(seed))
+    exps = np.concatenate([np.full(int(c), int(e), np.uint32) for e, c in counts.items() if c > 0])
+    assert exps.max() < (1 << E)
+    rng.shuffle(exps)
+    sm = rng.integers(0, 1 << (M + 1), size=exps.size, dtype=np.uint32)
+    words = ((sm >> M) << (E + M)) | (exps << M) | (sm & ((1 << M) - 1))
+    return words.astype(word_dtype(vf))
+
+
 def fibonacci_histogram(nsym: int = 40, first_exponent: int = 90) -> dict:
     """Fibonacci counts over `nsym` exponents: the unconstrained Huffman tree has depth nsym-1."""
     a, b = 1, 1
