@@ -12,6 +12,6 @@ is listed in DESIGN.md §4.
 """
 from .oracle import (FormatError, VALUE_FORMATS, WORD_DTYPE, build_oracle, compose,  # noqa: F401
                      compose_v, compressed_bytes, decode_alg1, decode_alg1_blocks, decode_alg1_range,
-                     decode_sequential, encode, entropy_bits, histogram, residual_array_bytes, residual_bits,
+                     decode_sequential, decode_sequential_blocks, encode, entropy_bits, histogram, residual_array_bytes, residual_bits,
                      split, split_v, vf_code)
 from . import huffman  # noqa: F401

@@ -233,9 +233,24 @@ static uint32_t read_gap(const uint8_t *gaps, uint64_t gaps_bytes, uint64_t g)
  * Bit by bit: append the next stream bit to `code`; after l bits, if code - first_code[l] < count[l]
  * the codeword is complete and names symbol sorted[offset[l] + code - first_code[l]].
  * Returns 0 on success, -1 if the stream runs out (corrupt), -2 on a malformed codebook. */
+int df11o_decode_sequential_range(const uint8_t *stream, uint64_t stream_bytes, const uint8_t *code_len /*256*/,
+                                  const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t start_bit,
+                                  uint64_t first, uint64_t n, int vf, void *out);
+
 int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const uint8_t *code_len /*256*/,
                             const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t n, int vf,
                             void *out)
+{
+    return df11o_decode_sequential_range(stream, stream_bytes, code_len, packed_sign_mantissa, psm_bytes, 0, 0, n,
+                                         vf, out);
+}
+
+/* D1 from the middle of the stream: the same decode started at stream bit `start_bit` with output index
+ * `first`, for n elements.  A format block b's first code starts at bit 8nT*b + Gaps[bT] and is element
+ * BlockOutputPos[b], so the blocks of a tensor can be decoded independently. */
+int df11o_decode_sequential_range(const uint8_t *stream, uint64_t stream_bytes, const uint8_t *code_len /*256*/,
+                                  const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t start_bit,
+                                  uint64_t first, uint64_t n, int vf, void *out)
 {
     const int R = 1 + VF_MAN_BITS[vf];
     uint32_t count[33] = {0};
@@ -267,8 +282,8 @@ int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const 
     }
 
     uint64_t total_bits = stream_bytes * 8;
-    uint64_t bit = 0;
-    for (uint64_t i = 0; i < n; i++) {
+    uint64_t bit = start_bit;
+    for (uint64_t i = first; i < first + n; i++) {
         uint64_t c = 0;
         int l = 0;
         int found = -1;

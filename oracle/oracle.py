@@ -65,6 +65,8 @@ def _load():
         lib.df11o_pack_gaps.argtypes = [P, U64, P]
         lib.df11o_decode_sequential.argtypes = [P, U64, P, P, U64, U64, I, P]
         lib.df11o_decode_sequential.restype = I
+        lib.df11o_decode_sequential_range.argtypes = [P, U64, P, P, U64, U64, U64, U64, I, P]
+        lib.df11o_decode_sequential_range.restype = I
         lib.df11o_decode_alg1.argtypes = [P, U32, U32, U32, P, P, U64, P, U64, P, P, U64, U32, U32, U32, U64, I, I,
                                           P]
         lib.df11o_decode_alg1.restype = I
@@ -261,6 +263,23 @@ def decode_sequential(fmt: dict) -> np.ndarray:
     if rc != 0:
         raise FormatError("corrupt", f"sequential decode failed ({rc})")
     return out
+
+
+def decode_sequential_blocks(fmt: dict, b0: int, b1: int, out: np.ndarray) -> None:
+    """D1 over format blocks [b0, b1): the sequential decoder started at block b0's first code (stream
+    bit 8nT*b0 + Gaps[b0 T], element BlockOutputPos[b0]) for the blocks' elements, written
+    into `out` (the whole tensor's array).  Lets a caller spread one tensor over threads."""
+    if b1 <= b0:
+        return
+    T, n = int(fmt["T"]), int(fmt["n"])
+    bop = fmt["block_output_pos"]
+    first, last = int(bop[b0]), int(bop[b1])
+    start = 8 * n * T * b0 + _read_gap(fmt["gaps"], b0 * T)
+    s, psm = fmt["encoded_exponent"], fmt["packed_sign_mantissa"]
+    rc = _load().df11o_decode_sequential_range(_ptr(s), s.size, _ptr(fmt["code_lengths"]), _ptr(psm), psm.size,
+                                               start, first, last - first, _vf(fmt), _ptr(out))
+    if rc != 0:
+        raise FormatError("corrupt", f"sequential decode failed ({rc})")
 
 
 def decode_alg1(fmt: dict, check_counts: bool = True) -> np.ndarray:

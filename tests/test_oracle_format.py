@@ -203,3 +203,17 @@ def test_shared_codebook_scope(oracle_mod):
     assert fa["encoded_bits"] >= own["encoded_bits"]          # the tensor's own Huffman code is optimal
     with pytest.raises(oracle_mod.FormatError):
         oracle_mod.encode(b, codebook_hist=ha * (hb == 0))
+
+
+def test_d1_block_ranges_equal_whole_decode(oracle_mod):
+    """D1 started at format block boundaries (bit 8nT*b + gap, element BOP[b]) reproduces the tensor
+    block range by block range: the gap / BlockOutputPos definitions locate every block."""
+    import workloads
+    for w, kw in ((workloads.gaussian_bf16((200003,), seed=12), {}),
+                  (workloads.gaussian_values((150001,), 13, "fp16"), dict(vf="fp16", T=128, n=16))):
+        fmt = oracle_mod.encode(w, **kw)
+        out = np.zeros_like(w.reshape(-1))
+        B = fmt["B"]
+        for b0 in range(0, B, 3):
+            oracle_mod.decode_sequential_blocks(fmt, b0, min(B, b0 + 3), out)
+        assert np.array_equal(out, w.reshape(-1))
