@@ -149,7 +149,8 @@ def _word_np(vf):
 def oracle_decode_rate(tensors_np, budget_s: float = 8.0, vf: str = "bf16", lut_bits=8):
     """Time the CPU oracle on a bounded sample of this workload (whole tensors in config order until
     ~budget_s of single-thread work), two ways (SURVEY 8(d) "CPU oracle timing"):
-      D1: the sequential decoder, one thread per tensor (it is sequential by definition);
+      D1: the sequential decoder, all host cores over the format blocks (started at each block's first
+          code, which Gaps / BlockOutputPos locate);
       D2: the Algorithm 1 emulator with all host cores spread over the format blocks of each tensor.
     Returns the cpu_baseline dict (value = the faster of the two, with the threads it used)."""
     import concurrent.futures as cf
@@ -166,18 +167,26 @@ def oracle_decode_rate(tensors_np, budget_s: float = 8.0, vf: str = "bf16", lut_
     elems = sum(w.size for _, _, w in fmts)
     host_cores = os.cpu_count() or 1
 
-    # D1: one thread per tensor, whole passes until ~budget_s of thread time (at most 8 passes)
-    d1_threads = min(len(fmts), host_cores)
+    # D1: every host core on the format blocks of each tensor (the sequential decoder started at each
+    # block's first code: bit 8nT*b + gap, element BlockOutputPos[b]); whole passes until ~budget_s of
+    # thread time (at most 8 passes)
+    wb = np.dtype(workloads.word_dtype(vf)).itemsize
+    d1_threads = host_cores
+    outs = [np.zeros(w.size, workloads.word_dtype(vf)) for _, _, w in fmts]
+    jobs1 = []
+    for (name, f, w), o in zip(fmts, outs):
+        B = int(f["B"])
+        step = max(1, -(-B // (4 * host_cores)))
+        jobs1 += [(f, b, min(B, b + step), o) for b in range(0, B, step)]
     passes, dt = 0, 0.0
     with cf.ThreadPoolExecutor(max_workers=d1_threads) as ex:
         while passes < 8 and (passes == 0 or dt * d1_threads < budget_s):
             t0 = time.perf_counter()
-            outs = list(ex.map(lambda f: oracle.decode_sequential(f[1]), fmts))
+            list(ex.map(lambda j: oracle.decode_sequential_blocks(*j), jobs1))
             dt += time.perf_counter() - t0
             passes += 1
     for (name, _, w), o in zip(fmts, outs):
         assert np.array_equal(o, w.reshape(-1)), name
-    wb = np.dtype(workloads.word_dtype(vf)).itemsize
     d1 = {"gbs": wb * elems * passes / dt / 1e9, "threads": d1_threads, "passes": passes, "seconds": round(dt, 2)}
 
     # D2: every host core on the format blocks of each tensor in turn
@@ -200,37 +209,53 @@ def oracle_decode_rate(tensors_np, budget_s: float = 8.0, vf: str = "bf16", lut_
           "seconds": round(dt2, 2)}
     best = d2 if d2["gbs"] >= d1["gbs"] else d1
     sample = (f"{len(fmts)} tensor(s) of the workload ({elems} elements: " + ", ".join(n for n, _, _ in fmts) +
-              f"); D1 sequential decode, {d1_threads} thread(s) (one per tensor); D2 Alg. 1 emulation, "
-              f"{host_cores} threads over the format blocks")
+              f"); D1 sequential decode and D2 Alg. 1 emulation, each with {host_cores} threads over the "
+              f"format blocks")
     return {"value": best["gbs"], "unit": UNIT, "cores": best["threads"], "kind": "oracle", "sample": sample,
             "d1": d1, "d2": d2, "host_cores": host_cores, "cpu_model": cpu_model()}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle (D1) timed as the reference arm on this workload."""
+    """--impl reference: the CPU oracle (D1, the sequential decoder) timed as the reference arm on this
+    workload, with every host core over the format blocks of a bounded sample."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import concurrent.futures as cf
+
     import oracle
     oracle.build_oracle()
     name, shape = workloads.CONFIGS[args.config][0]
-    w = workloads.gaussian_bf16(shape, workloads.seed_for(args.config, 0, name)).reshape(-1)
-    w = w[: 1 << 22]                                       # bounded sample per step: 4 Mi elements
-    fmt = oracle.encode(w)
-    for _ in range(args.warmup):
-        oracle.decode_sequential(fmt)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        out = oracle.decode_sequential(fmt)
-    dt = time.perf_counter() - t0
+    w = workloads.gaussian_values(shape, workloads.seed_for(args.config, 0, name), args.vf).reshape(-1)
+    w = w[: 1 << 24]                                       # bounded sample per step: 16 Mi elements
+    lut_bits = args.lut_bits if args.lut_bits == "mono" else int(args.lut_bits)
+    fmt = oracle.encode(w, vf=args.vf, lut_bits=lut_bits)
+    cores = os.cpu_count() or 1
+    out = np.zeros_like(w)
+    B = int(fmt["B"])
+    step_b = max(1, -(-B // (4 * cores)))
+    jobs = [(fmt, b, min(B, b + step_b), out) for b in range(0, B, step_b)]
+    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
+        def one():
+            list(ex.map(lambda j: oracle.decode_sequential_blocks(*j), jobs))
+        for _ in range(args.warmup):
+            one()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            one()
+        dt = time.perf_counter() - t0
     assert np.array_equal(out, w)
-    value = 2 * w.size * args.steps / dt / 1e9
-    sample = f"D1 sequential decode of the first {w.size} elements of {args.config}/{name} per step, 1 thread"
+    wb = np.dtype(workloads.word_dtype(args.vf)).itemsize
+    value = wb * w.size * args.steps / dt / 1e9
+    sample = (f"D1 sequential decode of the first {w.size} elements of {args.config}/{name} per step, "
+              f"{cores} threads over its format blocks")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic", "config": {"workload": args.config, "elements_per_step": int(w.size)},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "data": "synthetic", "config": {"workload": args.config, "elements_per_step": int(w.size),
+                                             "value_format": args.vf},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -236,15 +236,17 @@ extern "C" df11_status df11_decompress_block_budget(const df11_device_tensor *ts
     int max_smem = 0, num_sms = 0;
     device_attrs(dev, max_smem, num_sms);
     if (nfast) {
-        // one product launch per chunk size (n = 8 and n = 16 tensors take different kernel builds)
-        uint32_t n8[DF11_MAX_BATCH], n16[DF11_MAX_BATCH], k8 = 0, k16 = 0;
-        for (uint32_t k = 0; k < nfast; k++) (ts[fast_idx[k]].n == 16 ? n16[k16++] : n8[k8++]) = fast_idx[k];
-        if (k8) {
-            df11_status st = launch_fast_batch(ts, n8, k8, num_sms, dev, stream, max_ctas);
-            if (st != DF11_OK) return st;
+        // one product launch per (chunk size, value format, byte tables or not): each takes its own
+        // kernel build
+        uint32_t grp[16][DF11_MAX_BATCH], cnt[16] = {};
+        for (uint32_t k = 0; k < nfast; k++) {
+            const df11_device_tensor &t = ts[fast_idx[k]];
+            const uint32_t key = (df11::lut_bits_of(t) == 8 ? 0u : 8u) + (t.n == 16 ? 4u : 0u) + t.value_format;
+            grp[key][cnt[key]++] = fast_idx[k];
         }
-        if (k16) {
-            df11_status st = launch_fast_batch(ts, n16, k16, num_sms, dev, stream, max_ctas);
+        for (uint32_t key = 0; key < 16; key++) {
+            if (!cnt[key]) continue;
+            df11_status st = launch_fast_batch(ts, grp[key], cnt[key], num_sms, dev, stream, max_ctas);
             if (st != DF11_OK) return st;
         }
     }

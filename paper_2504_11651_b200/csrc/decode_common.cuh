@@ -44,7 +44,11 @@ __device__ __forceinline__ uint16_t compose(uint32_t exponent, uint32_t psm) {
 
 // b of the format's LUTs (0 = 8, the paper's byte tables).
 __host__ __device__ __forceinline__ uint32_t lut_bits_of(const df11_device_tensor &t) {
+#ifdef DF11_LB8_ONLY
+    return 8u;                                   // A/B knob (register-pressure experiment)
+#else
     return t.lut_bits ? t.lut_bits : 8u;
+#endif
 }
 
 // Value formats (df11.h DF11_VF_*, R25): M mantissa bits, E exponent bits, residual R = 1 + M bits at

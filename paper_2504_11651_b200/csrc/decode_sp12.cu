@@ -134,8 +134,9 @@ __device__ __forceinline__ uint32_t res_smem(uint32_t buf, uint32_t bit) {
 // kNB = 16: T = 128, n = 16 (NEXT-4: half the gap bits); a format block has the same 2 048 stream
 // bytes and a lane decodes its one 16-byte chunk as one chain in a 160-bit buffer.
 // kVF: value format (DF11_VF_*, NEXT-4).  Decode, scan and compaction are the same for every format
-// (the symbols are exponent fields); the merge composes the format's words.
-template <uint32_t kNB, uint32_t kVF>
+// (the symbols are exponent fields); the merge composes the format's words.  kB8: the format's LUTs
+// are the paper's byte tables (b = 8); otherwise b-bit tables (App. I.2), walked in global memory.
+template <uint32_t kNB, uint32_t kVF, bool kB8>
 __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__ Batch bt) {
     using L = Lay12<kVF>;
     constexpr VF kF = vf_of(kVF);
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             }
         }
         bool safe, lut_in_smem;
-        const bool long_codes = build_t12<kCta12, kVF>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
+        const bool long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
                                                        kOffGrp + L::kGReg, tid, safe, lut_in_smem);
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
 
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 
         auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
             if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, 8u, len);
-            return lut_walk_global(w, ts, len);
+            return lut_walk_global<kB8>(w, ts, len);
         };
 
         // =============================== tiles of this group
@@ -719,19 +720,33 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 #undef K_S24
 }
 
-uint32_t g_sp12_attr_set[64];
+uint32_t g_sp12_attr_set[64];   // bit (b8 ? 0 : 8) + (n16 ? 4 : 0) + vf: smem attribute set
 
-template <uint32_t kNB, uint32_t kVF>
+template <uint32_t kNB, uint32_t kVF, bool kB8>
 cudaError_t launch_one(const Batch &bt, int device, uint32_t grid, cudaStream_t stream) {
-    constexpr uint32_t bit = 1u << ((kNB == 16 ? 4 : 0) + kVF);
+    constexpr uint32_t bit = 1u << ((kB8 ? 0 : 8) + (kNB == 16 ? 4 : 0) + kVF);
     if (device >= 0 && device < 64 && !(g_sp12_attr_set[device] & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(sp12_kernel<kNB, kVF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(sp12_kernel<kNB, kVF, kB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)Lay12<kVF>::kSmem);
         if (e != cudaSuccess) return e;
         g_sp12_attr_set[device] |= bit;
     }
-    sp12_kernel<kNB, kVF><<<grid, kCta12, Lay12<kVF>::kSmem, stream>>>(bt);
+    sp12_kernel<kNB, kVF, kB8><<<grid, kCta12, Lay12<kVF>::kSmem, stream>>>(bt);
     return cudaGetLastError();
+}
+
+template <bool kB8>
+cudaError_t launch_vf(const Batch &bt, int device, uint32_t grid, cudaStream_t stream, uint32_t key) {
+    switch (key) {
+        case 0: return launch_one<8, DF11_VF_BF16, kB8>(bt, device, grid, stream);
+        case 1: return launch_one<8, DF11_VF_FP16, kB8>(bt, device, grid, stream);
+        case 2: return launch_one<8, DF11_VF_FP8_E4M3, kB8>(bt, device, grid, stream);
+        case 3: return launch_one<8, DF11_VF_FP8_E5M2, kB8>(bt, device, grid, stream);
+        case 4: return launch_one<16, DF11_VF_BF16, kB8>(bt, device, grid, stream);
+        case 5: return launch_one<16, DF11_VF_FP16, kB8>(bt, device, grid, stream);
+        case 6: return launch_one<16, DF11_VF_FP8_E4M3, kB8>(bt, device, grid, stream);
+        default: return launch_one<16, DF11_VF_FP8_E5M2, kB8>(bt, device, grid, stream);
+    }
 }
 
 }  // namespace
@@ -752,7 +767,8 @@ bool fast_supports(const df11_device_tensor &t) {
            (reinterpret_cast<uintptr_t>(t.out) & (vf_of(t.value_format).word_bytes - 1)) == 0;
 }
 
-// Launch for a batch whose tensors share n (8 with T = 256, or 16 with T = 128) and the value format.
+// Launch for a batch whose tensors share n (8 with T = 256, or 16 with T = 128), the value format and
+// whether their LUTs are the paper's byte tables.
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches) {
     if (bt.total_tiles == 0) return cudaSuccess;
     int num_sms = 0;
@@ -762,16 +778,9 @@ cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64
     const uint32_t vf = bt.t[0].value_format;
     const uint32_t grid = bt.grid ? bt.grid
                                   : min((uint32_t)num_sms, (bt.total_tiles + kGroups12 - 1) / kGroups12);
-    switch (vf + (n16 ? 4u : 0u)) {
-        case 0: e = launch_one<8, DF11_VF_BF16>(bt, device, grid, stream); break;
-        case 1: e = launch_one<8, DF11_VF_FP16>(bt, device, grid, stream); break;
-        case 2: e = launch_one<8, DF11_VF_FP8_E4M3>(bt, device, grid, stream); break;
-        case 3: e = launch_one<8, DF11_VF_FP8_E5M2>(bt, device, grid, stream); break;
-        case 4: e = launch_one<16, DF11_VF_BF16>(bt, device, grid, stream); break;
-        case 5: e = launch_one<16, DF11_VF_FP16>(bt, device, grid, stream); break;
-        case 6: e = launch_one<16, DF11_VF_FP8_E4M3>(bt, device, grid, stream); break;
-        default: e = launch_one<16, DF11_VF_FP8_E5M2>(bt, device, grid, stream); break;
-    }
+    const uint32_t key = vf + (n16 ? 4u : 0u);
+    e = lut_bits_of(bt.t[0]) == 8 ? launch_vf<true>(bt, device, grid, stream, key)
+                                  : launch_vf<false>(bt, device, grid, stream, key);
     if (e == cudaSuccess && launches) (*launches)++;
     return e;
 }

@@ -135,10 +135,13 @@ __device__ __forceinline__ uint32_t lut_level_idx(uint32_t w, uint32_t lb, uint3
 
 // Paper's hierarchical LUT walk over the format's b-bit tables in global memory; returns
 // the exponent and its code length.  Bounded: <= ceil(32/b) levels, child < k, zero length -> 32.
+// kB8: the paper's byte tables (b = 8, a compile-time constant: fewer registers at the call sites of
+// the product kernel); otherwise b = ts.lut_bits.
+template <bool kB8>
 __device__ __noinline__ uint32_t lut_walk_global(uint32_t w, const df11_device_tensor &ts, uint32_t &len) {
     const uint8_t *__restrict__ luts = ts.luts;
     const uint32_t eb = ts.lut_entry_bytes, thr = eb == 1 ? 240u : 256u;
-    const uint32_t lb = lut_bits_of(ts), levels = (32u + lb - 1u) / lb;
+    const uint32_t lb = kB8 ? 8u : lut_bits_of(ts), levels = kB8 ? 4u : (32u + lb - 1u) / lb;
     uint32_t table = 0, e = 0;
 #pragma unroll 1
     for (uint32_t i = 0; i < levels; i++) {

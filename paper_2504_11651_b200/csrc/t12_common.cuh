@@ -199,8 +199,8 @@ __device__ __forceinline__ uint16_t compose_r(uint32_t r, uint32_t psm) {
 // CodeLengths at len / rlen (indexed by exponent / by rotated exponent; absent codes: 32 in rlen).
 // fc: 8 KB of scratch for the first-code table.  Returns whether the all-ones row is an escape (some
 // code is longer than 12 bits); `safe` = some code is 1 bit long.  Symbols are stored as
-// to_stored<kVF>; b-bit tables (lut_bits != 8) are walked row by row.
-template <uint32_t kThreads, uint32_t kVF>
+// to_stored<kVF>; b-bit tables (lut_bits != 8, kB8 = false) are walked row by row.
+template <uint32_t kThreads, uint32_t kVF, bool kB8>
 __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t *sb, uint32_t sbase,
                                           uint32_t off_t, uint32_t off_lut, uint32_t off_len, uint32_t off_rlen,
                                           uint32_t off_fc, uint32_t tid, bool &safe, bool &lut_in_smem) {
@@ -208,7 +208,7 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
     // walked in global memory (only the table build and codes longer than 12 bits walk them)
     const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
     const uint32_t lut_bytes = kk * 256u * eb_bytes;
-    lut_in_smem = (ts.lut_bits == 0 || ts.lut_bits == 8) && lut_bytes <= kLutSmem;
+    lut_in_smem = kB8 && lut_bytes <= kLutSmem;
     if (lut_in_smem) {
         if ((reinterpret_cast<uintptr_t>(ts.luts) & 15) == 0) {       // 16-byte loads (k*256*eb bytes)
             for (uint32_t i = tid; i < lut_bytes / 16; i += kThreads)
@@ -281,7 +281,7 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
         // row (in global memory / L1: a cold path, kept simple so that it adds no register pressure)
         for (uint32_t row = tid; row < kRows; row += kThreads) {
             uint32_t len;
-            const uint32_t sym = lut_walk_global(row << (32 - kR), ts, len);
+            const uint32_t sym = lut_walk_global<kB8>(row << (32 - kR), ts, len);
             fc[fci(row)] = len <= kR ? (uint16_t)(to_stored<kVF>(sym) | (len << 8)) : (uint16_t)0;
         }
         __syncthreads();
