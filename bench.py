@@ -119,6 +119,13 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def variant_key(args) -> str:
+    """Suffix of the ncu summary key for a NEXT-4 format variant ("" for the paper's format)."""
+    if args.vf == "bf16" and str(args.lut_bits) == "8" and args.format == "256x8":
+        return ""
+    return f"/{args.vf}-b{args.lut_bits}-{args.format}"
+
+
 def ncu_traffic(config: str, kernel: str):
     """Per-launch dram bytes from the committed ncu summary (profiles/ncu_summary.json), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -407,7 +414,7 @@ def main():
     peak, peak_src = measured_peaks()
     achieved = algo_bytes / (avg_launch_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config, kernel_used),
+                "traffic": ncu_traffic(args.config, kernel_used + variant_key(args)),
                 "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu "
                                   "--set full capture (profiles/ncu_summary.json), not measured in this run",
                 "peak_source": peak_src,
