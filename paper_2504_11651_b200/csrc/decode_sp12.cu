@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         if (t == 0 && tile < seg_end) stage_sm(nlo, nhi);
 
         auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
-            if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, 8u, len);
+            if (lut_in_smem)
+                return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, kB8 ? 8u : lut_bits_of(ts), len);
             return lut_walk_global<kB8>(w, ts, len);
         };
 

@@ -204,11 +204,11 @@ template <uint32_t kThreads, uint32_t kVF, bool kB8>
 __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t *sb, uint32_t sbase,
                                           uint32_t off_t, uint32_t off_lut, uint32_t off_len, uint32_t off_rlen,
                                           uint32_t off_fc, uint32_t tid, bool &safe, bool &lut_in_smem) {
-    // the paper's byte tables (b = 8) are staged in SMEM when they fit; b-bit tables of other widths are
-    // walked in global memory (only the table build and codes longer than 12 bits walk them)
-    const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
-    const uint32_t lut_bytes = kk * 256u * eb_bytes;
-    lut_in_smem = kB8 && lut_bytes <= kLutSmem;
+    // the format tables are staged in SMEM when they fit (b = 8: the paper's byte tables, b a compile-time
+    // constant; other b: b-bit tables, App. I.2, walked with a runtime b); otherwise walked in global
+    const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k, lb = kB8 ? 8u : lut_bits_of(ts);
+    const uint32_t lut_bytes = (kk << lb) * eb_bytes;
+    lut_in_smem = lut_bytes <= kLutSmem;
     if (lut_in_smem) {
         if ((reinterpret_cast<uintptr_t>(ts.luts) & 15) == 0) {       // 16-byte loads (k*256*eb bytes)
             for (uint32_t i = tid; i < lut_bytes / 16; i += kThreads)
@@ -277,11 +277,12 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
             if (r == kRows - 1) row_esc_last = c2 == 0;
         }
     } else {
-        // b-bit tables other than b = 8, or tables too large for SMEM: one walk of the format LUTs per
-        // row (in global memory / L1: a cold path, kept simple so that it adds no register pressure)
+        // b-bit tables other than b = 8, or tables too large for SMEM: one walk of the format LUTs per row
         for (uint32_t row = tid; row < kRows; row += kThreads) {
             uint32_t len;
-            const uint32_t sym = lut_walk_global<kB8>(row << (32 - kR), ts, len);
+            const uint32_t sym = lut_in_smem ? lut_walk_smem(row << (32 - kR), sbase + off_lut, sbase + off_len,
+                                                             eb_bytes, kk, lb, len)
+                                             : lut_walk_global<kB8>(row << (32 - kR), ts, len);
             fc[fci(row)] = len <= kR ? (uint16_t)(to_stored<kVF>(sym) | (len << 8)) : (uint16_t)0;
         }
         __syncthreads();

@@ -26,11 +26,20 @@ class BlockWeights:
     def from_host(cls, hosts, device="cuda"):
         return cls([df11.to_device(h, device) for h in hosts])
 
+    @property
+    def vf(self) -> str:
+        return self.dts[0].vf if self.dts else "bf16"
+
+    def scratch_elements(self) -> int:
+        """Words of a scratch that holds every tensor at a 16-byte aligned offset."""
+        return self.numel + 16 * len(self.dts) + 64
+
     def plan(self, scratch):
+        upv = 16 // scratch.element_size()                  # words per 16 bytes
         outs, o = [], 0
         for d in self.dts:
             outs.append(scratch[o:o + d.num_elements])
-            o += (d.num_elements + 7) // 8 * 8
+            o += (d.num_elements + upv - 1) // upv * upv    # 16-byte aligned views (128-bit stores)
         return df11.BlockPlan(self.dts, outs)
 
 
@@ -43,8 +52,9 @@ class OverlapRunner:
         import torch
         self.blocks = list(blocks)
         self.device = torch.device(device)
-        cap = max(b.numel + 8 * len(b.dts) for b in self.blocks) + 64
-        self.scratch = [torch.empty(cap, dtype=torch.bfloat16, device=self.device) for _ in range(2)]
+        cap = max(b.scratch_elements() for b in self.blocks) if self.blocks else 64
+        dt = df11.out_dtype(self.blocks[0].vf if self.blocks else "bf16")
+        self.scratch = [torch.empty(cap, dtype=dt, device=self.device) for _ in range(2)]
         self.prefetch = prefetch
         self.decode_ctas = int(decode_ctas)
         self.decode_stream = torch.cuda.Stream(device=self.device)
@@ -80,3 +90,60 @@ class OverlapRunner:
             self.consumed[k].record(main)            # compute on this scratch is enqueued
             if not self.prefetch and i + 1 < n:
                 self._decode(i + 1, main)
+
+
+# --------------------------------------------------------------------------- PyTorch module hook
+_VF_OF_DTYPE = {"torch.bfloat16": "bf16", "torch.float16": "fp16", "torch.float8_e4m3fn": "fp8_e4m3",
+                "torch.float8_e5m2": "fp8_e5m2"}
+
+
+class DF11Hook:
+    """Thin PyTorch block hook (NEXT-1): the named weights of `module` live in HBM as DF11
+    tensors only.  A forward pre-hook decodes them with ONE df11_decompress_block launch into a scratch
+    and binds the views as the module's parameters; a forward hook unbinds them after the forward (the
+    decoded matrices are "immediately discarded": the scratch can be shared by every block)."""
+
+    def __init__(self, module, names, weights: BlockWeights, scratch=None):
+        import torch
+        self.module, self.names, self.weights = module, list(names), weights
+        if scratch is None:
+            dev = weights.dts[0].encoded_exponent.device
+            scratch = torch.empty(weights.scratch_elements(), dtype=df11.out_dtype(weights.vf), device=dev)
+        if scratch.numel() < weights.scratch_elements():
+            raise ValueError("scratch too small for this block")
+        self.plan = weights.plan(scratch)
+        self.slots = []
+        for n in self.names:
+            path, _, attr = n.rpartition(".")
+            sub = module.get_submodule(path) if path else module
+            sub._parameters[attr] = None                 # the dense weight is dropped
+            self.slots.append((sub, attr))
+        self.handles = [module.register_forward_pre_hook(self._bind), module.register_forward_hook(self._unbind)]
+
+    def _bind(self, mod, args):
+        import torch
+        self.plan.run()                                   # current stream, one launch
+        for (sub, attr), w in zip(self.slots, self.plan.outputs()):
+            sub._parameters[attr] = torch.nn.Parameter(w, requires_grad=False)
+
+    def _unbind(self, mod, args, out):
+        for sub, attr in self.slots:
+            sub._parameters[attr] = None
+
+    def remove(self):
+        for h in self.handles:
+            h.remove()
+
+
+def compress_module(module, names=None, device="cuda", scratch=None, **encode_kw) -> DF11Hook:
+    """Encode the named parameters of `module` (default: every floating-point parameter of BF16 /
+    FP16 / FP8 dtype) with df11_encode, keep only their DF11 form in HBM, and attach a DF11Hook."""
+    if names is None:
+        names = [n for n, p in module.named_parameters() if str(p.dtype) in _VF_OF_DTYPE]
+    dts = []
+    for n in names:
+        p = module.get_parameter(n)
+        vf = _VF_OF_DTYPE[str(p.dtype)]
+        h = df11.encode(p.detach().cpu(), vf=vf, **encode_kw)
+        dts.append(df11.to_device(h, device))
+    return DF11Hook(module, names, BlockWeights(dts), scratch)

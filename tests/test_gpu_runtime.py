@@ -98,3 +98,29 @@ def test_sm_budget_bit_exact(max_ctas):
     assert df11.launch_count() - before == 1
     for w, o in zip(ws, outs):
         assert np.array_equal(o.reshape(-1).view(torch.int16).cpu().numpy().view(np.uint16), w.reshape(-1))
+
+
+def test_module_hook_bit_exact():
+    """DF11Hook: a BF16 MLP block whose weights exist only as DF11 in HBM produces bit-identical outputs
+    (one decode launch per forward); two blocks share one scratch (decoded weights discarded)."""
+    from paper_2504_11651_b200 import df11, runtime
+    torch.manual_seed(0)
+
+    def block():
+        return torch.nn.Sequential(torch.nn.Linear(1024, 2816, bias=False), torch.nn.SiLU(),
+                                   torch.nn.Linear(2816, 1024, bias=False)).to("cuda", torch.bfloat16)
+    b1, b2 = block(), block()
+    x = torch.randn(8, 1024, device="cuda", dtype=torch.bfloat16)
+    ref = b2(b1(x))
+    shared = torch.empty(2 * 2816 * 1024 + 4096, dtype=torch.bfloat16, device="cuda")
+    h1 = runtime.compress_module(b1, scratch=shared)
+    h2 = runtime.compress_module(b2, scratch=shared)
+    assert b1[0].weight is None and b2[2].weight is None
+    n0 = df11.launch_count()
+    out = b2(b1(x))
+    torch.cuda.synchronize()
+    assert df11.launch_count() - n0 == 2
+    assert torch.equal(out, ref)
+    assert b1[0].weight is None                           # unbound after the forward
+    h1.remove()
+    h2.remove()
