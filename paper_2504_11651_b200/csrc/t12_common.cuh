@@ -210,12 +210,11 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
     const uint32_t lut_bytes = (kk << lb) * eb_bytes;
     lut_in_smem = lut_bytes <= kLutSmem;
     if (lut_in_smem) {
-        if ((reinterpret_cast<uintptr_t>(ts.luts) & 15) == 0) {       // 16-byte loads (k*256*eb bytes)
-            for (uint32_t i = tid; i < lut_bytes / 16; i += kThreads)
-                reinterpret_cast<uint4 *>(sb + off_lut)[i] = __ldg(reinterpret_cast<const uint4 *>(ts.luts) + i);
-        } else {
-            for (uint32_t i = tid; i < lut_bytes; i += kThreads) sb[off_lut + i] = __ldg(ts.luts + i);
-        }
+        // 16-byte loads (k * 2^b * entry bytes is a multiple of 16 for b >= 4), then the tail bytes
+        const uint32_t n16 = (reinterpret_cast<uintptr_t>(ts.luts) & 15) == 0 ? lut_bytes / 16 : 0;
+        for (uint32_t i = tid; i < n16; i += kThreads)
+            reinterpret_cast<uint4 *>(sb + off_lut)[i] = __ldg(reinterpret_cast<const uint4 *>(ts.luts) + i);
+        for (uint32_t i = 16 * n16 + tid; i < lut_bytes; i += kThreads) sb[off_lut + i] = __ldg(ts.luts + i);
     }
     uint32_t len_t = 0;
     if (tid < 256u) {
@@ -234,7 +233,7 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
     // so that they spread over the banks instead of piling into one
     auto fci = [](uint32_t i) { return i ^ (((i >> 6) & 31u) << 1); };
     bool row_esc_last = false;
-    if (kRows == 4 * kThreads && lut_in_smem) {
+    if (kB8 && kRows == 4 * kThreads && lut_in_smem) {
         // 12-bit prefix r: its first 8 bits index the root LUT; a code of 9..12 bits is
         // resolved by the second-level LUT from the last 4 bits (zero-padded).  Four rows per thread,
         // unrolled for ILP; then up to 4 chained first-code lookups per row.

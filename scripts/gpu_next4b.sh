@@ -17,5 +17,10 @@ echo "rc=$?"; tail -3 /tmp/san_var.log
 echo "== racecheck, FP16 / FP8 cases"
 DF11_MAX_GRID=2 timeout 1200 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest -q -x tests/test_gpu_variants.py -k "value_format_parity and gauss and fast and not 1m" > /tmp/san_var_rc.log 2>&1
 echo "rc=$?"; grep -E "RACECHECK SUMMARY|hazard|passed|failed" /tmp/san_var_rc.log | tail -5
+if [ -f paper_2504_11651_b200/lib/variants/smbar.so ]; then
+  echo "== racecheck, same cases, A/B variant with a group barrier before the residual TMA refill"
+  DF11_LIB=$PWD/paper_2504_11651_b200/lib/variants/smbar.so DF11_MAX_GRID=2 timeout 1200 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest -q -x tests/test_gpu_variants.py -k "value_format_parity and gauss and fast and not 1m" > /tmp/san_var_rb.log 2>&1
+  echo "rc=$?"; grep -E "RACECHECK SUMMARY|hazard|passed|failed" /tmp/san_var_rb.log | tail -5
+fi
 } > gpurun_out/${TAG}.log 2>&1
 cat gpurun_out/${TAG}.log
