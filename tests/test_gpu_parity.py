@@ -12,7 +12,7 @@ import workloads
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-KERNELS = ["alg1", "fast"]
+KERNELS = ["alg1", "fast", "fast_notable"]   # fast_notable: no load-time decode table (built per CTA)
 
 
 @pytest.fixture(scope="module")
@@ -29,7 +29,10 @@ def _fast_ok(df11, meta):
 
 
 def _gpu_decode_arrays(df11, meta, arrays, kernel, shape=None):
-    dt = df11.DeviceTensor.from_arrays(meta, arrays, shape=shape)
+    dt = df11.DeviceTensor.from_arrays(meta, arrays, shape=shape, decode_table=kernel != "fast_notable")
+    if kernel == "fast_notable":
+        assert dt.decode_table is None
+        kernel = "fast"
     out = df11.decompress(dt, kernel=kernel)
     torch.cuda.synchronize()
     return out.view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1)
@@ -40,7 +43,7 @@ def _check_oracle_format(df11, oracle_mod, w, kernel, **kw):
     fmt = oracle_mod.encode(w, **kw)
     meta = {k: fmt[k] for k in ("num_elements", "T", "n", "B", "k", "lut_entry_bytes", "encoded_bits",
                                 "max_code_len")}
-    if kernel == "fast" and not _fast_ok(df11, meta):
+    if kernel.startswith("fast") and not _fast_ok(df11, meta):
         with pytest.raises(df11.Df11Error):
             _gpu_decode_arrays(df11, meta, fmt, kernel)
         return
