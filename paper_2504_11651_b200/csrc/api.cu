@@ -238,15 +238,16 @@ extern "C" df11_status df11_decompress_block_budget(const df11_device_tensor *ts
     int max_smem = 0, num_sms = 0;
     device_attrs(dev, max_smem, num_sms);
     if (nfast) {
-        // one product launch per (chunk size, value format, byte tables or not): each takes its own
-        // kernel build
-        uint32_t grp[16][DF11_MAX_BATCH], cnt[16] = {};
+        // one product launch per (chunk size, value format, byte tables or not, load-time decode tables
+        // or not): each takes its own kernel build
+        uint32_t grp[32][DF11_MAX_BATCH], cnt[32] = {};
         for (uint32_t k = 0; k < nfast; k++) {
             const df11_device_tensor &t = ts[fast_idx[k]];
-            const uint32_t key = (df11::lut_bits_of(t) == 8 ? 0u : 8u) + (t.n == 16 ? 4u : 0u) + t.value_format;
+            const uint32_t key = (t.decode_table ? 16u : 0u) + (df11::lut_bits_of(t) == 8 ? 0u : 8u) +
+                                 (t.n == 16 ? 4u : 0u) + t.value_format;
             grp[key][cnt[key]++] = fast_idx[k];
         }
-        for (uint32_t key = 0; key < 16; key++) {
+        for (uint32_t key = 0; key < 32; key++) {
             if (!cnt[key]) continue;
             df11_status st = launch_fast_batch(ts, grp[key], cnt[key], num_sms, dev, stream, max_ctas);
             if (st != DF11_OK) return st;

@@ -139,8 +139,9 @@ __device__ __forceinline__ uint32_t res_smem(uint32_t buf, uint32_t bit) {
 // bytes and a lane decodes its one 16-byte chunk as one chain in a 160-bit buffer.
 // kVF: value format (DF11_VF_*, NEXT-4).  Decode, scan and compaction are the same for every format
 // (the symbols are exponent fields); the merge composes the format's words.  kB8: the format's LUTs
-// are the paper's byte tables (b = 8); otherwise b-bit tables (App. I.2), walked in global memory.
-template <uint32_t kNB, uint32_t kVF, bool kB8>
+// are the paper's byte tables (b = 8); otherwise b-bit tables (App. I.2).  kPre: every tensor of the
+// launch carries a load-time decode table (df11_build_decode_table), loaded instead of built.
+template <uint32_t kNB, uint32_t kVF, bool kB8, bool kPre>
 __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__ Batch bt) {
     using L = Lay12<kVF>;
     constexpr VF kF = vf_of(kVF);
@@ -179,10 +180,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         mbar_init(mbar, 1);
         mbar_init(smbar, 1);
         sts32(mcnt, 0);
-        if (tid == 0) mbar_init(sbase + L::kTbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    uint32_t q = 0, parity = 0, qs = 0, tph = 0;
+    uint32_t q = 0, parity = 0, qs = 0;
 
     int ti_idx = tensor_of_tile(bt, c_begin);
     for (uint32_t seg_begin = c_begin; seg_begin < c_end; ti_idx++) {
@@ -206,12 +206,16 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             }
         }
         bool safe, lut_in_smem, long_codes;
-        if (ts.decode_table) {
+        if constexpr (kPre) {
             // the load-time table (df11_build_decode_table): one bulk copy of its SMEM image.  The
             // __syncthreads above orders every read of the previous table before the proxy fence and
             // the async-proxy write.
+            // The barrier is initialised afresh for every table (its phase is then always 0): the
+            // __syncthreads after the init makes it visible before anyone waits.
             const uint8_t *img = static_cast<const uint8_t *>(ts.decode_table);
             if (tid == 0) {
+                mbar_init(sbase + L::kTbar, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(sbase + L::kTbar, kOffGrp);
                 tma_g2s(sbase + kOffT, img, kOffGrp, sbase + L::kTbar);
@@ -220,8 +224,8 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             long_codes = (fl & 1u) != 0;
             safe = (fl & 2u) != 0;
             lut_in_smem = (fl & 4u) != 0;
-            mbar_wait(sbase + L::kTbar, tph);
-            tph ^= 1u;
+            __syncthreads();
+            mbar_wait(sbase + L::kTbar, 0u);
         } else {
             long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
                                                      kOffGrp + L::kGReg, tid, safe, lut_in_smem);
@@ -744,32 +748,32 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 #undef K_S24
 }
 
-uint32_t g_sp12_attr_set[64];   // bit (b8 ? 0 : 8) + (n16 ? 4 : 0) + vf: smem attribute set
+uint32_t g_sp12_attr_set[64];   // bit (pre ? 16 : 0) + (b8 ? 0 : 8) + (n16 ? 4 : 0) + vf: smem attribute set
 
-template <uint32_t kNB, uint32_t kVF, bool kB8>
+template <uint32_t kNB, uint32_t kVF, bool kB8, bool kPre>
 cudaError_t launch_one(const Batch &bt, int device, uint32_t grid, cudaStream_t stream) {
-    constexpr uint32_t bit = 1u << ((kB8 ? 0 : 8) + (kNB == 16 ? 4 : 0) + kVF);
+    constexpr uint32_t bit = 1u << ((kPre ? 16 : 0) + (kB8 ? 0 : 8) + (kNB == 16 ? 4 : 0) + kVF);
     if (device >= 0 && device < 64 && !(g_sp12_attr_set[device] & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(sp12_kernel<kNB, kVF, kB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)Lay12<kVF>::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(sp12_kernel<kNB, kVF, kB8, kPre>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay12<kVF>::kSmem);
         if (e != cudaSuccess) return e;
         g_sp12_attr_set[device] |= bit;
     }
-    sp12_kernel<kNB, kVF, kB8><<<grid, kCta12, Lay12<kVF>::kSmem, stream>>>(bt);
+    sp12_kernel<kNB, kVF, kB8, kPre><<<grid, kCta12, Lay12<kVF>::kSmem, stream>>>(bt);
     return cudaGetLastError();
 }
 
-template <bool kB8>
+template <bool kB8, bool kPre>
 cudaError_t launch_vf(const Batch &bt, int device, uint32_t grid, cudaStream_t stream, uint32_t key) {
     switch (key) {
-        case 0: return launch_one<8, DF11_VF_BF16, kB8>(bt, device, grid, stream);
-        case 1: return launch_one<8, DF11_VF_FP16, kB8>(bt, device, grid, stream);
-        case 2: return launch_one<8, DF11_VF_FP8_E4M3, kB8>(bt, device, grid, stream);
-        case 3: return launch_one<8, DF11_VF_FP8_E5M2, kB8>(bt, device, grid, stream);
-        case 4: return launch_one<16, DF11_VF_BF16, kB8>(bt, device, grid, stream);
-        case 5: return launch_one<16, DF11_VF_FP16, kB8>(bt, device, grid, stream);
-        case 6: return launch_one<16, DF11_VF_FP8_E4M3, kB8>(bt, device, grid, stream);
-        default: return launch_one<16, DF11_VF_FP8_E5M2, kB8>(bt, device, grid, stream);
+        case 0: return launch_one<8, DF11_VF_BF16, kB8, kPre>(bt, device, grid, stream);
+        case 1: return launch_one<8, DF11_VF_FP16, kB8, kPre>(bt, device, grid, stream);
+        case 2: return launch_one<8, DF11_VF_FP8_E4M3, kB8, kPre>(bt, device, grid, stream);
+        case 3: return launch_one<8, DF11_VF_FP8_E5M2, kB8, kPre>(bt, device, grid, stream);
+        case 4: return launch_one<16, DF11_VF_BF16, kB8, kPre>(bt, device, grid, stream);
+        case 5: return launch_one<16, DF11_VF_FP16, kB8, kPre>(bt, device, grid, stream);
+        case 6: return launch_one<16, DF11_VF_FP8_E4M3, kB8, kPre>(bt, device, grid, stream);
+        default: return launch_one<16, DF11_VF_FP8_E5M2, kB8, kPre>(bt, device, grid, stream);
     }
 }
 
@@ -835,8 +839,8 @@ bool fast_supports(const df11_device_tensor &t) {
            (reinterpret_cast<uintptr_t>(t.out) & (vf_of(t.value_format).word_bytes - 1)) == 0;
 }
 
-// Launch for a batch whose tensors share n (8 with T = 256, or 16 with T = 128), the value format and
-// whether their LUTs are the paper's byte tables.
+// Launch for a batch whose tensors share n (8 with T = 256, or 16 with T = 128), the value format,
+// whether their LUTs are the paper's byte tables, and whether they carry load-time decode tables.
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches) {
     if (bt.total_tiles == 0) return cudaSuccess;
     int num_sms = 0;
@@ -847,8 +851,9 @@ cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64
     const uint32_t grid = bt.grid ? bt.grid
                                   : min((uint32_t)num_sms, (bt.total_tiles + kGroups12 - 1) / kGroups12);
     const uint32_t key = vf + (n16 ? 4u : 0u);
-    e = lut_bits_of(bt.t[0]) == 8 ? launch_vf<true>(bt, device, grid, stream, key)
-                                  : launch_vf<false>(bt, device, grid, stream, key);
+    const bool b8 = lut_bits_of(bt.t[0]) == 8, pre = bt.t[0].decode_table != nullptr;
+    if (pre) e = b8 ? launch_vf<true, true>(bt, device, grid, stream, key) : launch_vf<false, true>(bt, device, grid, stream, key);
+    else e = b8 ? launch_vf<true, false>(bt, device, grid, stream, key) : launch_vf<false, false>(bt, device, grid, stream, key);
     if (e == cudaSuccess && launches) (*launches)++;
     return e;
 }
