@@ -46,8 +46,6 @@ def parse():
                         "the same N(0, 0.02) recipe (value = GB/s of decoded words out)")
     p.add_argument("--lut-bits", default="8",
                    help="b of the format's b-bit LUTs (App. I.2; 8 = the paper) or 'mono' (App. I.1, b = L)")
-    p.add_argument("--no-decode-table", action="store_true",
-                   help="do not build the load-time decode tables (df11_build_decode_table): every CTA builds them")
     p.add_argument("--dist", choices=["gauss", "t5", "sigma-lu"], default="gauss",
                    help="weight distribution: gauss = the headline recipe; t5 / sigma-lu = realism variants")
     p.add_argument("--no-e2e", action="store_true")
@@ -344,7 +342,7 @@ def main():
         outs.append(scratch[o:o + h.num_elements])
         o += (h.num_elements + upv - 1) // upv * upv                       # keep views 16-byte aligned
     assert o <= scratch.numel()
-    dts = [df11.to_device(h, dev, decode_table=not args.no_decode_table) for h in hs]
+    dts = [df11.to_device(h, dev) for h in hs]
     plan = df11.BlockPlan(dts, outs)
     kernel_used = args.kernel
     if args.kernel == "auto":
@@ -454,8 +452,6 @@ def main():
                        "df11_bytes_per_gpu": algo_bytes - bf16_bytes,
                        "bits_per_weight": 8 * (algo_bytes - bf16_bytes) / N, "T": hs[0].T, "n": hs[0].n,
                        "format": args.format, "value_format": args.vf, "lut_bits": hs[0].lut_bits,
-                       "decode_table": "built once per tensor at load (df11_build_decode_table)"
-                       if not args.no_decode_table else "built by every CTA in the kernel",
                        "kernel": kernel_used, "parallelism": f"shard{world} (one block per GPU, no collective)",
                        "bf16_bytes_all_ranks_per_step": tot_bf16, "l2": l2_note, "l2_copies": copies},
             "roofline": roofline,
@@ -663,8 +659,7 @@ def run_e2e(df11, hs, dts, dev, steps, barrier, tensors, vf="bf16"):
     import ctypes
     n = len(hs)
     H = (df11.HostTensorC * n)(*host_views)
-    # (the host path re-uploads the arrays every step: the load-time decode table is not used)
-    D = (df11.DeviceTensorC * n)(*[dt.without_decode_table().descriptor() for dt in dts])
+    D = (df11.DeviceTensorC * n)(*[dt.descriptor() for dt in dts])
     O = (ctypes.c_void_p * n)(*[ho.data_ptr() for ho in host_outs])
     copy_stream = torch.cuda.Stream()
 

@@ -99,7 +99,6 @@ typedef struct {
     const uint8_t  *code_lengths;
     const uint32_t *block_output_pos;
     void           *out;
-    const void     *decode_table;          /* optional (NULL = built by each CTA): see df11_build_decode_table */
     uint64_t        num_elements;
     uint32_t        T, n, B, k, lut_entry_bytes;
     uint32_t        value_format;          /* DF11_VF_* (0 = BF16) */
@@ -145,19 +144,6 @@ df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t coun
 df11_status df11_decompress_block_budget(const df11_device_tensor *ts, uint32_t count, void *stream,
                                          int kernel, uint32_t max_ctas);
 
-/* ---- load-time decode table (product kernel) ----------------------------------------------------
- * The product kernel decodes through a 12-bit multi-code table derived from a tensor's CodeLengths and
- * LUTs.  Without help every persistent CTA builds it in SMEM at kernel start and at
- * every tensor switch (~5 us).  df11_build_decode_table builds it ONCE per tensor (e.g. when the model
- * is loaded; one small kernel on `stream`) into `table`: DF11_DECODE_TABLE_BYTES of caller-owned,
- * 16-byte aligned device memory.  Setting t->decode_table = table afterwards makes the product kernel
- * load it with one bulk copy instead of building it; the result is identical.  The table depends only
- * on the codebook (CodeLengths, LUTs, value format, b): it is derived data, like the LUTs.  Its
- * contents are trusted: it must come from this call on the same tensor's metadata.
- * Errors: as the decode calls (validation of *t), DF11_E_CUDA. */
-#define DF11_DECODE_TABLE_BYTES 41616u
-df11_status df11_build_decode_table(const df11_device_tensor *t, void *table, void *stream);
-
 /* ---- launcher planning (host; used by df11_decompress_block, exported for tests) ----------------
  * df11_plan_cta_ranges: tile ranges of the persistent decode grid.  entry_start[0..count] are the
  * exclusive prefix sums of the batch entries' format-block counts (entry_start[count] = total);
@@ -171,7 +157,7 @@ void df11_plan_cta_ranges(const uint32_t *entry_start, uint32_t count, uint32_t 
  * df11_decompress_host: copies the host arrays of `h` into the caller-provided device staging
  * buffers described by `d` (same sizes as h's arrays), decodes into d->out and copies the result
  * into `host_out` (N words of the value format; pinned memory recommended; NULL = leave the result in
- * d->out), all enqueued on `stream`.  d->decode_table is ignored (the staging buffers get new contents).
+ * d->out), all enqueued on `stream`.
  * Returns after enqueueing; synchronise the stream before reading host_out. */
 df11_status df11_decompress_host(const df11_host_tensor *h, const df11_device_tensor *d,
                                  void *host_out, void *stream);

@@ -18,7 +18,6 @@ namespace df11 {
 cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 bool fast_supports(const df11_device_tensor &t);
-cudaError_t build_decode_table(const df11_device_tensor &t, void *table, cudaStream_t stream);
 uint32_t fast_grid(uint32_t total_tiles, int num_sms);
 }  // namespace df11
 
@@ -76,7 +75,6 @@ df11_status validate(const df11_device_tensor &t, uint32_t idx) {
     if (!t.encoded_exponent || !t.packed_sign_mantissa || !t.gaps || !t.luts || !t.code_lengths ||
         !t.block_output_pos || !t.out)
         return bad("NULL device pointer");
-    if (reinterpret_cast<uintptr_t>(t.decode_table) & 15) return bad("decode_table must be 16-byte aligned");
     return DF11_OK;
 }
 }  // namespace
@@ -238,37 +236,21 @@ extern "C" df11_status df11_decompress_block_budget(const df11_device_tensor *ts
     int max_smem = 0, num_sms = 0;
     device_attrs(dev, max_smem, num_sms);
     if (nfast) {
-        // one product launch per (chunk size, value format, byte tables or not, load-time decode tables
-        // or not): each takes its own kernel build
-        uint32_t grp[32][DF11_MAX_BATCH], cnt[32] = {};
+        // one product launch per (chunk size, value format, byte tables or not): each takes its own
+        // kernel build
+        uint32_t grp[16][DF11_MAX_BATCH], cnt[16] = {};
         for (uint32_t k = 0; k < nfast; k++) {
             const df11_device_tensor &t = ts[fast_idx[k]];
-            const uint32_t key = (t.decode_table ? 16u : 0u) + (df11::lut_bits_of(t) == 8 ? 0u : 8u) +
-                                 (t.n == 16 ? 4u : 0u) + t.value_format;
+            const uint32_t key = (df11::lut_bits_of(t) == 8 ? 0u : 8u) + (t.n == 16 ? 4u : 0u) + t.value_format;
             grp[key][cnt[key]++] = fast_idx[k];
         }
-        for (uint32_t key = 0; key < 32; key++) {
+        for (uint32_t key = 0; key < 16; key++) {
             if (!cnt[key]) continue;
             df11_status st = launch_fast_batch(ts, grp[key], cnt[key], num_sms, dev, stream, max_ctas);
             if (st != DF11_OK) return st;
         }
     }
     if (nslow) return launch_alg1_batch(ts, slow_idx, nslow, (size_t)max_smem, stream);
-    return DF11_OK;
-}
-
-extern "C" df11_status df11_build_decode_table(const df11_device_tensor *t, void *table, void *stream) {
-    if (!t || !table) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL argument");
-    if (reinterpret_cast<uintptr_t>(table) & 15) return df11_fail(DF11_E_INVALID_ARGUMENT, "table not 16-byte aligned");
-    df11_device_tensor d = *t;
-    d.decode_table = nullptr;
-    df11_status st = validate(d, 0);
-    if (st != DF11_OK) return st;
-    if (!d.luts || !d.code_lengths) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL LUTs / CodeLengths");
-    if (!d.num_elements) return DF11_OK;                         // nothing to decode: no table needed
-    cudaError_t e = df11::build_decode_table(d, table, (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_fail(e, "decode table build");
-    g_launches++;
     return DF11_OK;
 }
 
@@ -308,10 +290,7 @@ extern "C" df11_status df11_decompress_host(const df11_host_tensor *h, const df1
         cudaError_t e = cudaMemcpyAsync(c.dst, c.src, c.n, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
     }
-    // the staging buffers now hold h's arrays: a load-time table built for earlier contents may be stale
-    df11_device_tensor dd = *d;
-    dd.decode_table = nullptr;
-    df11_status st = df11_decompress(&dd, stream_v);
+    df11_status st = df11_decompress(d, stream_v);
     if (st != DF11_OK) return st;
     if (!host_out) return DF11_OK;                   // decode only: the result stays in d->out
     const uint64_t out_bytes = (uint64_t)df11::vf_of(h->value_format).word_bytes * h->num_elements;

@@ -57,9 +57,6 @@ constexpr uint32_t kOffLut = kOffT + kT12Bytes;
 constexpr uint32_t kOffLen = kOffLut + kLutSmem;                    // CodeLengths[e]
 constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengths[stored symbol]
 constexpr uint32_t kOffGrp = kOffRLen + 256;                        // [groups][kGrpBytes]
-// df11_build_decode_table: the SMEM image [0, kOffGrp) (T12 | LUTs | CodeLengths | by stored symbol)
-// followed by a flags word (bit 0: long codes, bit 1: a 1-bit code, bit 2: LUTs staged in SMEM)
-static_assert(DF11_DECODE_TABLE_BYTES == kOffGrp + 16, "decode table size");
 // PackedSignMantissa bytes of one tile staged in SMEM: BF16 ~6.3 KB per tile on LLM weights; FP16
 // (11-bit residuals, NEXT-4) ~8.7 KB: it takes the SMEM left over (tiles above the cap read their
 // residuals through L1/L2 instead)
@@ -76,8 +73,7 @@ struct Lay12 {
     static constexpr uint32_t kGCnt = kGWsum + 2 * kWarps12 * 4;    // warps done with the merge
     static constexpr uint32_t kGMbar = kGCnt + 16;                  // [stage, sign/mantissa] mbarriers
     static constexpr uint32_t kGrpBytes = kGMbar + 16;
-    static constexpr uint32_t kTbar = kOffGrp + kGroups12 * kGrpBytes;   // load-time table landed
-    static constexpr uint32_t kSmem = kTbar + 16;
+    static constexpr uint32_t kSmem = kOffGrp + kGroups12 * kGrpBytes;
     static_assert(kOffGrp % 16 == 0 && kGSm % 16 == 0 && kGReg % 16 == 0 && kWarpReg12 % 16 == 0 &&
                       kGWsum % 16 == 0 && kGMbar % 8 == 0 && kGrpBytes % 16 == 0,
                   "alignment");
@@ -139,9 +135,8 @@ __device__ __forceinline__ uint32_t res_smem(uint32_t buf, uint32_t bit) {
 // bytes and a lane decodes its one 16-byte chunk as one chain in a 160-bit buffer.
 // kVF: value format (DF11_VF_*, NEXT-4).  Decode, scan and compaction are the same for every format
 // (the symbols are exponent fields); the merge composes the format's words.  kB8: the format's LUTs
-// are the paper's byte tables (b = 8); otherwise b-bit tables (App. I.2).  kPre: every tensor of the
-// launch carries a load-time decode table (df11_build_decode_table), loaded instead of built.
-template <uint32_t kNB, uint32_t kVF, bool kB8, bool kPre>
+// are the paper's byte tables (b = 8); otherwise b-bit tables (App. I.2), walked in global memory.
+template <uint32_t kNB, uint32_t kVF, bool kB8>
 __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__ Batch bt) {
     using L = Lay12<kVF>;
     constexpr VF kF = vf_of(kVF);
@@ -205,31 +200,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 else issue_tile16(ts, tile - base_tile, stage, mbar);
             }
         }
-        bool safe, lut_in_smem, long_codes;
-        if constexpr (kPre) {
-            // the load-time table (df11_build_decode_table): one bulk copy of its SMEM image.  The
-            // __syncthreads above orders every read of the previous table before the proxy fence and
-            // the async-proxy write.
-            // The barrier is initialised afresh for every table (its phase is then always 0): the
-            // __syncthreads after the init makes it visible before anyone waits.
-            const uint8_t *img = static_cast<const uint8_t *>(ts.decode_table);
-            if (tid == 0) {
-                mbar_init(sbase + L::kTbar, 1);
-                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(sbase + L::kTbar, kOffGrp);
-                tma_g2s(sbase + kOffT, img, kOffGrp, sbase + L::kTbar);
-            }
-            const uint32_t fl = __ldg(reinterpret_cast<const uint32_t *>(img + kOffGrp));
-            long_codes = (fl & 1u) != 0;
-            safe = (fl & 2u) != 0;
-            lut_in_smem = (fl & 4u) != 0;
-            __syncthreads();
-            mbar_wait(sbase + L::kTbar, 0u);
-        } else {
-            long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
-                                                     kOffGrp + L::kGReg, tid, safe, lut_in_smem);
-        }
+        bool safe, lut_in_smem;
+        const bool long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
+                                                       kOffGrp + L::kGReg, tid, safe, lut_in_smem);
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
 
         const uint32_t N = (uint32_t)ts.num_elements;
@@ -748,80 +721,36 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 #undef K_S24
 }
 
-uint32_t g_sp12_attr_set[64];   // bit (pre ? 16 : 0) + (b8 ? 0 : 8) + (n16 ? 4 : 0) + vf: smem attribute set
+uint32_t g_sp12_attr_set[64];   // bit (b8 ? 0 : 8) + (n16 ? 4 : 0) + vf: smem attribute set
 
-template <uint32_t kNB, uint32_t kVF, bool kB8, bool kPre>
+template <uint32_t kNB, uint32_t kVF, bool kB8>
 cudaError_t launch_one(const Batch &bt, int device, uint32_t grid, cudaStream_t stream) {
-    constexpr uint32_t bit = 1u << ((kPre ? 16 : 0) + (kB8 ? 0 : 8) + (kNB == 16 ? 4 : 0) + kVF);
+    constexpr uint32_t bit = 1u << ((kB8 ? 0 : 8) + (kNB == 16 ? 4 : 0) + kVF);
     if (device >= 0 && device < 64 && !(g_sp12_attr_set[device] & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(sp12_kernel<kNB, kVF, kB8, kPre>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay12<kVF>::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(sp12_kernel<kNB, kVF, kB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)Lay12<kVF>::kSmem);
         if (e != cudaSuccess) return e;
         g_sp12_attr_set[device] |= bit;
     }
-    sp12_kernel<kNB, kVF, kB8, kPre><<<grid, kCta12, Lay12<kVF>::kSmem, stream>>>(bt);
+    sp12_kernel<kNB, kVF, kB8><<<grid, kCta12, Lay12<kVF>::kSmem, stream>>>(bt);
     return cudaGetLastError();
 }
 
-template <bool kB8, bool kPre>
+template <bool kB8>
 cudaError_t launch_vf(const Batch &bt, int device, uint32_t grid, cudaStream_t stream, uint32_t key) {
     switch (key) {
-        case 0: return launch_one<8, DF11_VF_BF16, kB8, kPre>(bt, device, grid, stream);
-        case 1: return launch_one<8, DF11_VF_FP16, kB8, kPre>(bt, device, grid, stream);
-        case 2: return launch_one<8, DF11_VF_FP8_E4M3, kB8, kPre>(bt, device, grid, stream);
-        case 3: return launch_one<8, DF11_VF_FP8_E5M2, kB8, kPre>(bt, device, grid, stream);
-        case 4: return launch_one<16, DF11_VF_BF16, kB8, kPre>(bt, device, grid, stream);
-        case 5: return launch_one<16, DF11_VF_FP16, kB8, kPre>(bt, device, grid, stream);
-        case 6: return launch_one<16, DF11_VF_FP8_E4M3, kB8, kPre>(bt, device, grid, stream);
-        default: return launch_one<16, DF11_VF_FP8_E5M2, kB8, kPre>(bt, device, grid, stream);
+        case 0: return launch_one<8, DF11_VF_BF16, kB8>(bt, device, grid, stream);
+        case 1: return launch_one<8, DF11_VF_FP16, kB8>(bt, device, grid, stream);
+        case 2: return launch_one<8, DF11_VF_FP8_E4M3, kB8>(bt, device, grid, stream);
+        case 3: return launch_one<8, DF11_VF_FP8_E5M2, kB8>(bt, device, grid, stream);
+        case 4: return launch_one<16, DF11_VF_BF16, kB8>(bt, device, grid, stream);
+        case 5: return launch_one<16, DF11_VF_FP16, kB8>(bt, device, grid, stream);
+        case 6: return launch_one<16, DF11_VF_FP8_E4M3, kB8>(bt, device, grid, stream);
+        default: return launch_one<16, DF11_VF_FP8_E5M2, kB8>(bt, device, grid, stream);
     }
-}
-
-// df11_build_decode_table: one CTA builds the tensor's table in SMEM (the same build_t12 as the product
-// kernel) and writes the SMEM image + flags to global memory.
-template <uint32_t kVF, bool kB8>
-__global__ void __launch_bounds__(kCta12, 1) t12_export_kernel(const __grid_constant__ df11_device_tensor ts,
-                                                               uint8_t *__restrict__ table) {
-    uint8_t *sb = smem_b();
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_w);
-    const uint32_t tid = threadIdx.x;
-    bool safe, lut_in_smem;
-    const bool long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
-                                                        kOffGrp, tid, safe, lut_in_smem);
-    __syncthreads();
-    for (uint32_t i = tid; i < kOffGrp / 16; i += kCta12)
-        reinterpret_cast<uint4 *>(table)[i] = reinterpret_cast<const uint4 *>(sb)[i];
-    if (tid == 0)
-        *reinterpret_cast<uint4 *>(table + kOffGrp) =
-            make_uint4((long_codes ? 1u : 0u) | (safe ? 2u : 0u) | (lut_in_smem ? 4u : 0u), 0u, 0u, 0u);
-}
-
-template <uint32_t kVF, bool kB8>
-cudaError_t launch_export(const df11_device_tensor &t, uint8_t *table, cudaStream_t stream) {
-    constexpr uint32_t smem = kOffGrp + 8192;                      // image + first-code scratch
-    cudaError_t e = cudaFuncSetAttribute(t12_export_kernel<kVF, kB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    t12_export_kernel<kVF, kB8><<<1, kCta12, smem, stream>>>(t, table);
-    return cudaGetLastError();
 }
 
 }  // namespace
-
-cudaError_t build_decode_table(const df11_device_tensor &t, void *table, cudaStream_t stream) {
-    uint8_t *p = static_cast<uint8_t *>(table);
-    const bool b8 = lut_bits_of(t) == 8;
-    switch (t.value_format) {
-        case DF11_VF_FP16: return b8 ? launch_export<DF11_VF_FP16, true>(t, p, stream)
-                                     : launch_export<DF11_VF_FP16, false>(t, p, stream);
-        case DF11_VF_FP8_E4M3: return b8 ? launch_export<DF11_VF_FP8_E4M3, true>(t, p, stream)
-                                         : launch_export<DF11_VF_FP8_E4M3, false>(t, p, stream);
-        case DF11_VF_FP8_E5M2: return b8 ? launch_export<DF11_VF_FP8_E5M2, true>(t, p, stream)
-                                         : launch_export<DF11_VF_FP8_E5M2, false>(t, p, stream);
-        default: return b8 ? launch_export<DF11_VF_BF16, true>(t, p, stream)
-                           : launch_export<DF11_VF_BF16, false>(t, p, stream);
-    }
-}
 
 uint32_t fast_grid(uint32_t total_tiles, int num_sms) {
     return min((uint32_t)num_sms, (total_tiles + kGroups12 - 1) / kGroups12);
@@ -839,8 +768,8 @@ bool fast_supports(const df11_device_tensor &t) {
            (reinterpret_cast<uintptr_t>(t.out) & (vf_of(t.value_format).word_bytes - 1)) == 0;
 }
 
-// Launch for a batch whose tensors share n (8 with T = 256, or 16 with T = 128), the value format,
-// whether their LUTs are the paper's byte tables, and whether they carry load-time decode tables.
+// Launch for a batch whose tensors share n (8 with T = 256, or 16 with T = 128), the value format and
+// whether their LUTs are the paper's byte tables.
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches) {
     if (bt.total_tiles == 0) return cudaSuccess;
     int num_sms = 0;
@@ -851,9 +780,8 @@ cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64
     const uint32_t grid = bt.grid ? bt.grid
                                   : min((uint32_t)num_sms, (bt.total_tiles + kGroups12 - 1) / kGroups12);
     const uint32_t key = vf + (n16 ? 4u : 0u);
-    const bool b8 = lut_bits_of(bt.t[0]) == 8, pre = bt.t[0].decode_table != nullptr;
-    if (pre) e = b8 ? launch_vf<true, true>(bt, device, grid, stream, key) : launch_vf<false, true>(bt, device, grid, stream, key);
-    else e = b8 ? launch_vf<true, false>(bt, device, grid, stream, key) : launch_vf<false, false>(bt, device, grid, stream, key);
+    e = lut_bits_of(bt.t[0]) == 8 ? launch_vf<true>(bt, device, grid, stream, key)
+                                  : launch_vf<false>(bt, device, grid, stream, key);
     if (e == cudaSuccess && launches) (*launches)++;
     return e;
 }

@@ -32,8 +32,7 @@ EXPORTED_SYMBOLS = ("df11_encode", "df11_encode_group", "df11_host_tensor_free",
                     "df11_decompress_host",
                     "df11_decompress_host_block", "df11_plan_cta_ranges", "df11_status_string", "df11_last_cuda_error", "df11_last_error_message", "df11_version",
                     "df11_launch_count", "df11_last_kernel_mask", "df11_histogram_device", "df11_encode_plan_create",
-                    "df11_encode_plan_free", "df11_encode_device", "df11_build_decode_table")
-DECODE_TABLE_BYTES = 41616
+                    "df11_encode_plan_free", "df11_encode_device")
 
 
 class Df11Error(RuntimeError):
@@ -66,7 +65,7 @@ class HostTensorC(ctypes.Structure):
 class DeviceTensorC(ctypes.Structure):
     _fields_ = [("encoded_exponent", ctypes.c_void_p), ("packed_sign_mantissa", ctypes.c_void_p),
                 ("gaps", ctypes.c_void_p), ("luts", ctypes.c_void_p), ("code_lengths", ctypes.c_void_p),
-                ("block_output_pos", ctypes.c_void_p), ("out", ctypes.c_void_p), ("decode_table", ctypes.c_void_p),
+                ("block_output_pos", ctypes.c_void_p), ("out", ctypes.c_void_p),
                 ("num_elements", ctypes.c_uint64), ("T", ctypes.c_uint32), ("n", ctypes.c_uint32),
                 ("B", ctypes.c_uint32), ("k", ctypes.c_uint32), ("lut_entry_bytes", ctypes.c_uint32),
                 ("value_format", ctypes.c_uint32), ("lut_bits", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
@@ -116,12 +115,11 @@ def lib():
         L.df11_encode_plan_create.argtypes = [P, P, ctypes.POINTER(EncodeOpts), ctypes.POINTER(EncodePlanC)]
         L.df11_encode_plan_free.argtypes = [ctypes.POINTER(EncodePlanC)]
         L.df11_encode_device.argtypes = [P, ctypes.POINTER(EncodePlanC), ctypes.POINTER(DeviceBuffersC), P, U64, P]
-        L.df11_build_decode_table.argtypes = [ctypes.POINTER(DeviceTensorC), P, P]
         for f in ("df11_encode", "df11_encode_group", "df11_decompress", "df11_decompress_block",
                   "df11_decompress_block_ex", "df11_decompress_block_budget", "df11_decompress_host",
                   "df11_decompress_host_block",
                   "df11_histogram_device",
-                  "df11_encode_plan_create", "df11_encode_device", "df11_build_decode_table"):
+                  "df11_encode_plan_create", "df11_encode_device"):
             getattr(L, f).restype = ctypes.c_int
         L.df11_status_string.argtypes = [ctypes.c_int]
         L.df11_status_string.restype = ctypes.c_char_p
@@ -290,21 +288,18 @@ def encode_group(ws, T: int = 256, n: int = 8, lut_mode: str = "auto", shared_co
 class DeviceTensor:
     """Device-resident DF11 tensor: torch uint8/int32 buffers + the C descriptor pointing at them."""
 
-    def __init__(self, h: HostTensor, device="cuda", out=None, decode_table: bool = True):
-        self._want_table = decode_table
+    def __init__(self, h: HostTensor, device="cuda", out=None):
         m = dict(num_elements=h.num_elements, T=h.T, n=h.n, B=h.B, k=h.k, lut_entry_bytes=h.lut_entry_bytes,
                  encoded_bits=h.encoded_bits, max_code_len=h.max_code_len, value_format=h.value_format,
                  lut_bits=h.lut_bits)
         self._init(m, h.arrays(), h.shape, device, out)
 
     @classmethod
-    def from_arrays(cls, meta: dict, arrays: dict, shape=None, device="cuda", out=None,
-                    decode_table: bool = True) -> "DeviceTensor":
+    def from_arrays(cls, meta: dict, arrays: dict, shape=None, device="cuda", out=None) -> "DeviceTensor":
         """Upload DF11 arrays given as numpy (e.g. read from disk): keys code_lengths, luts,
         encoded_exponent, packed_sign_mantissa, gaps, block_output_pos; meta: num_elements, T, n, B, k,
         lut_entry_bytes, encoded_bits, max_code_len (+ value_format, lut_bits; default BF16, 8)."""
         self = cls.__new__(cls)
-        self._want_table = decode_table
         self._init(meta, arrays, shape if shape is not None else (int(meta["num_elements"]),), device, out)
         return self
 
@@ -336,39 +331,17 @@ class DeviceTensor:
         self.block_output_pos = up(np.asarray(a["block_output_pos"], np.uint32).view(np.uint8))
         self.out = out if out is not None else torch.empty(max(self.num_elements, 1), dtype=out_dtype(self.vf),
                                                            device=dev)
-        self.decode_table = None
-        if getattr(self, "_want_table", True):
-            self.build_decode_table()
-
-    def build_decode_table(self, stream=None):
-        """df11_build_decode_table: the product kernel's decode table, built once (load time) into a
-        DECODE_TABLE_BYTES device buffer; later decodes load it instead of building it per CTA."""
-        import torch
-        t = torch.empty(DECODE_TABLE_BYTES, dtype=torch.uint8, device=self.encoded_exponent.device)
-        d = self.descriptor()
-        _check(lib().df11_build_decode_table(ctypes.byref(d), ctypes.c_void_p(t.data_ptr()), _stream_ptr(stream)))
-        self.decode_table = t
-        return t
 
     def descriptor(self, out=None) -> DeviceTensorC:
         o = self.out if out is None else out
         if o.numel() < self.num_elements or o.element_size() != VALUE_FORMATS[self.vf][1]:
             raise ValueError(f"output buffer too small or not {VALUE_FORMATS[self.vf][1]}-byte words")
         m = self.meta
-        table = getattr(self, "decode_table", None)
         return DeviceTensorC(self.encoded_exponent.data_ptr(), self.packed_sign_mantissa.data_ptr(),
                              self.gaps.data_ptr(), self.luts.data_ptr(), self.code_lengths.data_ptr(),
-                             self.block_output_pos.data_ptr(), o.data_ptr(),
-                             table.data_ptr() if table is not None else None, self.num_elements,
+                             self.block_output_pos.data_ptr(), o.data_ptr(), self.num_elements,
                              m["T"], m["n"], m["B"], m["k"], m["lut_entry_bytes"], m["value_format"],
                              m["lut_bits"], 0)
-
-    def without_decode_table(self) -> "DeviceTensor":
-        """A view of this tensor whose descriptor has no load-time table (each CTA builds it)."""
-        c = DeviceTensor.__new__(DeviceTensor)
-        c.__dict__.update(self.__dict__)
-        c.decode_table = None
-        return c
 
     def staging_bytes(self) -> int:
         return sum(int(t.numel()) for t in (self.encoded_exponent, self.packed_sign_mantissa, self.gaps,
@@ -382,7 +355,6 @@ def clone_device_tensor(d: "DeviceTensor", out=None) -> "DeviceTensor":
     c.__dict__.update(d.__dict__)
     for key in ("encoded_exponent", "packed_sign_mantissa", "gaps", "luts", "code_lengths", "block_output_pos"):
         setattr(c, key, getattr(d, key).clone())
-    c.decode_table = d.decode_table.clone() if getattr(d, "decode_table", None) is not None else None
     c.out = out if out is not None else d.out.clone()
     return c
 
@@ -399,8 +371,8 @@ def out_dtype(vf: str):
             "fp8_e5m2": torch.float8_e5m2}[vf]
 
 
-def to_device(h: HostTensor, device="cuda", out=None, decode_table: bool = True) -> DeviceTensor:
-    return DeviceTensor(h, device, out, decode_table)
+def to_device(h: HostTensor, device="cuda", out=None) -> DeviceTensor:
+    return DeviceTensor(h, device, out)
 
 
 def _stream_ptr(stream):
@@ -595,8 +567,6 @@ def _encode_device_with_plan(x, plan, stream, out):
                                     ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
                                     _stream_ptr(stream)))
     dt._workspace = ws     # keep alive until the stream has consumed it
-    dt.decode_table = None
-    dt.build_decode_table(stream)
     return dt
 
 

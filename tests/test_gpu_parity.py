@@ -12,7 +12,7 @@ import workloads
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-KERNELS = ["alg1", "fast", "fast_notable"]   # fast_notable: no load-time decode table (built per CTA)
+KERNELS = ["alg1", "fast"]
 
 
 @pytest.fixture(scope="module")
@@ -28,15 +28,8 @@ def _fast_ok(df11, meta):
     return (meta["T"], meta["n"]) in ((256, 8), (128, 16))
 
 
-def _kname(kernel):
-    return "fast" if kernel == "fast_notable" else kernel
-
-
 def _gpu_decode_arrays(df11, meta, arrays, kernel, shape=None):
-    dt = df11.DeviceTensor.from_arrays(meta, arrays, shape=shape, decode_table=kernel != "fast_notable")
-    if kernel == "fast_notable":
-        assert dt.decode_table is None
-        kernel = "fast"
+    dt = df11.DeviceTensor.from_arrays(meta, arrays, shape=shape)
     out = df11.decompress(dt, kernel=kernel)
     torch.cuda.synchronize()
     return out.view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1)
@@ -47,7 +40,7 @@ def _check_oracle_format(df11, oracle_mod, w, kernel, **kw):
     fmt = oracle_mod.encode(w, **kw)
     meta = {k: fmt[k] for k in ("num_elements", "T", "n", "B", "k", "lut_entry_bytes", "encoded_bits",
                                 "max_code_len")}
-    if kernel.startswith("fast") and not _fast_ok(df11, meta):
+    if kernel == "fast" and not _fast_ok(df11, meta):
         with pytest.raises(df11.Df11Error):
             _gpu_decode_arrays(df11, meta, fmt, kernel)
         return
@@ -171,9 +164,9 @@ def test_block_batch_flux_single(df11, oracle_mod, kernel):
     tiny tensors, ragged sizes, different codebooks per tensor."""
     ts = workloads.config_tensors("flux_single_block")
     hs = [df11.encode(w) for _, w in ts]
-    dts = [df11.to_device(h, decode_table=kernel != "fast_notable") for h in hs]
+    dts = [df11.to_device(h) for h in hs]
     before = df11.launch_count()
-    outs = df11.decompress_block(dts, kernel=_kname(kernel))
+    outs = df11.decompress_block(dts, kernel=kernel)
     torch.cuda.synchronize()
     assert df11.launch_count() - before == 1
     for (name, w), o in zip(ts, outs):
@@ -250,8 +243,8 @@ def test_full_size_llama8b_block(df11, oracle_mod, kernel):
     largest tensor; sampled format blocks == oracle D2 (Alg. 1 emulator)."""
     ts = workloads.config_tensors("llama8b_block")
     hs = [df11.encode(w) for _, w in ts]
-    dts = [df11.to_device(h, decode_table=kernel != "fast_notable") for h in hs]
-    outs = df11.decompress_block(dts, kernel=_kname(kernel))
+    dts = [df11.to_device(h) for h in hs]
+    outs = df11.decompress_block(dts, kernel=kernel)
     torch.cuda.synchronize()
     for (name, w), o, h in zip(ts, outs, hs):
         got = o.view(torch.int16).cpu().numpy().view(np.uint16)

@@ -38,8 +38,7 @@ def _words(out, vf):
 
 
 def _decode(df11, fmt, kernel):
-    dt = df11.DeviceTensor.from_arrays(_meta(fmt), fmt, decode_table=kernel != "fast_notable")
-    kernel = "fast" if kernel == "fast_notable" else kernel
+    dt = df11.DeviceTensor.from_arrays(_meta(fmt), fmt)
     out = df11.decompress(dt, kernel=kernel)
     torch.cuda.synchronize()
     assert df11.last_kernels() == {kernel}
@@ -89,7 +88,7 @@ CASES = ["gauss", "gauss_1m", "patterns", "tiny", "one", "constant_1bit", "one_b
          "escapes"]
 
 
-@pytest.mark.parametrize("kernel", ["alg1", "fast", "fast_notable"])
+@pytest.mark.parametrize("kernel", ["alg1", "fast"])
 @pytest.mark.parametrize("vf", VFS)
 @pytest.mark.parametrize("case", CASES)
 def test_value_format_parity(df11, oracle_mod, case, vf, kernel):
@@ -103,7 +102,7 @@ def test_value_format_n16(df11, oracle_mod, vf):
         _check(df11, oracle_mod, _weights(case, vf), vf, "fast", T=128, n=16)
 
 
-@pytest.mark.parametrize("kernel", ["alg1", "fast", "fast_notable"])
+@pytest.mark.parametrize("kernel", ["alg1", "fast"])
 @pytest.mark.parametrize("lut_bits", [1, 2, 5, 7, 8, 11, 12, 16, "mono"])
 def test_lut_bits_parity(df11, oracle_mod, lut_bits, kernel):
     """b-bit tables: decode through them (Alg. 1 walks them for every code; the product kernel builds
@@ -167,23 +166,3 @@ def test_value_format_host_path(df11):
         df11.decompress_host(h, dt, host)
         torch.cuda.synchronize()
         assert np.array_equal(_words(host, vf), w)
-
-
-def test_decode_table_is_deterministic_and_optional(df11):
-    """df11_build_decode_table: the same table bytes on every build, and the product kernel's output is
-    identical with the load-time table, without it, and with a table built on a side stream."""
-    w = workloads.gaussian_bf16((3, 70001), seed=61)
-    h = df11.encode(w)
-    dt = df11.to_device(h)
-    t1 = dt.decode_table.clone()
-    s = torch.cuda.Stream()
-    dt.build_decode_table(stream=s)
-    s.synchronize()
-    assert torch.equal(t1, dt.decode_table)
-    a = _words(df11.decompress(dt, kernel="fast").clone(), "bf16")
-    b = _words(df11.decompress(dt.without_decode_table(), kernel="fast").clone(), "bf16")
-    assert np.array_equal(a, w.reshape(-1)) and np.array_equal(b, a)
-    with pytest.raises(df11.Df11Error):                   # a misaligned table is rejected
-        d = dt.descriptor()
-        d.decode_table = dt.decode_table.data_ptr() + 8
-        df11._check(df11.lib().df11_decompress_block(__import__("ctypes").byref(d), 1, None))
