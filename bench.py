@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--dist", choices=["gauss", "t5", "sigma-lu"], default="gauss",
                    help="weight distribution: gauss = the headline recipe; t5 / sigma-lu = realism variants")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true",
+                   help="skip the extra CUDA-graph replay of the same K steps (reported as 'graph')")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-transfer", action="store_true", help="skip the CPU->GPU transfer baseline (NEXT-2)")
@@ -425,6 +427,30 @@ def main():
                 "note": "achieved = (DF11 bytes read + BF16 bytes written) / mean launch time (CUDA events); "
                         "launch_us: this rank's per-launch CUDA-event times"}
 
+    # ---- the same K steps captured in ONE CUDA graph and replayed (the C ABI is graph-capturable): the
+    # launch gaps between steps disappear; reported beside the eager headline, not instead of it
+    graph = None
+    if not args.no_graph:
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            for i in range(args.steps):
+                plans[(args.warmup + i) % copies].run(gs, kernel_used)
+        g.replay()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ga.record(gs)
+        g.replay()
+        gb.record(gs)
+        torch.cuda.synchronize()
+        gval, _, gms = shard.aggregate_rate(bf16_bytes, ga.elapsed_time(gb), args.steps)
+        graph = {"value": gval, "unit": UNIT, "ms_per_step": gms / args.steps,
+                 "what": "the same K block decodes captured in one CUDA graph and replayed (no launch gaps)"}
+        del g
+
     # ---- e2e: through the C ABI with host buffers (pinned H2D of the DF11 arrays, decode, D2H of BF16)
     e2e = None
     if not args.no_e2e:
@@ -457,6 +483,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "graph": graph,
             "transfer_baseline": transfer,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
