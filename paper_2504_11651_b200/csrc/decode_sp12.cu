@@ -757,11 +757,14 @@ uint32_t fast_grid(uint32_t total_tiles, int num_sms) {
 }
 
 // Tensors the product kernel decodes: the paper's format parameters (T = 256, n = 8) or
-// T = 128, n = 16 (NEXT-4), any value format and LUT width b, and the alignment its bulk copies need
-// (stream, gaps and PackedSignMantissa 16-byte aligned, output aligned to its word size);
+// T = 128, n = 16 (NEXT-4), any value format and LUT width b (FP16 up to ~3.1 G elements: 32-bit residual
+// offsets), and the alignment its bulk copies need (stream, gaps and PackedSignMantissa 16-byte aligned,
+// output aligned to its word size);
 // df11_decompress_block_ex sends every other tensor to the Algorithm 1 kernel.
 bool fast_supports(const df11_device_tensor &t) {
-    return ((t.T == kT && t.n == kN) || (t.T == 128 && t.n == 16)) &&
+    // residual byte offsets are 32-bit in the kernel: R * roundup(N, 16) / 8 (+ padding) must fit
+    const uint64_t res_bytes = (uint64_t)vf_of(t.value_format).R * ((t.num_elements + 15) & ~15ull) / 8 + 64;
+    return ((t.T == kT && t.n == kN) || (t.T == 128 && t.n == 16)) && res_bytes < (1ull << 32) &&
            (reinterpret_cast<uintptr_t>(t.encoded_exponent) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.gaps) & 15) == 0 &&
            (reinterpret_cast<uintptr_t>(t.packed_sign_mantissa) & 15) == 0 &&
