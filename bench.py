@@ -437,15 +437,16 @@ def main():
         with torch.cuda.graph(g, stream=gs):
             for i in range(args.steps):
                 plans[(args.warmup + i) % copies].run(gs, kernel_used)
-        g.replay()
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ga.record(gs)
-        g.replay()
-        gb.record(gs)
-        torch.cuda.synchronize()
+        with torch.cuda.stream(gs):                      # replay() launches on the current stream
+            g.replay()
+            torch.cuda.synchronize()
+            barrier()
+            torch.cuda.synchronize()
+            ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ga.record(gs)
+            g.replay()
+            gb.record(gs)
+            torch.cuda.synchronize()
         gval, _, gms = shard.aggregate_rate(bf16_bytes, ga.elapsed_time(gb), args.steps)
         graph = {"value": gval, "unit": UNIT, "ms_per_step": gms / args.steps,
                  "what": "the same K block decodes captured in one CUDA graph and replayed (no launch gaps)"}

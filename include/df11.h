@@ -131,8 +131,10 @@ void df11_host_tensor_free(df11_host_tensor *t);
 df11_status df11_decompress(const df11_device_tensor *t, void *stream);
 df11_status df11_decompress_block(const df11_device_tensor *ts, uint32_t count, void *stream);
 /* Same with an explicit kernel: DF11_KERNEL_ALG1 (literal Alg. 1, any valid T/n) or DF11_KERNEL_FAST
- * (persistent sm_100a kernel; DF11_E_UNSUPPORTED if a tensor is outside its parameter range: T = 256,
- * n = 8, encoded_exponent / gaps / packed_sign_mantissa 16-byte aligned, out 2-byte aligned).  With
+ * (persistent sm_100a kernel, every value format and LUT width; DF11_E_UNSUPPORTED if a tensor is
+ * outside its parameter range: T = 256, n = 8 or T = 128, n = 16, encoded_exponent / gaps /
+ * packed_sign_mantissa 16-byte aligned, out aligned to its word size, residual stream < 4 GiB, i.e.
+ * FP16 tensors below ~3.1 G elements).  With
  * DF11_KERNEL_AUTO the batch is split: tensors in that range take ONE product-kernel launch, the rest
  * the Alg. 1 kernel (one launch per distinct T); df11_last_kernel_mask() says which ran. */
 df11_status df11_decompress_block_ex(const df11_device_tensor *ts, uint32_t count, void *stream,
