@@ -4,7 +4,7 @@
 # usage: bash scripts/gpu_ab_lib.sh TAG "configs" [extra bench args]
 TAG=$1; CONFIGS=${2:-llama8b_block}; EXTRA=$3
 mkdir -p gpurun_out
-run() { timeout 600 python bench.py --config $1 --steps 200 --warmup 5 --no-e2e --no-cpu-baseline --no-transfer $EXTRA 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(round(d['value'],1), round(r['frac'],4), round(d['ms_per_step']*1e3,2), round(r['launch_us']['mean'],2))" 2>&1 | tail -1; }
+run() { timeout 600 python bench.py --config $1 --steps 200 --warmup 5 --no-e2e --no-cpu-baseline --no-transfer $EXTRA 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(round(d['value'],1), round(r['frac'],4), round(d['ms_per_step']*1e3,2), round(r['avg_launch_us'],2))" 2>&1 | tail -1; }
 {
 for round in 1 2; do
 for c in $CONFIGS; do

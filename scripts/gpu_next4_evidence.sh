@@ -23,5 +23,5 @@ python -c "
 import json,sys
 for l in open('gpurun_out/${TAG}_variants.jsonl'):
     d=json.loads(l); c=d['config']; r=d['roofline']
-    print(c['workload'], c['value_format'], c['lut_bits'], c['format'], round(c['bits_per_weight'],3), round(d['value'],1), round(r['frac'],4), round(r['launch_us']['mean'],1))
+    print(c['workload'], c['value_format'], c['lut_bits'], c['format'], round(c['bits_per_weight'],3), round(d['value'],1), round(r['frac'],4), round(r['avg_launch_us'],1))
 "

@@ -9,7 +9,7 @@ for a in "--lut-bits 5" "--lut-bits 12" "--lut-bits 10" "--vf fp16 --lut-bits mo
   timeout 600 python bench.py --steps 200 --warmup 5 --no-e2e --no-transfer --no-cpu-baseline $a 2>> gpurun_out/${TAG}_err.log | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); c=d['config']; r=d['roofline']
-print('$a', c['value_format'], c['lut_bits'], round(c['bits_per_weight'],3), round(d['value'],1), round(r['frac'],4), round(r['launch_us']['mean'],1))"
+print('$a', c['value_format'], c['lut_bits'], round(c['bits_per_weight'],3), round(d['value'],1), round(r['frac'],4), round(r['avg_launch_us'],1))"
 done
 echo "== memcheck over the variant parity cases (DF11_MAX_GRID=4)"
 DF11_MAX_GRID=4 timeout 1800 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest -q -x tests/test_gpu_variants.py -k "parity and not full_size" > /tmp/san_var.log 2>&1
