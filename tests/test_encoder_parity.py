@@ -220,3 +220,30 @@ def test_encoder_rejects_bad_variant_options():
     hist = (ctypes.c_uint64 * 256)(*([0] * 100 + [10] + [0] * 155))
     st = df11.lib().df11_encode_plan_create(hist, None, ctypes.byref(o), ctypes.byref(plan))
     assert df11.STATUS[st] == "DF11_E_UNSUPPORTED"
+
+
+def test_encoder_variant_fuzz_vs_oracle(oracle_mod):
+    """Seeded sweep: value format x b (incl. monolithic) x (T, n) x lut mode x size x distribution;
+    the library encoder writes the oracle's bytes every time."""
+    rng = np.random.default_rng(77)
+    vfs = ["bf16", "fp16", "fp8_e4m3", "fp8_e5m2"]
+    checked = 0
+    for i in range(40):
+        vf = vfs[i % 4]
+        N = int(rng.choice([1, 33, 4097, 70001, 262147]))
+        if rng.random() < 0.5:
+            w = workloads.gaussian_values((N,), 500 + i, vf, sigma=float(rng.choice([0.003, 0.02, 0.4])))
+        else:
+            pats = workloads.all_patterns(vf)
+            w = pats[rng.integers(0, pats.size, size=N)]
+        T, n = [(256, 8), (128, 16), (64, 4), (32, 32)][int(rng.integers(0, 4))]
+        lut_bits = [8, 2, 7, 11, 16, "mono"][int(rng.integers(0, 6))]
+        mode = ["auto", "wide"][int(rng.integers(0, 2))]
+        try:
+            fmt = oracle_mod.encode(w, T=T, n=n, lut_mode=mode, vf=vf, lut_bits=lut_bits)
+        except oracle_mod.FormatError:
+            assert lut_bits == "mono"
+            continue
+        _cmp_variant(fmt, df11.encode(w, T=T, n=n, lut_mode=mode, vf=vf, lut_bits=lut_bits))
+        checked += 1
+    assert checked >= 30
