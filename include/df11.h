@@ -196,13 +196,13 @@ typedef struct {
 } df11_device_buffers;
 
 /* Codebook + geometry of one tensor, built on the host.  `luts` is library-owned host memory: free
- * the plan with df11_encode_plan_free.  The device encoder codes BF16 (any lut_bits); other value
- * formats are DF11_E_UNSUPPORTED there (use df11_encode). */
+ * the plan with df11_encode_plan_free.  Every value format and lut_bits of df11_encode_opts. */
 typedef struct {
     uint64_t num_elements;            /* N = sum of tensor_hist */
     uint64_t encoded_bits;            /* sum over the tensor of code lengths */
     uint32_t T, n, B, k, lut_entry_bytes, max_code_len;
     uint32_t lut_bits;                /* b (the plan's tables have 2^b entries) */
+    uint32_t value_format;            /* DF11_VF_* of the words df11_encode_device reads */
     uint8_t  code_lengths[256];
     uint32_t codes[256];              /* canonical codes, right-aligned, MSB-first when emitted */
     uint8_t  *luts;             uint64_t luts_bytes;
@@ -210,9 +210,11 @@ typedef struct {
     uint64_t workspace_bytes;         /* device scratch df11_encode_device needs */
 } df11_encode_plan;
 
-/* Adds the exponent histogram of d_bf16[0..n) to d_hist (256 uint64 counters in device memory;
- * zero them first).  d_bf16 must be 2-byte aligned.  Enqueues on `stream`; does not synchronise. */
-df11_status df11_histogram_device(const uint16_t *d_bf16, uint64_t n, uint64_t *d_hist, void *stream);
+/* Adds the exponent histogram of d_values[0..n) (words of value_format, DF11_VF_*) to d_hist (256
+ * uint64 counters in device memory; zero them first).  d_values must be aligned to its word size.
+ * Enqueues on `stream`; does not synchronise. */
+df11_status df11_histogram_device(const void *d_values, uint64_t n, uint32_t value_format, uint64_t *d_hist,
+                                  void *stream);
 
 /* codebook_hist: host histogram the codebook is built from (the tensor's own, or the sum over a
  * group for a shared codebook, R5).  tensor_hist: the tensor's own host histogram (NULL = same as
@@ -223,12 +225,13 @@ df11_status df11_encode_plan_create(const uint64_t *codebook_hist, const uint64_
                                     const df11_encode_opts *opts, df11_encode_plan *plan);
 void df11_encode_plan_free(df11_encode_plan *plan);
 
-/* Encodes d_bf16[0..plan->num_elements) into `dst` on `stream` (memsets + kernels only; CodeLengths
- * and LUTs travel as kernel parameters, so the call never waits for the stream).  d_bf16 must hold exactly the tensor the plan's tensor_hist was
- * taken from; a mismatch yields a wrong encoding but no out-of-bounds access (the bit packer clips
- * to the planned sizes).  `workspace`: >= plan->workspace_bytes of device memory, 16-byte aligned.
+/* Encodes d_values[0..plan->num_elements) (words of plan->value_format) into `dst` on `stream`
+ * (memsets + kernels only; CodeLengths and LUTs travel as kernel parameters, so the call never waits
+ * for the stream).  d_values must hold exactly the tensor the plan's tensor_hist was taken from; a
+ * mismatch yields a wrong encoding but no out-of-bounds access (the bit packer clips to the planned
+ * sizes).  `workspace`: >= plan->workspace_bytes of device memory, 16-byte aligned.
  * Returns after enqueueing. */
-df11_status df11_encode_device(const uint16_t *d_bf16, const df11_encode_plan *plan,
+df11_status df11_encode_device(const void *d_values, const df11_encode_plan *plan,
                                const df11_device_buffers *dst, void *workspace, uint64_t workspace_bytes,
                                void *stream);
 

@@ -573,8 +573,6 @@ extern "C" df11_status df11_encode_plan_create(const uint64_t *codebook_hist, co
     df11_encode_opts o;
     df11_status st = check_opts(opts, o);
     if (st != DF11_OK) return st;
-    if (o.value_format != DF11_VF_BF16)
-        return df11_fail(DF11_E_UNSUPPORTED, "the device encoder codes BF16 only (use df11_encode)");
     try {
         Codebook cb;
         st = make_codebook(codebook_hist, (int)o.lut_mode, o.lut_bits, cb);
@@ -602,10 +600,11 @@ extern "C" df11_status df11_encode_plan_create(const uint64_t *codebook_hist, co
         plan->lut_entry_bytes = cb.entry_bytes;
         plan->max_code_len = cb.max_len;
         plan->lut_bits = cb.lut_bits;
+        plan->value_format = o.value_format;
         std::memcpy(plan->code_lengths, cb.len, 256);
         std::memcpy(plan->codes, cb.code, sizeof(plan->codes));
         plan->encoded_exponent_bytes = B * o.threads_per_block * o.bytes_per_thread + 16;
-        plan->packed_sign_mantissa_bytes = roundup(n, 16) + 16;
+        plan->packed_sign_mantissa_bytes = residual_bytes(n, kVF[o.value_format]);
         plan->gaps_bytes = roundup((5ull * B * o.threads_per_block + 7) / 8, 16) + 16;
         // workspace: one gap byte per format thread | one look-back word per pack segment | ticket
         const uint64_t segments = (n + DF11_ENCODE_SEGMENT - 1) / DF11_ENCODE_SEGMENT;

@@ -1,9 +1,10 @@
 // encode_gpu.cu — device half of the GPU encoder.
 //
-// Produces the DF11 arrays of DESIGN.md §2 from a BF16 tensor already in HBM, byte-identical to the
-// host encoder (encode.cpp) for the same codebook:
+// Produces the DF11 arrays of DESIGN.md §2 from a tensor already in HBM (BF16, or FP16 / FP8 words:
+// NEXT-4, R25), byte-identical to the host encoder (encode.cpp) for the same codebook:
 //   EncodedExponent   canonical Huffman codes of the exponents, MSB-first, tightly packed
-//   PackedSignMantissa sign<<7 | mantissa, one byte per element
+//   PackedSignMantissa sign<<7 | mantissa, one byte per element; other value formats: the
+//                     R-bit residuals sign << M | mantissa, MSB-first (R25)
 //   Gaps              per format thread: bit offset of the first code starting in its n-byte chunk,
 //                     0 if none (R13), packed 5 bits MSB-first (R12)
 //   BlockOutputPos    per block: number of codes starting before the block's first bit
@@ -27,6 +28,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "df11.h"
 #include "df11_internal.h"
@@ -44,10 +46,23 @@ constexpr unsigned long long kFlagAgg = 1ull << 62;   // look-back word: status 
 constexpr unsigned long long kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
-__device__ __forceinline__ uint32_t exp_of(uint32_t x) { return (x >> 7) & 0xFFu; }
+// value formats (df11.h DF11_VF_*): exponent field at bits [M, M + E) of a word
+template <uint32_t kVF>
+struct VFT {
+    static constexpr uint32_t M = kVF == DF11_VF_BF16 ? 7 : kVF == DF11_VF_FP16 ? 10 : kVF == DF11_VF_FP8_E4M3 ? 3 : 2;
+    static constexpr uint32_t E = kVF == DF11_VF_BF16 ? 8 : kVF == DF11_VF_FP8_E4M3 ? 4 : 5;
+    static constexpr uint32_t R = 1 + M;
+    static constexpr uint32_t WB = (kVF == DF11_VF_BF16 || kVF == DF11_VF_FP16) ? 2 : 1;   // word bytes
+    using W = typename std::conditional<WB == 2, uint16_t, uint8_t>::type;
+    __device__ static uint32_t exp_of(uint32_t x) { return (x >> M) & ((1u << E) - 1u); }
+    __device__ static uint32_t res_of(uint32_t x) { return ((x >> (E + M)) << M) | (x & ((1u << M) - 1u)); }
+};
 
-__global__ void __launch_bounds__(kHistThreads) hist_kernel(const uint16_t *__restrict__ w, uint64_t n,
+template <uint32_t kVF>
+__global__ void __launch_bounds__(kHistThreads) hist_kernel(const typename VFT<kVF>::W *__restrict__ w, uint64_t n,
                                                             unsigned long long *__restrict__ hist) {
+    using F = VFT<kVF>;
+    constexpr uint32_t kPerVec = 16 / F::WB;                 // words per 16-byte load
     constexpr int kWarps = kHistThreads / 32;
     __shared__ uint32_t h[kWarps][256];
     for (int i = threadIdx.x; i < kWarps * 256; i += kHistThreads) (&h[0][0])[i] = 0;
@@ -55,12 +70,12 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(const uint16_t *__re
     uint32_t *mine = h[threadIdx.x >> 5];
     const uint64_t gt = (uint64_t)blockIdx.x * kHistThreads + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * kHistThreads;
-    // elements before the first 16-byte boundary (w is 2-byte aligned)
-    const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(w) & 15u) >> 1);
-    const uint64_t head = mis ? (n < 8u - mis ? n : 8u - mis) : 0;
-    if (gt < head) atomicAdd(&mine[exp_of(w[gt])], 1u);
+    // elements before the first 16-byte boundary (w is aligned to its word size)
+    const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(w) & 15u) / F::WB);
+    const uint64_t head = mis ? (n < kPerVec - mis ? n : kPerVec - mis) : 0;
+    if (gt < head) atomicAdd(&mine[F::exp_of(w[gt])], 1u);
     const uint4 *v = reinterpret_cast<const uint4 *>(w + head);
-    const uint64_t nv = (n - head) / 8;
+    const uint64_t nv = (n - head) / kPerVec;
     for (uint64_t q = gt; q < nv; q += stride) {
         uint4 x;
         asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -68,12 +83,12 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(const uint16_t *__re
         const uint32_t ws[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            atomicAdd(&mine[exp_of(ws[j])], 1u);
-            atomicAdd(&mine[exp_of(ws[j] >> 16)], 1u);
+#pragma unroll
+            for (uint32_t k = 0; k < 4 / F::WB; k++) atomicAdd(&mine[F::exp_of(ws[j] >> (8 * F::WB * k))], 1u);
         }
     }
-    const uint64_t tail = head + nv * 8;
-    if (tail + gt < n) atomicAdd(&mine[exp_of(w[tail + gt])], 1u);
+    const uint64_t tail = head + nv * kPerVec;
+    for (uint64_t i = tail + gt; i < n; i += stride) atomicAdd(&mine[F::exp_of(w[i])], 1u);
     __syncthreads();
     for (int s = threadIdx.x; s < 256; s += kHistThreads) {
         uint32_t c = 0;
@@ -84,7 +99,7 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(const uint16_t *__re
 }
 
 struct PackParams {
-    const uint16_t *w;
+    const void *w;
     uint64_t n;                       // elements
     uint32_t *stream;                 // EncodedExponent as 32-bit words (zeroed)
     uint64_t stream_words;            // clip bound
@@ -97,6 +112,7 @@ struct PackParams {
     uint64_t chunks;                  // B*T
     uint32_t B;
     uint32_t aligned;                 // w and psm 16-byte aligned
+    uint32_t vf;
     uint32_t codes[256];
     uint8_t lens[256];
 };
@@ -110,7 +126,11 @@ __device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long 
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+template <uint32_t kVF>
 __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constant__ PackParams p) {
+    using F = VFT<kVF>;
+    using W = typename F::W;
+    const W *__restrict__ wp = static_cast<const W *>(p.w);
     __shared__ uint32_t s_code[256];
     __shared__ uint32_t s_len[256];
     __shared__ uint32_t s_warp[kPackThreads / 32];
@@ -128,26 +148,29 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
     const uint64_t base = seg * kSeg + (uint64_t)t * kPerThread;
     const int cnt = base >= p.n ? 0 : (p.n - base >= kPerThread ? kPerThread : (int)(p.n - base));
 
-    uint32_t x[kPerThread / 2];              // two BF16 words per register
+    constexpr uint32_t kPer32 = 4 / F::WB;                    // words per register
+    uint32_t x[kPerThread / kPer32];
     if (cnt == kPerThread && p.aligned) {
 #pragma unroll
-        for (int q = 0; q < kPerThread / 8; q++) {
+        for (int q = 0; q < (int)(kPerThread * F::WB / 16); q++) {
             asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(x[4 * q]), "=r"(x[4 * q + 1]), "=r"(x[4 * q + 2]), "=r"(x[4 * q + 3])
-                         : "l"(p.w + base + 8 * q));
+                         : "l"(wp + base + (16 / F::WB) * q));
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < kPerThread / 2; j++) {
-            const uint32_t lo = 2 * j < cnt ? p.w[base + 2 * j] : 0u;
-            const uint32_t hi = 2 * j + 1 < cnt ? p.w[base + 2 * j + 1] : 0u;
-            x[j] = lo | hi << 16;
+        for (int j = 0; j < kPerThread / (int)kPer32; j++) {
+            uint32_t v = 0;
+#pragma unroll
+            for (uint32_t k = 0; k < kPer32; k++)
+                v |= (j * kPer32 + k < (uint32_t)cnt ? (uint32_t)wp[base + j * kPer32 + k] : 0u) << (8 * F::WB * k);
+            x[j] = v;
         }
     }
-#define ELEM(j) (((j) & 1) ? x[(j) >> 1] >> 16 : x[(j) >> 1] & 0xFFFFu)
+#define ELEM(j) ((x[(j) / kPer32] >> (8 * F::WB * ((j) % kPer32))) & (F::WB == 2 ? 0xFFFFu : 0xFFu))
     uint32_t bits = 0;
 #pragma unroll
-    for (int j = 0; j < kPerThread; j++) bits += j < cnt ? s_len[exp_of(ELEM(j))] : 0u;
+    for (int j = 0; j < kPerThread; j++) bits += j < cnt ? s_len[F::exp_of(ELEM(j))] : 0u;
 
     // CTA exclusive scan of per-thread bit counts
     uint32_t incl = bits;
@@ -213,7 +236,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
 #pragma unroll
         for (int j = 0; j < kPerThread; j++) {
             if (j >= cnt) break;
-            const uint32_t e = exp_of(ELEM(j));
+            const uint32_t e = F::exp_of(ELEM(j));
             const uint32_t l = s_len[e];
             acc = (acc << l) | s_code[e];
             nb += l;
@@ -255,24 +278,41 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
     }
     if (cnt == 0) return;
 
-    // PackedSignMantissa: sign << 7 | mantissa
-    if (cnt == kPerThread && p.aligned) {
-        uint32_t o[kPerThread / 4];
+    // PackedSignMantissa: sign << 7 | mantissa (BF16); other formats: 16 R-bit residuals = 2R bytes at
+    // byte R * base / 8, MSB-first (base is a multiple of 16: every thread's range is whole bytes)
+    if constexpr (kVF == DF11_VF_BF16) {
+        if (cnt == kPerThread && p.aligned) {
+            uint32_t o[kPerThread / 4];
 #pragma unroll
-        for (int q = 0; q < kPerThread / 4; q++) {
-            const uint32_t a = x[2 * q], b = x[2 * q + 1];
-            // bytes: e0 = a lo, e1 = a hi, e2 = b lo, e3 = b hi; psm = (w >> 8 & 0x80) | (w & 0x7F)
-            const uint32_t sgn = __byte_perm(a, b, 0x7531) & 0x80808080u;   // high bytes -> sign bits
-            const uint32_t man = __byte_perm(a, b, 0x6420) & 0x7F7F7F7Fu;   // low bytes -> mantissa
-            o[q] = sgn | man;
+            for (int q = 0; q < kPerThread / 4; q++) {
+                const uint32_t a = x[2 * q], b = x[2 * q + 1];
+                // bytes: e0 = a lo, e1 = a hi, e2 = b lo, e3 = b hi; psm = (w >> 8 & 0x80) | (w & 0x7F)
+                const uint32_t sgn = __byte_perm(a, b, 0x7531) & 0x80808080u;   // high bytes -> sign bits
+                const uint32_t man = __byte_perm(a, b, 0x6420) & 0x7F7F7F7Fu;   // low bytes -> mantissa
+                o[q] = sgn | man;
+            }
+#pragma unroll
+            for (int q = 0; q < kPerThread / 16; q++)
+                *reinterpret_cast<uint4 *>(p.psm + base + 16 * q) = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kPerThread; j++)
+                if (j < cnt) p.psm[base + j] = (uint8_t)(((ELEM(j) >> 8) & 0x80u) | (ELEM(j) & 0x7Fu));
         }
-#pragma unroll
-        for (int q = 0; q < kPerThread / 16; q++)
-            *reinterpret_cast<uint4 *>(p.psm + base + 16 * q) = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
     } else {
+        uint8_t *dst = p.psm + base / 8 * F::R;
+        unsigned long long acc = 0;
+        uint32_t nb = 0, k = 0;
 #pragma unroll
-        for (int j = 0; j < kPerThread; j++)
-            if (j < cnt) p.psm[base + j] = (uint8_t)(((ELEM(j) >> 8) & 0x80u) | (ELEM(j) & 0x7Fu));
+        for (int j = 0; j < kPerThread; j++) {
+            acc = (acc << F::R) | (j < cnt ? F::res_of(ELEM(j)) : 0u);
+            nb += F::R;
+            while (nb >= 8) {
+                nb -= 8;
+                if (k < (uint32_t)((cnt * F::R + 7) / 8)) dst[k] = (uint8_t)(acc >> nb);
+                k++;
+            }
+        }
     }
 
     // Gaps and BlockOutputPos: position of this thread's first code relative to its chunk / block,
@@ -282,7 +322,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
     uint64_t chunk = (uint64_t)s_geo[0] + lc / CB;
     uint64_t blk = (uint64_t)s_geo[2] + lb / BB;
     uint32_t rc = lc % CB, rb = lb % BB;
-    const uint32_t lprev = base > 0 ? s_len[exp_of(p.w[base - 1])] : 0u;
+    const uint32_t lprev = base > 0 ? s_len[F::exp_of(wp[base - 1])] : 0u;
     if (base == 0 || rc < lprev) {       // the previous code started in an earlier chunk
         if (chunk < p.chunks) p.gapv[chunk] = (uint8_t)rc;
     }
@@ -292,7 +332,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
 #pragma unroll
     for (int j = 0; j < kPerThread - 1; j++) {
         if (j + 1 >= cnt) break;
-        const uint32_t l = s_len[exp_of(ELEM(j))];
+        const uint32_t l = s_len[F::exp_of(ELEM(j))];
         rc += l;
         rb += l;
         if (rc >= CB) {                  // codes are <= 32 <= 8n bits: at most one boundary per code
@@ -353,23 +393,48 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 }  // namespace
 }  // namespace df11
 
-extern "C" df11_status df11_histogram_device(const uint16_t *d_bf16, uint64_t n, uint64_t *d_hist, void *stream) {
-    using namespace df11;
-    if (!d_hist || (n && !d_bf16)) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL argument");
-    if (reinterpret_cast<uintptr_t>(d_bf16) & 1u) return df11_fail(DF11_E_INVALID_ARGUMENT, "d_bf16 not 2-byte aligned");
-    if (n == 0) return DF11_OK;
-    const uint64_t vec = n / 8;
+namespace df11 {
+namespace {
+template <uint32_t kVF>
+cudaError_t launch_hist(const void *d, uint64_t n, uint64_t *hist, cudaStream_t stream) {
+    using F = VFT<kVF>;
+    const uint64_t vec = n / (16 / F::WB);
     uint64_t want = (vec + kHistThreads - 1) / kHistThreads;
     const uint64_t cap = (uint64_t)num_sms() * 4;
     const unsigned grid = (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
-    hist_kernel<<<grid, kHistThreads, 0, (cudaStream_t)stream>>>(d_bf16, n, reinterpret_cast<unsigned long long *>(d_hist));
-    cudaError_t e = cudaGetLastError();
+    hist_kernel<kVF><<<grid, kHistThreads, 0, stream>>>(static_cast<const typename F::W *>(d), n,
+                                                        reinterpret_cast<unsigned long long *>(hist));
+    return cudaGetLastError();
+}
+uint32_t word_bytes(uint32_t vf) { return vf == DF11_VF_BF16 || vf == DF11_VF_FP16 ? 2u : 1u; }
+uint32_t residual_bits(uint32_t vf) {
+    return vf == DF11_VF_FP16 ? 11u : vf == DF11_VF_FP8_E4M3 ? 4u : vf == DF11_VF_FP8_E5M2 ? 3u : 8u;
+}
+}  // namespace
+}  // namespace df11
+
+extern "C" df11_status df11_histogram_device(const void *d_values, uint64_t n, uint32_t value_format, uint64_t *d_hist,
+                                             void *stream) {
+    using namespace df11;
+    if (!d_hist || (n && !d_values)) return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL argument");
+    if (value_format > DF11_VF_FP8_E5M2) return df11_fail(DF11_E_INVALID_ARGUMENT, "bad value_format");
+    if (reinterpret_cast<uintptr_t>(d_values) & (word_bytes(value_format) - 1))
+        return df11_fail(DF11_E_INVALID_ARGUMENT, "d_values not aligned to the word size");
+    if (n == 0) return DF11_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    switch (value_format) {
+        case DF11_VF_FP16: e = launch_hist<DF11_VF_FP16>(d_values, n, d_hist, s); break;
+        case DF11_VF_FP8_E4M3: e = launch_hist<DF11_VF_FP8_E4M3>(d_values, n, d_hist, s); break;
+        case DF11_VF_FP8_E5M2: e = launch_hist<DF11_VF_FP8_E5M2>(d_values, n, d_hist, s); break;
+        default: e = launch_hist<DF11_VF_BF16>(d_values, n, d_hist, s); break;
+    }
     if (e != cudaSuccess) return df11_cuda_fail((int)e, "histogram launch");
     df11_count_launches(1);
     return DF11_OK;
 }
 
-extern "C" df11_status df11_encode_device(const uint16_t *d_bf16, const df11_encode_plan *plan,
+extern "C" df11_status df11_encode_device(const void *d_values, const df11_encode_plan *plan,
                                           const df11_device_buffers *dst, void *workspace, uint64_t workspace_bytes,
                                           void *stream_) {
     using namespace df11;
@@ -377,13 +442,16 @@ extern "C" df11_status df11_encode_device(const uint16_t *d_bf16, const df11_enc
     const uint64_t N = plan->num_elements;
     const uint64_t chunks = (uint64_t)plan->B * plan->T;
     if (!dst->encoded_exponent || !dst->packed_sign_mantissa || !dst->gaps || !dst->luts || !dst->code_lengths ||
-        !dst->block_output_pos || (N && !d_bf16) || !workspace)
+        !dst->block_output_pos || (N && !d_values) || !workspace)
         return df11_fail(DF11_E_INVALID_ARGUMENT, "NULL buffer");
     if (workspace_bytes < plan->workspace_bytes) return df11_fail(DF11_E_INVALID_ARGUMENT, "workspace too small");
     if (!aligned16(dst->encoded_exponent) || !aligned16(dst->packed_sign_mantissa) || !aligned16(dst->gaps) ||
         !aligned16(dst->block_output_pos) || !aligned16(workspace))
         return df11_fail(DF11_E_INVALID_ARGUMENT, "device buffers must be 16-byte aligned");
-    if (reinterpret_cast<uintptr_t>(d_bf16) & 1u) return df11_fail(DF11_E_INVALID_ARGUMENT, "d_bf16 not 2-byte aligned");
+    if (plan->value_format > DF11_VF_FP8_E5M2) return df11_fail(DF11_E_INVALID_ARGUMENT, "bad value_format");
+    const uint32_t vf = plan->value_format;
+    if (reinterpret_cast<uintptr_t>(d_values) & (word_bytes(vf) - 1))
+        return df11_fail(DF11_E_INVALID_ARGUMENT, "d_values not aligned to the word size");
     if (plan->n < 4 || plan->n > 32 || plan->T < 32 || plan->T > 1024 || plan->max_code_len > 32)
         return df11_fail(DF11_E_INVALID_ARGUMENT, "plan geometry out of range");
     cudaStream_t st = (cudaStream_t)stream_;
@@ -404,7 +472,11 @@ extern "C" df11_status df11_encode_device(const uint16_t *d_bf16, const df11_enc
     DF11_TRY(cudaMemsetAsync(ws, 0, plan->workspace_bytes, st), "workspace memset");
     DF11_TRY(cudaMemsetAsync(dst->encoded_exponent, 0, plan->encoded_exponent_bytes, st), "stream memset");
     DF11_TRY(cudaMemsetAsync(dst->gaps, 0, plan->gaps_bytes, st), "gaps memset");
-    DF11_TRY(cudaMemsetAsync(dst->packed_sign_mantissa + N, 0, plan->packed_sign_mantissa_bytes - N, st), "psm memset");
+    {   // residual bytes past the last element's (its partial byte is written whole by the pack kernel)
+        const uint64_t used = N * residual_bits(vf) / 8;
+        DF11_TRY(cudaMemsetAsync(dst->packed_sign_mantissa + used, 0, plan->packed_sign_mantissa_bytes - used, st),
+                 "psm memset");
+    }
     {   // CodeLengths + LUTs through kernel parameters (no host synchronisation)
         Blob b;
         b.dst = dst->code_lengths;
@@ -435,7 +507,8 @@ extern "C" df11_status df11_encode_device(const uint16_t *d_bf16, const df11_enc
     if (N) {
         PackParams p;
         std::memset(&p, 0, sizeof(p));
-        p.w = d_bf16;
+        p.w = d_values;
+        p.vf = vf;
         p.n = N;
         p.stream = reinterpret_cast<uint32_t *>(dst->encoded_exponent);
         p.stream_words = plan->encoded_exponent_bytes / 4;
@@ -448,11 +521,16 @@ extern "C" df11_status df11_encode_device(const uint16_t *d_bf16, const df11_enc
         p.block_bits = 8ull * plan->n * plan->T;
         p.chunks = chunks;
         p.B = plan->B;
-        p.aligned = aligned16(d_bf16) ? 1u : 0u;
+        p.aligned = aligned16(d_values) ? 1u : 0u;
         std::memcpy(p.codes, plan->codes, sizeof(p.codes));
         std::memcpy(p.lens, plan->code_lengths, 256);
         if (segments > 0x7FFFFFFFull) return df11_fail(DF11_E_TOO_LARGE, "too many segments");
-        pack_kernel<<<(unsigned)segments, kPackThreads, 0, st>>>(p);
+        switch (vf) {
+            case DF11_VF_FP16: pack_kernel<DF11_VF_FP16><<<(unsigned)segments, kPackThreads, 0, st>>>(p); break;
+            case DF11_VF_FP8_E4M3: pack_kernel<DF11_VF_FP8_E4M3><<<(unsigned)segments, kPackThreads, 0, st>>>(p); break;
+            case DF11_VF_FP8_E5M2: pack_kernel<DF11_VF_FP8_E5M2><<<(unsigned)segments, kPackThreads, 0, st>>>(p); break;
+            default: pack_kernel<DF11_VF_BF16><<<(unsigned)segments, kPackThreads, 0, st>>>(p); break;
+        }
         DF11_TRY(cudaGetLastError(), "pack launch");
         launches++;
         const uint64_t groups = (chunks + 7) / 8;

@@ -75,7 +75,7 @@ class EncodePlanC(ctypes.Structure):
     _fields_ = [("num_elements", ctypes.c_uint64), ("encoded_bits", ctypes.c_uint64),
                 ("T", ctypes.c_uint32), ("n", ctypes.c_uint32), ("B", ctypes.c_uint32), ("k", ctypes.c_uint32),
                 ("lut_entry_bytes", ctypes.c_uint32), ("max_code_len", ctypes.c_uint32),
-                ("lut_bits", ctypes.c_uint32),
+                ("lut_bits", ctypes.c_uint32), ("value_format", ctypes.c_uint32),
                 ("code_lengths", ctypes.c_uint8 * 256), ("codes", ctypes.c_uint32 * 256),
                 ("luts", ctypes.POINTER(ctypes.c_uint8)), ("luts_bytes", ctypes.c_uint64),
                 ("encoded_exponent_bytes", ctypes.c_uint64), ("packed_sign_mantissa_bytes", ctypes.c_uint64),
@@ -111,7 +111,7 @@ def lib():
         L.df11_plan_cta_ranges.restype = None
         L.df11_decompress_host_block.argtypes = [ctypes.POINTER(HostTensorC), ctypes.POINTER(DeviceTensorC),
                                                  ctypes.POINTER(P), U32, P, P]
-        L.df11_histogram_device.argtypes = [P, U64, P, P]
+        L.df11_histogram_device.argtypes = [P, U64, U32, P, P]
         L.df11_encode_plan_create.argtypes = [P, P, ctypes.POINTER(EncodeOpts), ctypes.POINTER(EncodePlanC)]
         L.df11_encode_plan_free.argtypes = [ctypes.POINTER(EncodePlanC)]
         L.df11_encode_device.argtypes = [P, ctypes.POINTER(EncodePlanC), ctypes.POINTER(DeviceBuffersC), P, U64, P]
@@ -456,13 +456,13 @@ class EncodePlan:
     """df11_encode_plan: codebook + geometry of one tensor (host); frees its LUT copy on deletion."""
 
     def __init__(self, codebook_hist, tensor_hist=None, T: int = 256, n: int = 8, lut_mode: str = "auto",
-                 lut_bits=8):
+                 lut_bits=8, vf: str = "bf16"):
         cb = np.ascontiguousarray(codebook_hist, dtype=np.uint64)
         th = None if tensor_hist is None else np.ascontiguousarray(tensor_hist, dtype=np.uint64)
         if cb.shape != (256,) or (th is not None and th.shape != (256,)):
             raise ValueError("histograms have 256 bins")
         self._c = EncodePlanC()
-        o = _opts(T, n, lut_mode, 0, "bf16", lut_bits)
+        o = _opts(T, n, lut_mode, 0, vf, lut_bits)
         _check(lib().df11_encode_plan_create(ctypes.c_void_p(cb.ctypes.data),
                                              None if th is None else ctypes.c_void_p(th.ctypes.data),
                                              ctypes.byref(o), ctypes.byref(self._c)))
@@ -475,6 +475,7 @@ class EncodePlan:
 
     def __getattr__(self, name):
         if name in ("num_elements", "encoded_bits", "T", "n", "B", "k", "lut_entry_bytes", "max_code_len", "lut_bits",
+                    "value_format",
                     "luts_bytes", "encoded_exponent_bytes", "packed_sign_mantissa_bytes", "gaps_bytes",
                     "workspace_bytes"):
             return int(getattr(self.__dict__["_c"], name))
@@ -485,13 +486,27 @@ class EncodePlan:
         return np.frombuffer(bytes(self._c.code_lengths), np.uint8).copy()
 
 
-def _dev_u16(x):
+_VF_OF_TORCH = {"torch.bfloat16": "bf16", "torch.float16": "fp16", "torch.float8_e4m3fn": "fp8_e4m3",
+                "torch.float8_e5m2": "fp8_e5m2"}
+
+
+def _dev_words(x, vf=None):
+    """A contiguous CUDA tensor of words and its value format: BF16 / FP16 / FP8 dtypes name their
+    format; int16 / uint16 / uint8 bit patterns need `vf` (default bf16 for 16-bit words)."""
     import torch
     if not isinstance(x, torch.Tensor) or not x.is_cuda:
         raise ValueError("expected a CUDA tensor")
-    if x.dtype not in _u16_dtypes():
-        raise ValueError("expected a 16-bit tensor (BF16 bit patterns)")
-    return x.contiguous()
+    if vf is None:
+        vf = _VF_OF_TORCH.get(str(x.dtype), "bf16" if x.element_size() == 2 else None)
+        if vf is None:
+            raise ValueError("pass vf= for 8-bit bit patterns")
+    if x.element_size() != VALUE_FORMATS[vf][1]:
+        raise ValueError(f"{vf} words are {VALUE_FORMATS[vf][1]} bytes")
+    return x.contiguous(), vf
+
+
+def _dev_u16(x):
+    return _dev_words(x, "bf16")[0]
 
 
 def _on(stream):
@@ -503,28 +518,29 @@ def _on(stream):
     return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
 
-def histogram_device(x, out=None, stream=None):
-    """df11_histogram_device: exponent histogram of a device BF16 tensor, accumulated into `out`
-    (int64[256] on the same device; zeroed when created here).  Everything runs on `stream`."""
+def histogram_device(x, out=None, stream=None, vf=None):
+    """df11_histogram_device: exponent histogram of a device tensor (BF16 / FP16 / FP8 words),
+    accumulated into `out` (int64[256] on the same device; zeroed when created here).  Everything runs on
+    `stream`."""
     import torch
     with _on(stream):
-        x = _dev_u16(x)
+        x, vf = _dev_words(x, vf)
         if out is None:
             out = torch.zeros(256, dtype=torch.int64, device=x.device)
-        _check(lib().df11_histogram_device(ctypes.c_void_p(x.data_ptr()), x.numel(),
+        _check(lib().df11_histogram_device(ctypes.c_void_p(x.data_ptr()), x.numel(), VALUE_FORMATS[vf][0],
                                            ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
     return out
 
 
 def encode_device(x, T: int = 256, n: int = 8, lut_mode: str = "auto", codebook_hist=None, stream=None,
-                  out=None) -> "DeviceTensor":
-    """GPU encoder: device BF16 tensor -> DeviceTensor (histogram on the GPU, codebook on the host,
-    packing on the GPU).  Byte-identical to encode(x.cpu()) with the same options; with
-    `codebook_hist` (host, 256 bins, e.g. a group's summed histogram) the codebook is built from it."""
+                  out=None, vf=None, lut_bits=8) -> "DeviceTensor":
+    """GPU encoder: device tensor -> DeviceTensor (histogram on the GPU, codebook on the host, packing on
+    the GPU).  Byte-identical to encode(x.cpu()) with the same options; with `codebook_hist` (host, 256
+    bins, e.g. a group's summed histogram) the codebook is built from it."""
     with _on(stream):
-        x = _dev_u16(x)
-        th = histogram_device(x, stream=stream).cpu().numpy().view(np.uint64)   # read back on `stream`
-    plan = EncodePlan(th if codebook_hist is None else codebook_hist, th, T, n, lut_mode)
+        x, vf = _dev_words(x, vf)
+        th = histogram_device(x, stream=stream, vf=vf).cpu().numpy().view(np.uint64)   # read back on `stream`
+    plan = EncodePlan(th if codebook_hist is None else codebook_hist, th, T, n, lut_mode, lut_bits, vf)
     return encode_device_with_plan(x, plan, stream=stream, out=out)
 
 
@@ -535,7 +551,8 @@ def encode_device_with_plan(x, plan: EncodePlan, stream=None, out=None) -> "Devi
 
 def _encode_device_with_plan(x, plan, stream, out):
     import torch
-    x = _dev_u16(x)
+    vf = VF_NAMES[plan.value_format]
+    x, _ = _dev_words(x, vf)
     if x.numel() != plan.num_elements:
         raise ValueError("tensor size does not match the plan")
     dev = x.device
@@ -548,8 +565,8 @@ def _encode_device_with_plan(x, plan, stream, out):
     dt.num_elements = plan.num_elements
     dt.meta = {k: getattr(plan, k) for k in ("T", "n", "B", "k", "lut_entry_bytes", "encoded_bits", "max_code_len",
                                              "lut_bits")}
-    dt.meta["value_format"] = 0
-    dt.vf = "bf16"
+    dt.meta["value_format"] = plan.value_format
+    dt.vf = vf
     dt.encoded_exponent = buf(plan.encoded_exponent_bytes)
     dt.packed_sign_mantissa = buf(plan.packed_sign_mantissa_bytes)
     dt.gaps = buf(plan.gaps_bytes)
@@ -557,9 +574,10 @@ def _encode_device_with_plan(x, plan, stream, out):
     dt.code_lengths = buf(256)
     dt.block_output_pos = buf(4 * (plan.B + 1))
     B, T = plan.B, plan.T
-    dt.compressed_bytes = ((plan.encoded_bits + 7) // 8 + plan.num_elements + (5 * B * T + 7) // 8
+    R = VALUE_FORMATS[vf][2]
+    dt.compressed_bytes = ((plan.encoded_bits + 7) // 8 + (R * plan.num_elements + 7) // 8 + (5 * B * T + 7) // 8
                            + 4 * (B + 1) + plan.luts_bytes + 256)
-    dt.out = out if out is not None else torch.empty(max(plan.num_elements, 1), dtype=torch.bfloat16, device=dev)
+    dt.out = out if out is not None else torch.empty(max(plan.num_elements, 1), dtype=out_dtype(vf), device=dev)
     ws = buf(plan.workspace_bytes)
     d = DeviceBuffersC(dt.encoded_exponent.data_ptr(), dt.packed_sign_mantissa.data_ptr(), dt.gaps.data_ptr(),
                        dt.luts.data_ptr(), dt.code_lengths.data_ptr(), dt.block_output_pos.data_ptr())
@@ -571,15 +589,16 @@ def _encode_device_with_plan(x, plan, stream, out):
 
 
 def encode_device_group(xs, T: int = 256, n: int = 8, lut_mode: str = "auto", shared_codebook: bool = True,
-                        stream=None):
+                        stream=None, vf=None, lut_bits=8):
     """GPU encoder for a group of tensors (e.g. one transformer block); shared_codebook builds one
     codebook from the summed histogram (R5)."""
     with _on(stream):
-        hists = [histogram_device(x, stream=stream) for x in xs]
+        hists = [histogram_device(x, stream=stream, vf=vf) for x in xs]
         hs = [h.cpu().numpy().view(np.uint64) for h in hists]
     total = np.sum(np.stack(hs), axis=0, dtype=np.uint64) if hs else np.zeros(256, np.uint64)
     res = []
     for x, h in zip(xs, hs):
-        plan = EncodePlan(total if shared_codebook else h, h, T, n, lut_mode)
+        x, xvf = _dev_words(x, vf)
+        plan = EncodePlan(total if shared_codebook else h, h, T, n, lut_mode, lut_bits, xvf)
         res.append(encode_device_with_plan(x, plan, stream=stream))
     return res

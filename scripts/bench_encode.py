@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--configs", default="llama8b_block,llama70b_block,llama405b_block")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--host", action="store_true", help="also time the host encoder (slow for 405B)")
+    ap.add_argument("--vf", default="bf16", choices=list(workloads.VALUE_FORMATS),
+                    help="value format of the weights (NEXT-4): bf16 / fp16 / fp8_e4m3 / fp8_e5m2")
     args = ap.parse_args()
     import torch
 
@@ -36,19 +38,28 @@ def main():
     torch.cuda.set_device(dev)
     for cfg in args.configs.split(","):
         shapes = workloads.CONFIGS[cfg]
-        xs = [torch.from_numpy(workloads.gaussian_bf16_torch(sh, workloads.seed_for(cfg, 0, name), dev)
-                               .view(np.int16)).to(dev) for name, sh in shapes]
+        vf = args.vf
+        if vf == "bf16":
+            xs = [torch.from_numpy(workloads.gaussian_bf16_torch(sh, workloads.seed_for(cfg, 0, name), dev)
+                                   .view(np.int16)).to(dev) for name, sh in shapes]
+        else:
+            xs = []
+            for name, sh in shapes:
+                w = workloads.gaussian_values(sh, workloads.seed_for(cfg, 0, name), vf)
+                xs.append(torch.from_numpy(w.view(np.int16) if w.dtype == np.uint16 else w).to(dev))
+        wb = xs[0].element_size()
+        wv = torch.int16 if wb == 2 else torch.uint8
         numel = sum(x.numel() for x in xs)
         # correctness: round trip
-        dts = [df11.encode_device(x) for x in xs]
+        dts = [df11.encode_device(x, vf=vf) for x in xs]
         outs = df11.decompress_block(dts)
         torch.cuda.synchronize()
         for x, o in zip(xs, outs):
-            assert torch.equal(o.reshape(-1).view(torch.int16), x.reshape(-1))
+            assert torch.equal(o.reshape(-1).view(wv), x.reshape(-1))
         comp = sum(d.compressed_bytes for d in dts)
 
         def full():   # histograms of the whole block first (one read-back), then the plans and packing
-            return df11.encode_device_group(xs, shared_codebook=False)
+            return df11.encode_device_group(xs, shared_codebook=False, vf=vf)
 
         for _ in range(2):
             full()
@@ -65,8 +76,8 @@ def main():
         # pack stage alone (plans prebuilt)
         plans = []
         for x in xs:
-            h = df11.histogram_device(x).cpu().numpy().view(np.uint64)
-            plans.append(df11.EncodePlan(h, h))
+            h = df11.histogram_device(x, vf=vf).cpu().numpy().view(np.uint64)
+            plans.append(df11.EncodePlan(h, h, vf=vf))
         for _ in range(2):
             [df11.encode_device_with_plan(x, p) for x, p in zip(xs, plans)]
         torch.cuda.synchronize()
@@ -78,24 +89,24 @@ def main():
         ms_pack = s.elapsed_time(e) / args.reps
         hbuf = torch.zeros(256, dtype=torch.int64, device=dev)
         for _ in range(2):
-            [df11.histogram_device(x, out=hbuf) for x in xs]
+            [df11.histogram_device(x, out=hbuf, vf=vf) for x in xs]
         s.record()
         for _ in range(args.reps):
-            [df11.histogram_device(x, out=hbuf) for x in xs]
+            [df11.histogram_device(x, out=hbuf, vf=vf) for x in xs]
         e.record()
         torch.cuda.synchronize()
         ms_hist = s.elapsed_time(e) / args.reps
-        line = {"config": cfg, "elements": numel, "bf16_bytes": 2 * numel, "df11_bytes": comp,
-                "ratio": comp / (2 * numel), "gpu_encode_ms_per_block": ms_full, "gpu_encode_wall_ms": wall_full,
+        line = {"config": cfg, "value_format": vf, "elements": numel, "input_bytes": wb * numel, "df11_bytes": comp,
+                "ratio": comp / (wb * numel), "gpu_encode_ms_per_block": ms_full, "gpu_encode_wall_ms": wall_full,
                 "gpu_pack_ms_per_block": ms_pack, "gpu_hist_ms_per_block": ms_hist,
-                "hist_gbs": 2 * numel / ms_hist / 1e6, "gpu_encode_gelem_s": numel / ms_full / 1e6,
+                "hist_gbs": wb * numel / ms_hist / 1e6, "gpu_encode_gelem_s": numel / ms_full / 1e6,
                 "paper_single_thread_s_per_block": {"llama8b_block": 191, "llama70b_block": 547,
                                                     "llama405b_block": 2133}.get(cfg)}
         if args.host:
-            ws = [x.cpu().numpy().view(np.uint16) for x in xs]
+            ws = [x.cpu().numpy().view(workloads.word_dtype(vf)) for x in xs]
             t0 = time.perf_counter()
             for w in ws:
-                df11.encode(w)
+                df11.encode(w, vf=vf)
             line["host_encode_ms_per_block"] = (time.perf_counter() - t0) * 1e3
             line["host_threads"] = os.cpu_count()
         print(json.dumps(line), flush=True)

@@ -214,12 +214,21 @@ def test_encoder_rejects_bad_variant_options():
     for kw in (dict(lut_bits=17), dict(lut_bits=40)):
         with pytest.raises(df11.Df11Error):
             df11.encode(w, **kw)
-    # the device encoder's plan is BF16 only
-    o = df11._opts(256, 8, "auto", 0, "fp16", 8)
-    plan = df11.EncodePlanC()
-    hist = (ctypes.c_uint64 * 256)(*([0] * 100 + [10] + [0] * 155))
-    st = df11.lib().df11_encode_plan_create(hist, None, ctypes.byref(o), ctypes.byref(plan))
-    assert df11.STATUS[st] == "DF11_E_UNSUPPORTED"
+
+
+@pytest.mark.parametrize("vf", ["bf16", "fp16", "fp8_e4m3", "fp8_e5m2"])
+def test_device_plan_matches_host_encoder(vf):
+    """df11_encode_plan_create (the GPU encoder's host half) plans the host encoder's codebook and sizes
+    for every value format and b."""
+    w = workloads.gaussian_values((100003,), 3, vf)
+    E, M = {"bf16": (8, 7), "fp16": (5, 10), "fp8_e4m3": (4, 3), "fp8_e5m2": (5, 2)}[vf]
+    hist = np.bincount((w.astype(np.uint32) >> M) & ((1 << E) - 1), minlength=256).astype(np.uint64)
+    for lut_bits in (8, 5, "mono"):
+        h = df11.encode(w, vf=vf, lut_bits=lut_bits)
+        plan = df11.EncodePlan(hist, vf=vf, lut_bits=lut_bits)
+        assert (plan.value_format, plan.lut_bits, plan.k, plan.B) == (h.value_format, h.lut_bits, h.k, h.B)
+        assert plan.packed_sign_mantissa_bytes == h.packed_sign_mantissa.size
+        assert np.array_equal(plan.code_lengths, h.code_lengths)
 
 
 def test_encoder_variant_fuzz_vs_oracle(oracle_mod):

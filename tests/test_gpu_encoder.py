@@ -145,3 +145,39 @@ def test_encoder_full_size_block(df11, oracle_mod):
         out = df11.decompress(dt)
         torch.cuda.synchronize()
         assert torch.equal(out.reshape(-1).view(torch.int16), _dev(w).reshape(-1)), name
+
+
+@pytest.mark.parametrize("vf", ["fp16", "fp8_e4m3", "fp8_e5m2"])
+@pytest.mark.parametrize("case", ["gauss", "patterns", "ragged", "tiny"])
+def test_encoder_value_formats_match_oracle(df11, oracle_mod, vf, case):
+    """NEXT-3 x NEXT-4: the device encoder writes the oracle's bytes for FP16 / FP8 words (R-bit residual
+    stream included), for aligned and unaligned (view) inputs, and the result decodes back."""
+    import workloads as wl
+    if case == "gauss":
+        w = wl.gaussian_values((1 << 20,), 71, vf)
+    elif case == "patterns":
+        w = np.tile(wl.all_patterns(vf), 5 if vf == "fp16" else 1000)
+        np.random.default_rng(2).shuffle(w)
+    elif case == "ragged":
+        w = wl.gaussian_values((300007,), 72, vf)
+    else:
+        w = wl.gaussian_values((19,), 73, vf)
+    tdt = torch.int16 if w.dtype == np.uint16 else torch.uint8
+    x = torch.from_numpy(w.view(np.int16) if w.dtype == np.uint16 else w).to("cuda")
+    fmt = oracle_mod.encode(w, vf=vf)
+    _compare(df11.encode_device(x, vf=vf), fmt)
+    big = torch.zeros(w.size + 16, dtype=tdt, device="cuda")
+    big[3: 3 + w.size] = x
+    dt = df11.encode_device(big[3: 3 + w.size], vf=vf)           # unaligned view: scalar head path
+    _compare(dt, fmt)
+    out = df11.decompress(dt)
+    torch.cuda.synchronize()
+    got = out.view(tdt).cpu().numpy().view(w.dtype).reshape(-1)
+    assert np.array_equal(got, w)
+
+
+@pytest.mark.parametrize("lut_bits", [3, 12, "mono"])
+def test_encoder_lut_bits_match_oracle(df11, oracle_mod, lut_bits):
+    w = workloads.gaussian_values((200003,), 74, "fp16")
+    x = torch.from_numpy(w.view(np.int16)).to("cuda").view(torch.float16)
+    _compare(df11.encode_device(x, lut_bits=lut_bits), oracle_mod.encode(w, vf="fp16", lut_bits=lut_bits))
