@@ -166,3 +166,16 @@ def test_value_format_host_path(df11):
         df11.decompress_host(h, dt, host)
         torch.cuda.synchronize()
         assert np.array_equal(_words(host, vf), w)
+
+
+def test_fp16_large_tensor_offsets(df11):
+    """FP16 with 420 M elements: residual bit positions (11 * index) pass 2^32, which the product kernel
+    handles in modular 32-bit arithmetic relative to the staged range.  Every element == original."""
+    N = 420_000_000
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = (torch.randn(N, generator=g, device="cuda") * 0.02).to(torch.float16)
+    dt = df11.encode_device(x)                                      # GPU encoder (byte parity elsewhere)
+    out = df11.decompress(dt, kernel="fast")
+    torch.cuda.synchronize()
+    assert df11.last_kernels() == {"fast"}
+    assert torch.equal(out.view(torch.int16), x.view(torch.int16))
