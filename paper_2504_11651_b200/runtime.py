@@ -135,15 +135,36 @@ class DF11Hook:
             h.remove()
 
 
-def compress_module(module, names=None, device="cuda", scratch=None, **encode_kw) -> DF11Hook:
-    """Encode the named parameters of `module` (default: every floating-point parameter of BF16 /
-    FP16 / FP8 dtype) with df11_encode, keep only their DF11 form in HBM, and attach a DF11Hook."""
+def encode_module(module, names=None, device="cuda", **encode_kw):
+    """df11_encode the named parameters of `module` (default: every BF16 / FP16 / FP8 parameter) and
+    upload them: returns (names, BlockWeights)."""
     if names is None:
         names = [n for n, p in module.named_parameters() if str(p.dtype) in _VF_OF_DTYPE]
     dts = []
     for n in names:
         p = module.get_parameter(n)
-        vf = _VF_OF_DTYPE[str(p.dtype)]
-        h = df11.encode(p.detach().cpu(), vf=vf, **encode_kw)
+        h = df11.encode(p.detach().cpu(), vf=_VF_OF_DTYPE[str(p.dtype)], **encode_kw)
         dts.append(df11.to_device(h, device))
-    return DF11Hook(module, names, BlockWeights(dts), scratch)
+    return list(names), BlockWeights(dts)
+
+
+def compress_module(module, names=None, device="cuda", scratch=None, **encode_kw) -> DF11Hook:
+    """Encode the named parameters of `module` (default: every floating-point parameter of BF16 /
+    FP16 / FP8 dtype) with df11_encode, keep only their DF11 form in HBM, and attach a DF11Hook."""
+    names, weights = encode_module(module, names, device, **encode_kw)
+    return DF11Hook(module, names, weights, scratch)
+
+
+def compress_blocks(modules, device="cuda", **encode_kw):
+    """The paper's deployment: the weights of every transformer block (and, passed as
+    modules too, the embedding and the LM head) live in HBM as DF11 only; each module's forward is
+    preceded by ONE batched decode of its weights into a scratch shared by all of them (the BF16
+    matrices are "immediately discarded" after the forward).  Returns the hooks."""
+    import torch
+    encoded = [encode_module(m, None, device, **encode_kw) for m in modules]
+    formats = {w.vf for _, w in encoded if w.dts}
+    if len(formats) > 1:
+        raise ValueError("one value format per model (the shared scratch has one dtype)")
+    cap = max((w.scratch_elements() for _, w in encoded), default=64)
+    scratch = torch.empty(cap, dtype=df11.out_dtype(formats.pop() if formats else "bf16"), device=device)
+    return [DF11Hook(m, names, w, scratch) for m, (names, w) in zip(modules, encoded)]

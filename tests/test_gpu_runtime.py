@@ -124,3 +124,30 @@ def test_module_hook_bit_exact():
     assert b1[0].weight is None                           # unbound after the forward
     h1.remove()
     h2.remove()
+
+
+def test_compress_blocks_llama_bit_exact():
+    """A randomly initialised (offline, no weights downloaded) Llama-architecture model from
+    `transformers` whose decoder blocks, embedding and LM head exist only as DF11 in HBM: one decode
+    launch per block / embedding / head per forward into one shared scratch, and the logits are
+    bit-identical to the BF16 model's (lossless, P:8)."""
+    transformers = pytest.importorskip("transformers")
+    from paper_2504_11651_b200 import df11, runtime
+    torch.manual_seed(0)
+    cfg = transformers.LlamaConfig(vocab_size=1024, hidden_size=256, intermediate_size=704, num_hidden_layers=3,
+                                   num_attention_heads=4, num_key_value_heads=2, tie_word_embeddings=False)
+    model = transformers.LlamaForCausalLM(cfg).to("cuda", torch.bfloat16).eval()
+    ids = torch.randint(0, 1024, (2, 17), device="cuda")
+    with torch.no_grad():
+        ref = model(ids).logits.clone()
+    mods = list(model.model.layers) + [model.model.embed_tokens, model.lm_head]
+    hooks = runtime.compress_blocks(mods)
+    assert model.model.layers[0].self_attn.q_proj.weight is None
+    n0 = df11.launch_count()
+    with torch.no_grad():
+        out = model(ids).logits
+    torch.cuda.synchronize()
+    assert df11.launch_count() - n0 == len(mods)
+    assert torch.equal(out, ref)
+    for h in hooks:
+        h.remove()
