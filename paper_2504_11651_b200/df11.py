@@ -251,10 +251,19 @@ def _opts(T, n, lut_mode, num_threads, vf="bf16", lut_bits=8):
     return EncodeOpts(T, n, LUT_MODES[lut_mode], num_threads, VALUE_FORMATS[vf][0], _lut_bits(lut_bits))
 
 
-def encode(w, T: int = 256, n: int = 8, lut_mode: str = "auto", num_threads: int = 0, vf: str = "bf16",
+def _infer_vf(w, vf):
+    if vf is not None:
+        return vf
+    return {"torch.bfloat16": "bf16", "torch.float16": "fp16", "torch.float8_e4m3fn": "fp8_e4m3",
+            "torch.float8_e5m2": "fp8_e5m2", "float16": "fp16"}.get(str(getattr(w, "dtype", "")), "bf16")
+
+
+def encode(w, T: int = 256, n: int = 8, lut_mode: str = "auto", num_threads: int = 0, vf: str = None,
            lut_bits=8) -> HostTensor:
-    """df11_encode: host tensor of value format vf (bf16 default: torch.bfloat16 or uint16 bit patterns;
-    fp16; fp8_e4m3 / fp8_e5m2 as uint8 patterns) -> HostTensor.  lut_bits: b in [1, 16] or "mono"."""
+    """df11_encode: host tensor of value format vf -> HostTensor.  vf: "bf16" (torch.bfloat16 or uint16
+    bit patterns; the default), "fp16", "fp8_e4m3" / "fp8_e5m2" (uint8 patterns); inferred from a torch
+    (or numpy float16) dtype when not given.  lut_bits: b in [1, 16] or "mono"."""
+    vf = _infer_vf(w, vf)
     a = _as_words(w, vf)
     shape = a.shape
     a = a.reshape(-1)
@@ -266,7 +275,8 @@ def encode(w, T: int = 256, n: int = 8, lut_mode: str = "auto", num_threads: int
 
 
 def encode_group(ws, T: int = 256, n: int = 8, lut_mode: str = "auto", shared_codebook: bool = False,
-                 num_threads: int = 0, vf: str = "bf16", lut_bits=8):
+                 num_threads: int = 0, vf: str = None, lut_bits=8):
+    vf = _infer_vf(ws[0], vf) if ws else "bf16"
     arrs = [_as_words(w, vf) for w in ws]
     shapes = [a.shape for a in arrs]
     flat = [a.reshape(-1) for a in arrs]
