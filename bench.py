@@ -314,6 +314,9 @@ def main():
     from paper_2504_11651_b200 import df11, shard
 
     rank, world, local = shard.rank_info()
+    oversub = os.environ.get("DF11_BENCH_OVERSUBSCRIBE") == "1" and local >= torch.cuda.device_count()
+    if oversub:                                  # functional check of the N-rank path on fewer GPUs only
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     shard.init_host_group()                      # gloo on the host; NCCL is never initialised
@@ -480,6 +483,7 @@ def main():
         except Exception as exc:                                           # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle", "sample": f"failed: {exc}"}
 
+    oversub_any = shard.max_over_ranks([1.0 if oversub else 0.0])[0] > 0
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -498,6 +502,8 @@ def main():
             "graph": graph,
             "transfer_baseline": transfer,
             "gpu_launches": launches,
+            **({"oversubscribed": "ranks share GPUs (DF11_BENCH_OVERSUBSCRIBE): a functional check, not a "
+                                  "throughput"} if oversub_any else {}),
             "clocks": clocks.summary(),
             "per_gpu_gbs": value / world,
         }
