@@ -608,7 +608,8 @@ def encode_device_group(xs, T: int = 256, n: int = 8, lut_mode: str = "auto", sh
     total = np.sum(np.stack(hs), axis=0, dtype=np.uint64) if hs else np.zeros(256, np.uint64)
     res = []
     for x, h in zip(xs, hs):
-        x, xvf = _dev_words(x, vf)
+        with _on(stream):
+            x, xvf = _dev_words(x, vf)
         plan = EncodePlan(total if shared_codebook else h, h, T, n, lut_mode, lut_bits, xvf)
         res.append(encode_device_with_plan(x, plan, stream=stream))
     return res
