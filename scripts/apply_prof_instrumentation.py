@@ -17,7 +17,7 @@ def ins(marker, code, after=False):
     s = s.replace(marker, marker + code if after else code + marker)
 
 
-ins("__global__ void __launch_bounds__(kCta12, 1) sp12_kernel(", """__device__ unsigned long long g_sp12_prof[148 * 32][8];   // per warp: cycles per phase
+ins("// kVF: value format (DF11_VF_*, NEXT-4).  Decode, scan and compaction", """__device__ unsigned long long g_sp12_prof[148 * 32][8];   // per warp: cycles per phase
 #define PROF_MARK(i) do { const long long _n = clock64(); if (lane == 0) prof[i] += _n - prof_t; prof_t = _n; } while (0)
 """)
 ins("    const uint32_t FULL = 0xFFFFFFFFu;\n", """    unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};

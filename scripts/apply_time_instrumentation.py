@@ -19,7 +19,7 @@ def ins(marker, code, after=False):
     s = s.replace(marker, marker + code if after else code + marker)
 
 
-ins("__global__ void __launch_bounds__(kCta12, 1) sp12_kernel(", """__device__ unsigned long long g_sp12_times[256][12];   // per CTA: entry, table built, exit, 8 groups' ends
+ins("// kVF: value format (DF11_VF_*, NEXT-4).  Decode, scan and compaction", """__device__ unsigned long long g_sp12_times[256][12];   // per CTA: entry, table built, exit, 8 groups' ends
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
