@@ -8,7 +8,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
-#include <atomic>
 #include <cstring>
 #include <mutex>
 
@@ -20,7 +19,6 @@ cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 bool fast_supports(const df11_device_tensor &t);
 uint32_t fast_grid(uint32_t total_tiles, int num_sms);
-unsigned long long *pool_slot_ptr(int device, uint32_t epoch);
 }  // namespace df11
 
 namespace {
@@ -169,34 +167,7 @@ df11_status launch_fast_batch(const df11_device_tensor *ts, const uint32_t *idx,
             const char *v = std::getenv("DF11_SWITCH_TILES_ENV");
             return v ? (uint32_t)std::atoi(v) : (uint32_t)DF11_SWITCH_TILES;
         }();
-        // End-of-launch pool: the last pool_pct % of the tiles (all from the last entry, a whole number
-        // of group rounds) are left out of the static ranges; CTAs that finish early claim them, which
-        // absorbs the 2-4 % speed differences between SMs (per-CTA timelines: scripts/cta_times.py).
-        static const uint32_t pool_pct = [] {
-            const char *v = std::getenv("DF11_POOL_PCT");
-            return v ? (uint32_t)std::atoi(v) : 5u;
-        }();
-        static std::atomic<uint32_t> epoch{1};
-        uint32_t P = 0;
-        if (pool_pct && G > 1 && bt.count) {
-            const uint32_t last = bt.count - 1, last_tiles = bt.tile_start[last + 1] - bt.tile_start[last];
-            P = std::min<uint32_t>((uint32_t)((uint64_t)total * pool_pct / 100), last_tiles);
-            P -= P % df11::kPoolChunk;
-            if (P < 2 * df11::kPoolChunk) P = 0;
-        }
-        unsigned long long *slot = nullptr;
-        if (P) {
-            bt.pool_epoch = epoch.fetch_add(1) | 1u;                 // never 0 (a fresh slot holds 0)
-            slot = df11::pool_slot_ptr(dev, bt.pool_epoch);
-            if (!slot) P = 0;
-        }
-        bt.pool_tiles = P;
-        bt.pool_start = total - P;
-        bt.pool_entry = bt.count - 1;
-        bt.pool_slot = slot;
-        bt.tile_start[bt.count] = total - P;                      // plan the static ranges without the pool
         df11_plan_cta_ranges(bt.tile_start, bt.count, G, sw, bt.cta_start);
-        bt.tile_start[bt.count] = total;
         bt.cta_ranges = 1;
     }
     const uint32_t kpow[12] = {1u << 12, 1u << 4, 1u << 8, 8u, 0, 0, 0, 0, 0, 0, 0, 0};

@@ -12,7 +12,6 @@ namespace df11 {
 // parameter: no workspace, no H2D copy, graph-capturable.
 constexpr int kMaxEntries = 2 * DF11_MAX_BATCH;   // a tensor may be split into several tile ranges
 constexpr int kMaxCta = 256;                      // persistent grid bound for per-CTA tile ranges
-constexpr uint32_t kPoolChunk = 8;                // pool tiles claimed at a time (one per group of a CTA)
 
 struct Batch {
     df11_device_tensor t[kMaxEntries];
@@ -26,11 +25,6 @@ struct Batch {
     // powers of two used as IMAD multipliers (field extraction on the FMA pipe); read from the
     // constant bank so the compiler cannot strength-reduce them into ALU shifts (set by the launcher)
     uint32_t kpow[12];
-    // end-of-launch tile pool (product kernel): global tiles [pool_start, pool_start + pool_tiles), all of
-    // entry pool_entry, are not in any CTA's static range; CTAs that finish their range claim them in
-    // chunks of one tile per group from *pool_slot (a 64-bit word: launch epoch << 32 | claimed tiles)
-    uint32_t pool_start, pool_tiles, pool_entry, pool_epoch;
-    unsigned long long *pool_slot;
 };
 
 // Tensor owning global tile `g` (binary search over tile_start).

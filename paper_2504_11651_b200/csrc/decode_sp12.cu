@@ -44,7 +44,6 @@ constexpr int kFirst = SP12_FIRST;          // decode steps before the first war
 #endif
 constexpr uint32_t kGroups12 = SP12_GROUPS;
 constexpr uint32_t kCta12 = kLanes * kGroups12;
-static_assert(kPoolChunk == kGroups12, "a pool chunk is one tile per group");
 constexpr uint32_t kWarps12 = kLanes / 32;
 // slot words per chain: a chain holds <= 32 codes (<= 64 bits of code starts, codes >= 2 bits: 1-bit
 // codes take the direct path); without exact ends it may overshoot its end by <= 3 codes (one lookup
@@ -74,8 +73,7 @@ struct Lay12 {
     static constexpr uint32_t kGCnt = kGWsum + 2 * kWarps12 * 4;    // warps done with the merge
     static constexpr uint32_t kGMbar = kGCnt + 16;                  // [stage, sign/mantissa] mbarriers
     static constexpr uint32_t kGrpBytes = kGMbar + 16;
-    static constexpr uint32_t kTbar = kOffGrp + kGroups12 * kGrpBytes;   // pool claim | table flags
-    static constexpr uint32_t kSmem = kTbar + 16;
+    static constexpr uint32_t kSmem = kOffGrp + kGroups12 * kGrpBytes;
     static_assert(kOffGrp % 16 == 0 && kGSm % 16 == 0 && kGReg % 16 == 0 && kWarpReg12 % 16 == 0 &&
                       kGWsum % 16 == 0 && kGMbar % 8 == 0 && kGrpBytes % 16 == 0,
                   "alignment");
@@ -180,45 +178,13 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     uint32_t q = 0, parity = 0, qs = 0;
-    if (bt.pool_tiles && tid == 0) {
-        // the pool word belongs to this launch once its epoch is ours (the first CTA here resets it)
-        unsigned long long old = *reinterpret_cast<volatile unsigned long long *>(bt.pool_slot);
-        while ((uint32_t)(old >> 32) != bt.pool_epoch) {
-            const unsigned long long seen = atomicCAS(bt.pool_slot, old, (unsigned long long)bt.pool_epoch << 32);
-            if (seen == old) break;
-            old = seen;
-        }
-    }
 
     int ti_idx = tensor_of_tile(bt, c_begin);
-    const uint8_t *table_of = nullptr;                 // tensor whose decode table is in SMEM
-    bool in_pool = false;
-    for (uint32_t seg_begin = c_begin, seg_end = c_begin;; seg_begin = seg_end) {
-        if (!in_pool) {
-            if (seg_begin >= c_end) {                  // static range done: claim pool tiles
-                if (!bt.pool_tiles) break;
-                in_pool = true;
-            } else {
-                seg_end = min(c_end, bt.tile_start[ti_idx + 1]);
-                if (seg_end <= seg_begin) { ti_idx++; continue; }
-            }
-        }
-        if (in_pool) {
-            __syncthreads();                            // the claim word below is free again
-            if (tid == 0) {
-                const unsigned long long v = atomicAdd(bt.pool_slot, (unsigned long long)kPoolChunk);
-                sts32(sbase + L::kTbar, (uint32_t)v);
-            }
-            __syncthreads();
-            const uint32_t c = lds32(sbase + L::kTbar);
-            if (c >= bt.pool_tiles) break;
-            ti_idx = (int)bt.pool_entry;
-            seg_begin = bt.pool_start + c;
-            seg_end = bt.pool_start + min(c + kPoolChunk, bt.pool_tiles);
-        }
+    for (uint32_t seg_begin = c_begin; seg_begin < c_end; ti_idx++) {
         const df11_device_tensor &ts = bt.t[ti_idx];
+        const uint32_t seg_end = min(c_end, bt.tile_start[ti_idx + 1]);
         const uint32_t base_tile = bt.tile_start[ti_idx] - bt.tile_off[ti_idx];
-        if (!in_pool && seg_end >= bt.tile_start[ti_idx + 1]) ti_idx++;   // the next static segment's entry
+        if (seg_end <= seg_begin) continue;
 
         // =============================== T12 for this tensor (CTA-wide)
         __syncthreads();
@@ -234,19 +200,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 else issue_tile16(ts, tile - base_tile, stage, mbar);
             }
         }
-        // the table of the current tensor stays; flags of the last build are kept in SMEM
-        bool safe, lut_in_smem, long_codes;
-        if (ts.encoded_exponent != table_of) {
-            long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
-                                                     kOffGrp + L::kGReg, tid, safe, lut_in_smem);
-            if (tid == 0) sts32(sbase + L::kTbar + 4, (long_codes ? 1u : 0u) | (safe ? 2u : 0u) | (lut_in_smem ? 4u : 0u));
-            table_of = ts.encoded_exponent;
-        } else {
-            const uint32_t fl = lds32(sbase + L::kTbar + 4);
-            long_codes = (fl & 1u) != 0;
-            safe = (fl & 2u) != 0;
-            lut_in_smem = (fl & 4u) != 0;
-        }
+        bool safe, lut_in_smem;
+        const bool long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
+                                                       kOffGrp + L::kGReg, tid, safe, lut_in_smem);
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
 
         const uint32_t N = (uint32_t)ts.num_elements;
@@ -757,6 +713,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 __syncwarp();                  // the region's reads are done before the next tile's slots
             }
         }
+        seg_begin = seg_end;
     }
 #undef K_ROW
 #undef K_TOP
@@ -764,7 +721,6 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 #undef K_S24
 }
 
-__device__ unsigned long long g_pool_slots[4096];  // end-of-launch tile pools (Batch::pool_slot)
 uint32_t g_sp12_attr_set[64];   // bit (b8 ? 0 : 8) + (n16 ? 4 : 0) + vf: smem attribute set
 
 template <uint32_t kNB, uint32_t kVF, bool kB8>
@@ -795,20 +751,6 @@ cudaError_t launch_vf(const Batch &bt, int device, uint32_t grid, cudaStream_t s
 }
 
 }  // namespace
-
-// Device address of the pool word of launch `epoch` (4096 slots used round robin; a slot is re-armed by
-// the epoch the launch writes into it, so no reset is needed between launches; two launches in flight
-// at the same time share a slot only if 4096 launches separate them).
-unsigned long long *pool_slot_ptr(int device, uint32_t epoch) {
-    static unsigned long long *base[64];
-    if (device < 0 || device >= 64) return nullptr;
-    if (!base[device]) {
-        void *p = nullptr;
-        if (cudaGetSymbolAddress(&p, g_pool_slots) != cudaSuccess) return nullptr;
-        base[device] = static_cast<unsigned long long *>(p);
-    }
-    return base[device] + (epoch & 4095u);
-}
 
 uint32_t fast_grid(uint32_t total_tiles, int num_sms) {
     return min((uint32_t)num_sms, (total_tiles + kGroups12 - 1) / kGroups12);
