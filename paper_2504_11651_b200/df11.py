@@ -567,8 +567,11 @@ def _encode_device_with_plan(x, plan, stream, out):
         raise ValueError("tensor size does not match the plan")
     dev = x.device
 
-    def buf(nbytes):
-        return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=dev)
+    def buf(nbytes, zero=False):
+        # small metadata buffers are zero-filled: the encoder writes their first nbytes only (the rest is
+        # the 16-byte minimum allocation), and a host copy of the whole buffer must not read garbage
+        n = max(int(nbytes), 16)
+        return (torch.zeros if zero else torch.empty)(n, dtype=torch.uint8, device=dev)
 
     dt = DeviceTensor.__new__(DeviceTensor)
     dt.shape = tuple(x.shape)
@@ -580,9 +583,9 @@ def _encode_device_with_plan(x, plan, stream, out):
     dt.encoded_exponent = buf(plan.encoded_exponent_bytes)
     dt.packed_sign_mantissa = buf(plan.packed_sign_mantissa_bytes)
     dt.gaps = buf(plan.gaps_bytes)
-    dt.luts = buf(plan.luts_bytes)
+    dt.luts = buf(plan.luts_bytes, zero=True)
     dt.code_lengths = buf(256)
-    dt.block_output_pos = buf(4 * (plan.B + 1))
+    dt.block_output_pos = buf(4 * (plan.B + 1), zero=True)
     B, T = plan.B, plan.T
     R = VALUE_FORMATS[vf][2]
     dt.compressed_bytes = ((plan.encoded_bits + 7) // 8 + (R * plan.num_elements + 7) // 8 + (5 * B * T + 7) // 8
