@@ -19,8 +19,6 @@ cudaError_t launch_alg1(const Batch &bt, uint32_t T, size_t max_smem, cudaStream
 cudaError_t launch_sp12(const Batch &bt, int device, cudaStream_t stream, uint64_t *launches);
 bool fast_supports(const df11_device_tensor &t);
 uint32_t fast_grid(uint32_t total_tiles, int num_sms);
-bool ws_enabled();
-cudaError_t launch_ws(const Batch &bt, cudaStream_t stream, uint64_t *launches);
 }  // namespace df11
 
 namespace {
@@ -174,10 +172,7 @@ df11_status launch_fast_batch(const df11_device_tensor *ts, const uint32_t *idx,
     }
     const uint32_t kpow[12] = {1u << 12, 1u << 4, 1u << 8, 8u, 0, 0, 0, 0, 0, 0, 0, 0};
     std::memcpy(bt.kpow, kpow, sizeof(kpow));
-    // DF11_WS=1 (A/B experiment): the warp-specialised variant for BF16, T = 256, n = 8, byte tables
-    const bool ws = df11::ws_enabled() && bt.t[0].value_format == DF11_VF_BF16 && bt.t[0].n == 8 &&
-                    df11::lut_bits_of(bt.t[0]) == 8;
-    cudaError_t e = ws ? df11::launch_ws(bt, stream, &g_launches) : df11::launch_sp12(bt, dev, stream, &g_launches);
+    cudaError_t e = df11::launch_sp12(bt, dev, stream, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "fast decode launch");
     g_kernel_mask |= 2u;
     return DF11_OK;

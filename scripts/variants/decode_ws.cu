@@ -1,4 +1,6 @@
-// decode_ws.cu — A/B experiment (selected only with DF11_WS=1): a warp-specialised form of the product
+// decode_ws.cu — A/B experiment, not part of libdf11.so (measured -3 %: DESIGN.md §7 "Experiments that did
+// not pay"; to rebuild it, copy it back to csrc/ and dispatch to launch_ws in api.cu under DF11_WS=1).
+// A warp-specialised form of the product
 // kernel for BF16, T = 256, n = 8, byte tables.  Same per-tile work as sp12_kernel (decode_sp12.cu), split
 // over two roles so that neither carries the other's live state:
 //   decode warps (4 per group): stage wait -> chains into double-buffered private slots -> counts
