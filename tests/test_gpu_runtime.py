@@ -126,7 +126,8 @@ def test_module_hook_bit_exact():
     h2.remove()
 
 
-def test_compress_blocks_llama_bit_exact():
+@pytest.mark.parametrize("dtype", ["bfloat16", "float16"])
+def test_compress_blocks_llama_bit_exact(dtype):
     """A randomly initialised (offline, no weights downloaded) Llama-architecture model from
     `transformers` whose decoder blocks, embedding and LM head exist only as DF11 in HBM: one decode
     launch per block / embedding / head per forward into one shared scratch, and the logits are
@@ -136,7 +137,7 @@ def test_compress_blocks_llama_bit_exact():
     torch.manual_seed(0)
     cfg = transformers.LlamaConfig(vocab_size=1024, hidden_size=256, intermediate_size=704, num_hidden_layers=3,
                                    num_attention_heads=4, num_key_value_heads=2, tie_word_embeddings=False)
-    model = transformers.LlamaForCausalLM(cfg).to("cuda", torch.bfloat16).eval()
+    model = transformers.LlamaForCausalLM(cfg).to("cuda", getattr(torch, dtype)).eval()
     ids = torch.randint(0, 1024, (2, 17), device="cuda")
     with torch.no_grad():
         ref = model(ids).logits.clone()
