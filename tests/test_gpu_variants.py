@@ -179,3 +179,28 @@ def test_fp16_large_tensor_offsets(df11):
     torch.cuda.synchronize()
     assert df11.last_kernels() == {"fast"}
     assert torch.equal(out.view(torch.int16), x.view(torch.int16))
+
+
+@pytest.mark.parametrize("vf,lut_bits", [("fp16", 8), ("fp8_e4m3", 8), ("fp8_e5m2", 5), ("bf16", 5), ("fp16", "mono")])
+def test_corrupt_metadata_variants_never_fault(df11, vf, lut_bits):
+    """df11.h robustness contract for the format variants: random Gaps / BlockOutputPos / LUTs /
+    CodeLengths / stream bytes may give wrong output but never an out-of-bounds access (run under
+    compute-sanitizer memcheck in profiles/r02_final_sanitizer.log)."""
+    w = workloads.gaussian_values((150001,), 81, vf)
+    h = df11.encode(w, vf=vf, lut_bits=lut_bits)
+    a = h.arrays()
+    rng = np.random.default_rng(3)
+    meta = dict(num_elements=h.num_elements, T=h.T, n=h.n, B=h.B, k=h.k, lut_entry_bytes=h.lut_entry_bytes,
+                encoded_bits=h.encoded_bits, max_code_len=h.max_code_len, value_format=h.value_format,
+                lut_bits=h.lut_bits)
+    for trial in range(6):
+        b = {k: np.array(v, copy=True) for k, v in a.items()}
+        key = ["block_output_pos", "luts", "code_lengths", "gaps", "encoded_exponent", "packed_sign_mantissa"][trial]
+        if key == "block_output_pos":
+            b[key] = rng.integers(0, 1 << 32, size=b[key].size, dtype=np.uint64).astype(np.uint32)
+        else:
+            b[key] = rng.integers(0, 256, size=b[key].size, dtype=np.uint8)
+        for kernel in ("alg1", "fast"):
+            dt = df11.DeviceTensor.from_arrays(meta, b)
+            df11.decompress(dt, kernel=kernel)
+            torch.cuda.synchronize()   # a fault would raise here
