@@ -121,6 +121,25 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def run_env(dev) -> dict:
+    """GPU name, driver, torch / CUDA versions and the library build of this run."""
+    import torch
+    env = {"gpu": torch.cuda.get_device_name(dev), "torch": torch.__version__, "cuda": torch.version.cuda}
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        drv = pynvml.nvmlSystemGetDriverVersion()
+        env["driver"] = drv.decode() if isinstance(drv, bytes) else drv
+    except Exception:                                                     # reported, never fatal
+        pass
+    try:
+        from paper_2504_11651_b200 import df11
+        env["library"] = df11.lib().df11_version().decode()
+    except Exception:
+        pass
+    return env
+
+
 def variant_key(args) -> str:
     """Suffix of the ncu summary key for a NEXT-4 format variant ("" for the paper's format)."""
     if args.vf == "bf16" and str(args.lut_bits) == "8" and args.format == "256x8":
@@ -506,7 +525,10 @@ def main():
                                   "throughput"} if oversub_any else {}),
             "clocks": clocks.summary(),
             "per_gpu_gbs": value / world,
+            "env": run_env(dev),
         }
+        line["config"].update({"k": [h.k for h in hs], "max_code_len": [h.max_code_len for h in hs],
+                               "lut_entry_bytes": [h.lut_entry_bytes for h in hs]})
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
