@@ -360,7 +360,7 @@ extern "C" df11_status df11_cuda_fail(int e, const char *what) { return cuda_fai
 extern "C" void df11_count_launches(uint64_t k) { g_launches += k; }
 extern "C" int df11_last_cuda_error(void) { return g_cuda_err; }
 extern "C" const char *df11_last_error_message(void) { return g_msg; }
-extern "C" const char *df11_version(void) { return "df11-b200 0.1 (sm_100a)"; }
+extern "C" const char *df11_version(void) { return "df11-b200 0.2 (sm_100a; BF16 / FP16 / FP8 E4M3 / FP8 E5M2, b-bit LUTs)"; }
 extern "C" uint32_t df11_last_kernel_mask(void) { return g_kernel_mask; }
 extern "C" uint64_t df11_launch_count(int reset) {
     uint64_t v = g_launches;
