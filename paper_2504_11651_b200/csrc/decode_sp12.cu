@@ -85,12 +85,13 @@ struct Lay12 {
 // (8 FP16 / 16 FP8 words) and its residuals are R * (unit words) / 8 bytes at SMEM byte address o.
 // Eight FP16 words from 8 exponents (bytes of x0, x1) and eight 11-bit residuals s << 10 | m at o.
 __device__ __forceinline__ uint4 unit_fp16(uint32_t x0, uint32_t x1, uint32_t o) {
-    const uint32_t base = o & ~3u, sh = (o & 3u) * 8u;
-    const uint32_t B0 = bswap32(lds32(base)), B1 = bswap32(lds32(base + 4)), B2 = bswap32(lds32(base + 8));
-    uint32_t B3 = 0;
-    if (sh >= 16) B3 = bswap32(lds32(base + 12));      // 11 bytes from byte 2 or 3 reach a 4th word
-    const uint32_t H0 = __funnelshift_l(B1, B0, sh), H1 = __funnelshift_l(B2, B1, sh),
-                   H2 = __funnelshift_l(B3, B2, sh);   // the 88 residual bits, MSB-first
+    const uint32_t base = o & ~3u, ro = o & 3u;
+    const uint32_t L0 = lds32(base), L1 = lds32(base + 4), L2 = lds32(base + 8);
+    uint32_t L3 = 0;
+    if (ro >= 2) L3 = lds32(base + 12);                // 11 bytes from byte 2 or 3 reach a 4th word
+    // big-endian 32-bit windows at bytes r, r + 4, r + 8: one PRMT each (selector 0x0123 + r * 0x1111)
+    const uint32_t sel = 0x0123u + ro * 0x1111u;
+    const uint32_t H0 = prmt(L0, L1, sel), H1 = prmt(L1, L2, sel), H2 = prmt(L2, L3, sel);   // 88 bits, MSB-first
     const uint32_t f0 = H0 >> 21, f1 = (H0 >> 10) & 0x7FFu, f2 = __funnelshift_l(H1, H0, 22) >> 21,
                    f3 = (H1 >> 20) & 0x7FFu, f4 = (H1 >> 9) & 0x7FFu, f5 = __funnelshift_l(H2, H1, 23) >> 21,
                    f6 = (H2 >> 19) & 0x7FFu, f7 = (H2 >> 8) & 0x7FFu;
