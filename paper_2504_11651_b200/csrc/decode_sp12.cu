@@ -92,19 +92,19 @@ __device__ __forceinline__ uint4 unit_fp16(uint32_t x0, uint32_t x1, uint32_t o)
     // big-endian 32-bit windows at bytes r, r + 4, r + 8: one PRMT each (selector 0x0123 + r * 0x1111)
     const uint32_t sel = 0x0123u + ro * 0x1111u;
     const uint32_t H0 = prmt(L0, L1, sel), H1 = prmt(L1, L2, sel), H2 = prmt(L2, L3, sel);   // 88 bits, MSB-first
-    const uint32_t f0 = H0 >> 21, f1 = (H0 >> 10) & 0x7FFu, f2 = __funnelshift_l(H1, H0, 22) >> 21,
-                   f3 = (H1 >> 20) & 0x7FFu, f4 = (H1 >> 9) & 0x7FFu, f5 = __funnelshift_l(H2, H1, 23) >> 21,
-                   f6 = (H2 >> 19) & 0x7FFu, f7 = (H2 >> 8) & 0x7FFu;
-    // a pair: (s << 15 | e << 10 | m) in each 16-bit half
-    auto pair = [](uint32_t fa, uint32_t fb, uint32_t E) {
-        const uint32_t F = fa | (fb << 16);
-        return ((F << 5) & 0x80008000u) | (F & 0x03FF03FFu) | (E << 10);
+    // pair p = residual bits [22p, 22p + 22) as a 32-bit window G (MSB-first): element 2p in G's bits
+    // 31..21, element 2p + 1 in bits 20..10.  F puts them into the two 16-bit halves; a word is then
+    // (s << 15 | m) per half plus the exponents, which PRMT places at bits 10 / 26 from x << 2.
+    auto pair = [](uint32_t G, uint32_t E10) {
+        const uint32_t F = (G >> 21) | ((G << 6) & 0x07FF0000u);
+        return ((F << 5) & 0x80008000u) | (F & 0x03FF03FFu) | E10;
     };
+    const uint32_t y0 = x0 << 2, y1 = x1 << 2;            // exponents (< 32) << 2 stay inside their bytes
     uint4 r;
-    r.x = pair(f0, f1, prmt(x0, 0u, 0x4140u));
-    r.y = pair(f2, f3, prmt(x0, 0u, 0x4342u));
-    r.z = pair(f4, f5, prmt(x1, 0u, 0x4140u));
-    r.w = pair(f6, f7, prmt(x1, 0u, 0x4342u));
+    r.x = pair(H0, prmt(y0, 0u, 0x1404u));
+    r.y = pair(__funnelshift_l(H1, H0, 22), prmt(y0, 0u, 0x3424u));
+    r.z = pair(__funnelshift_l(H2, H1, 12), prmt(y1, 0u, 0x1404u));
+    r.w = pair(H2 << 2, prmt(y1, 0u, 0x3424u));
     return r;
 }
 // Four FP8 E4M3 bytes from 4 exponents E and the nibbles of residual bytes (b_lo, b_hi) of word r
