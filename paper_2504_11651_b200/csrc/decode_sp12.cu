@@ -99,7 +99,7 @@ __device__ __forceinline__ uint4 unit_fp16(uint32_t x0, uint32_t x1, uint32_t o)
         const uint32_t F = (G >> 21) | ((G << 6) & 0x07FF0000u);
         return ((F << 5) & 0x80008000u) | (F & 0x03FF03FFu) | E10;
     };
-    const uint32_t y0 = x0 << 2, y1 = x1 << 2;            // exponents (< 32) << 2 stay inside their bytes
+    const uint32_t y0 = x0, y1 = x1;                      // stored exponents are e << 2 (to_stored)
     uint4 r;
     r.x = pair(H0, prmt(y0, 0u, 0x1404u));
     r.y = pair(__funnelshift_l(H1, H0, 22), prmt(y0, 0u, 0x3424u));
@@ -113,13 +113,13 @@ template <uint32_t kSel>
 __device__ __forceinline__ uint32_t quad_e4m3(uint32_t r, uint32_t E) {
     const uint32_t P = prmt(r, 0u, kSel);                // [b, b, b', b']
     const uint32_t N = bitsel<0xFF00FF00u>(P >> 4, P);   // low nibble of byte j = residual of element j
-    return ((N << 4) & 0x80808080u) | (N & 0x07070707u) | (E << 3);
+    return ((N << 4) & 0x80808080u) | (N & 0x07070707u) | E;          // E: stored e << 3
 }
 // Four FP8 E5M2 bytes from 4 exponents E and 12 residual bits u (element 0 in bits 11..9): s << 7 |
 // e << 2 | m.
 __device__ __forceinline__ uint32_t quad_e5m2(uint32_t u, uint32_t E) {
     const uint32_t W = ((u >> 9) & 7u) | (((u >> 6) & 7u) << 8) | (((u >> 3) & 7u) << 16) | ((u & 7u) << 24);
-    return ((W << 5) & 0x80808080u) | (W & 0x03030303u) | (E << 2);
+    return ((W << 5) & 0x80808080u) | (W & 0x03030303u) | E;          // E: stored e << 2
 }
 // Residual of one element from the SMEM staging: R bits at bit position `bit` of the buffer at `buf`.
 template <uint32_t kR_>
@@ -631,7 +631,8 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 } else {
                     // other value formats (NEXT-4): residual bits of output e at bit kRb * e - 8 * a0
                     if (edge)
-                        out[es] = (OutT)compose_vf(kF, ld8(wreg + (es - F)), res_smem<kRb>(smb, es * kRb - 8u * a0));
+                        out[es] = (OutT)compose_vf(kF, from_stored<kVF>(ld8(wreg + (es - F))),
+                                                   res_smem<kRb>(smb, es * kRb - 8u * a0));
                     for (uint32_t u = ua + lane; u < ub; u += 32) {
                         const uint32_t e0 = u * kU;
                         const uint32_t o = smb + (e0 / 8u * kRb - a0), xa = wreg + (e0 - F);
@@ -708,7 +709,8 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                 } else {
                     // residuals of a tile above the SMEM cap (or an unaligned output): per element
                     for (uint32_t e = ra + lane; e < rb; e += 32)
-                        out[e] = (OutT)compose_vf(kF, ld8(wreg + (e - F)), load_residual(kF, ts.packed_sign_mantissa, e));
+                        out[e] = (OutT)compose_vf(kF, from_stored<kVF>(ld8(wreg + (e - F))),
+                                                  load_residual(kF, ts.packed_sign_mantissa, e));
                 }
                 if (t == 0 && has_next) stage_sm(nlo, nhi);
                 __syncwarp();                  // the region's reads are done before the next tile's slots

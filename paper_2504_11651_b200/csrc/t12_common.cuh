@@ -29,17 +29,20 @@ __device__ __forceinline__ uint32_t t12_addr(uint32_t a, uint32_t base, uint32_t
 }
 __device__ __forceinline__ uint32_t rot8(uint32_t e) { return ((e >> 1) | (e << 7)) & 0xFFu; }
 __device__ __forceinline__ uint32_t unrot8(uint32_t r) { return ((r << 1) | (r >> 7)) & 0xFFu; }
-// Symbol as stored in T12 / the slots: BF16 exponents rotated (the merge's bit-select trick), the
-// other value formats' exponents as they are.
+// Symbol as stored in T12 / the slots: BF16 exponents rotated (the merge's bit-select trick); the other
+// value formats' exponents pre-shifted to where the merge needs them inside their byte (FP16 and FP8
+// E5M2: e << 2, FP8 E4M3: e << 3; still < 256 and distinct, so CodeLengths by stored symbol works).
 template <uint32_t kVF>
 __device__ __forceinline__ uint32_t to_stored(uint32_t e) {
     if constexpr (kVF == DF11_VF_BF16) return rot8(e);
-    else return e & 0xFFu;
+    else if constexpr (kVF == DF11_VF_FP8_E4M3) return (e & 15u) << 3;
+    else return (e & 31u) << 2;
 }
 template <uint32_t kVF>
 __device__ __forceinline__ uint32_t from_stored(uint32_t r) {
     if constexpr (kVF == DF11_VF_BF16) return unrot8(r);
-    else return r & 0xFFu;
+    else if constexpr (kVF == DF11_VF_FP8_E4M3) return (r >> 3) & 15u;
+    else return (r >> 2) & 31u;
 }
 
 __device__ __forceinline__ void st8(uint32_t addr, uint32_t v) {
@@ -220,7 +223,10 @@ __device__ __forceinline__ bool build_t12(const df11_device_tensor &ts, uint8_t 
     if (tid < 256u) {
         len_t = __ldg(ts.code_lengths + tid);
         sb[off_len + tid] = (uint8_t)len_t;
-        sb[off_rlen + to_stored<kVF>(tid)] = (uint8_t)(len_t ? len_t : 32u);
+        // CodeLengths by stored symbol; only exponent fields of the format are symbols (their stored
+        // values are distinct: no two threads write one entry)
+        if (kVF == DF11_VF_BF16 || tid < (kVF == DF11_VF_FP8_E4M3 ? 16u : 32u))
+            sb[off_rlen + to_stored<kVF>(tid)] = (uint8_t)(len_t ? len_t : 32u);
     }
     // a 1-bit codeword allows 64 codes per chain: such tensors take the count + direct path
     safe = __syncthreads_or(len_t == 1) != 0;
