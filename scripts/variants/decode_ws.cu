@@ -10,11 +10,23 @@
 // Four groups of 256 threads per CTA.  Tensors with a 1-bit code (the count + direct path) are not
 // handled: the kernel traps (the launcher only selects it under the A/B knob).
 #include "t12_common.cuh"
+// Register redistribution knobs (round-2 follow-up, profiles/r02_ws_setmaxnreg_ab.log): -DWS_DEC_REGS=R /
+// -DWS_MRG_REGS=R make the decode / merge warpgroups setmaxnreg to R on entry to their role and back to
+// WS_BASE_REGS (the kernel's register target, 64 at 1 024 threads) before the roles rejoin; -DWS_GROUPS=3
+// gives 768 threads.  ptxas only accepts setmaxnreg here with the LUT walk inlined (a CALL inside a
+// setmaxnreg region fails register allocation).  Measured: 72 / 56 registers -1.4 %, 768 threads with
+// 96 / 64 -6 % against the plain split (itself -3 % against the product kernel).
+#ifndef WS_GROUPS
+#define WS_GROUPS 4
+#endif
+#ifndef WS_BASE_REGS
+#define WS_BASE_REGS 64
+#endif
 
 namespace df11 {
 namespace {
 
-constexpr uint32_t kGroupsWS = 4;
+constexpr uint32_t kGroupsWS = WS_GROUPS;
 constexpr uint32_t kCtaWS = 2 * kLanes * kGroupsWS;           // 1024
 constexpr uint32_t kSubWS = 10;                               // slot words per chain (see decode_sp12.cu)
 constexpr uint32_t kSlotWarp = 2 * kSubWS * 128;              // slots of one decode warp's 64 chains
@@ -123,6 +135,9 @@ __global__ void __launch_bounds__(kCtaWS, 1) ws_kernel(const __grid_constant__ B
         if (!decoder && t == 0 && tile < seg_end) stage_sm(tile - base_tile);
 
         if (decoder) {
+#ifdef WS_DEC_REGS
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_DEC_REGS));
+#endif
             // =============================== decode role
             auto walk = [&](uint32_t w, uint32_t &len) -> uint32_t {
                 if (lut_in_smem) return lut_walk_smem(w, sbase + kOffLut, sbase + kOffLen, eb_bytes, kk, 8u, len);
@@ -234,7 +249,13 @@ __global__ void __launch_bounds__(kCtaWS, 1) ws_kernel(const __grid_constant__ B
                 __syncwarp();
                 if (lane == 0) mbar_arrive(fullb + 8 * k);     // release: slots and counts of this warp
             }
+#ifdef WS_DEC_REGS
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_BASE_REGS));
+#endif
         } else {
+#ifdef WS_MRG_REGS
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_MRG_REGS));
+#endif
             // =============================== merge role
             uint32_t qq = q;
             for (; tile < seg_end; tile += kGroupsWS, qq++) {
@@ -364,6 +385,9 @@ __global__ void __launch_bounds__(kCtaWS, 1) ws_kernel(const __grid_constant__ B
                     __syncwarp();
                 }
             }
+#ifdef WS_MRG_REGS
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_BASE_REGS));
+#endif
         }
         // both roles walked the same tiles of this segment
         q += (seg_end > seg_begin + g) ? (seg_end - seg_begin - g + kGroupsWS - 1) / kGroupsWS : 0u;
