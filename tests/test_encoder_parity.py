@@ -256,3 +256,19 @@ def test_encoder_variant_fuzz_vs_oracle(oracle_mod):
         _cmp_variant(fmt, df11.encode(w, T=T, n=n, lut_mode=mode, vf=vf, lut_bits=lut_bits))
         checked += 1
     assert checked >= 30
+
+
+def test_missing_library_fails_loudly():
+    """The product path has no fallback: without the CUDA library every call raises (no oracle, no CPU
+    decode behind the binding)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np\nfrom paper_2504_11651_b200 import df11\n"
+            "try:\n    df11.encode(np.zeros(64, np.uint16))\nexcept ImportError as e:\n    print('RAISED', e)\n")
+    env = dict(os.environ, DF11_LIB="/nonexistent/libdf11.so")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "RAISED" in r.stdout and "not built" in r.stdout, r.stdout + r.stderr
+    src = open(df11.__file__).read()
+    assert "oracle" not in src.replace("# oracle", ""), "the binding must not reach oracle/"
