@@ -166,6 +166,12 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
     const uint32_t slotA = wreg + 16u + lane * 4u, slotB = slotA + kSubW * 128u;
     const uint32_t rlenb = sbase + kOffRLen;
 
+#ifndef SP12_NO_PDL
+    // programmatic dependent launch: the next decode in the stream may start its prologue (the table
+    // build, which reads only its own inputs) on SMs this grid leaves; it waits for this grid before
+    // its first output write (griddepcontrol.wait below)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     const uint32_t total = bt.total_tiles;
     const uint32_t c_begin = bt.cta_ranges ? bt.cta_start[blockIdx.x]
                                            : (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
@@ -204,6 +210,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         bool safe, lut_in_smem;
         const bool long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
                                                        kOffGrp + L::kGReg, tid, safe, lut_in_smem);
+#ifndef SP12_NO_PDL
+        asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous grid is complete and visible
+#endif
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
 
         const uint32_t N = (uint32_t)ts.num_elements;
@@ -753,8 +762,22 @@ cudaError_t launch_one(const Batch &bt, int device, uint32_t grid, cudaStream_t 
         if (e != cudaSuccess) return e;
         g_sp12_attr_set[device] |= bit;
     }
+#ifndef SP12_NO_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kCta12);
+    cfg.dynamicSmemBytes = Lay12<kVF>::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, sp12_kernel<kNB, kVF, kB8>, bt);
+#else
     sp12_kernel<kNB, kVF, kB8><<<grid, kCta12, Lay12<kVF>::kSmem, stream>>>(bt);
     return cudaGetLastError();
+#endif
 }
 
 template <bool kB8>
