@@ -127,7 +127,13 @@ void df11_host_tensor_free(df11_host_tensor *t);
  * df11_decompress: one tensor, one launch.  df11_decompress_block: every tensor of a transformer
  * block in ONE launch (count <= DF11_MAX_BATCH; empty tensors allowed).  On a validation error the
  * message names the offending descriptor index (df11_last_error_message()).  `stream` is a
- * cudaStream_t. */
+ * cudaStream_t.  Stream semantics: the product kernel is launched as a programmatic dependent launch,
+ * so when it directly follows another product-kernel decode on the same stream it may start reading
+ * its OWN inputs (LUTs, CodeLengths, BlockOutputPos, the first stream chunks) while that decode is
+ * still running; it writes its outputs only after that decode has completed (griddepcontrol.wait).
+ * Every other predecessor (copies, events, other kernels) is waited for in full, as usual.  A decode
+ * must therefore not take as input a buffer that the immediately preceding decode on its stream
+ * writes (no DF11 input is ever a decode output). */
 df11_status df11_decompress(const df11_device_tensor *t, void *stream);
 df11_status df11_decompress_block(const df11_device_tensor *ts, uint32_t count, void *stream);
 /* Same with an explicit kernel: DF11_KERNEL_ALG1 (literal Alg. 1, any valid T/n) or DF11_KERNEL_FAST
