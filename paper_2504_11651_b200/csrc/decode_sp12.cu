@@ -168,8 +168,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
 
 #ifndef SP12_NO_PDL
     // programmatic dependent launch: the next decode in the stream may start its prologue (the table
-    // build, which reads only its own inputs) on SMs this grid leaves; it waits for this grid before
-    // its first output write (griddepcontrol.wait below)
+    // build and the decode of its first tiles, which read only its own inputs) on SMs this grid leaves;
+    // it waits for this grid before its first global write (griddepcontrol.wait after each tile's scan
+    // barrier; -DSP12_PDL_EARLY: after the table build instead)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
     const uint32_t total = bt.total_tiles;
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         bool safe, lut_in_smem;
         const bool long_codes = build_t12<kCta12, kVF, kB8>(ts, sb, sbase, kOffT, kOffLut, kOffLen, kOffRLen,
                                                        kOffGrp + L::kGReg, tid, safe, lut_in_smem);
-#ifndef SP12_NO_PDL
+#if !defined(SP12_NO_PDL) && defined(SP12_PDL_EARLY)
         asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous grid is complete and visible
 #endif
         const uint32_t eb_bytes = ts.lut_entry_bytes, kk = ts.k;
@@ -482,6 +483,9 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             const uint32_t ws = gbase + L::kGWsum + parity * (kWarps12 * 4);
             if (lane == 31) sts32(ws + wig * 4, incl);
             group_bar(g);                          // also: every thread has read this tile's stage
+#if !defined(SP12_NO_PDL) && !defined(SP12_PDL_EARLY)
+            asm volatile("griddepcontrol.wait;" ::: "memory");   // before this tile's first global write
+#endif
             parity ^= 1u;
             if (t == 0 && has_next) {
                 if constexpr (kNB == 8) issue_tile(ts, b + kGroups12, stage, mbar);
