@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
             const uint32_t ws = gbase + L::kGWsum + parity * (kWarps12 * 4);
             if (lane == 31) sts32(ws + wig * 4, incl);
             group_bar(g);                          // also: every thread has read this tile's stage
-#if !defined(SP12_NO_PDL) && !defined(SP12_PDL_EARLY)
+#if !defined(SP12_NO_PDL) && !defined(SP12_PDL_EARLY) && !defined(SP12_PDL_NOWAIT)   // NOWAIT: negative test only
             asm volatile("griddepcontrol.wait;" ::: "memory");   // before this tile's first global write
 #endif
             parity ^= 1u;

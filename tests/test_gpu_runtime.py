@@ -152,3 +152,46 @@ def test_compress_blocks_llama_bit_exact(dtype):
     assert torch.equal(out, ref)
     for h in hooks:
         h.remove()
+
+
+def test_back_to_back_decodes_into_one_buffer():
+    """The product kernel is a programmatic dependent launch (df11.h stream semantics): a decode that
+    follows a decode on the same stream may read its own inputs early but must not write before the
+    previous decode is complete.  Write-after-write through one output buffer, no host sync in between:
+    a large decode (58.7 M elements) followed by a small one into the tail of the same buffer (the
+    region the large decode writes last), and two equal-size tensors alternating; the last decode's values must survive every time.
+    (A regression check: a build without the wait, -DSP12_PDL_NOWAIT, also passed on B200 - the second
+    decode's table build outlasts the first one's CTA-exit spread - so the wait is required by the PTX
+    memory model, not caught by timing.)"""
+    from paper_2504_11651_b200 import df11
+    dev = torch.device("cuda", 0)
+    big = workloads.gaussian_bf16((14336, 4096), workloads.seed_for("pdl", 0, "big"))
+    small = workloads.gaussian_bf16((1 << 20,), workloads.seed_for("pdl", 0, "small"), sigma=0.05)
+    other = workloads.gaussian_bf16((14336, 4096), workloads.seed_for("pdl", 1, "big"), sigma=0.01)
+    d_big, d_small, d_other = (df11.to_device(df11.encode(w), dev) for w in (big, small, other))
+    buf = torch.empty(big.size, dtype=torch.bfloat16, device=dev)
+    ref_small = torch.from_numpy(small.view(np.int16)).to(dev)
+    ref_big = torch.from_numpy(big.reshape(-1).view(np.int16)).to(dev)
+    ref_other = torch.from_numpy(other.reshape(-1).view(np.int16)).to(dev)
+    # the small decodes target the tail of the buffer, which the big decode's last CTA writes last:
+    # one tile (4 096 elements, one CTA that starts on the first SM the big decode frees) and 1 M
+    tiny = workloads.gaussian_bf16((4096,), workloads.seed_for("pdl", 0, "tiny"), sigma=0.05)
+    d_tiny = df11.to_device(df11.encode(tiny), dev)
+    ref_tiny = torch.from_numpy(tiny.view(np.int16)).to(dev)
+    bad = 0
+    for i in range(40):
+        df11.decompress(d_big, out=buf)
+        if i % 2:
+            df11.decompress(d_small, out=buf[-small.size:])
+            bad += not torch.equal(buf[-small.size:].view(torch.int16), ref_small)
+        else:
+            df11.decompress(d_tiny, out=buf[-tiny.size:])
+            bad += not torch.equal(buf[-tiny.size:].view(torch.int16), ref_tiny)
+    torch.cuda.synchronize()
+    assert bad == 0, f"{bad} of 40 back-to-back pairs lost the second decode's values"
+    assert torch.equal(buf[: -small.size].view(torch.int16), ref_big[: -small.size])
+    for i in range(21):
+        df11.decompress(d_other if i % 2 == 0 else d_big, out=buf)
+    torch.cuda.synchronize()
+    assert torch.equal(buf.view(torch.int16), ref_other)
+    assert df11.lib().df11_last_kernel_mask() & 2, "the product kernel ran"
