@@ -458,7 +458,10 @@ def main():
                                          "p90": float(np.percentile(launch_ms, 90)) * 1e3},
                 "note": "achieved = (DF11 bytes read + BF16 bytes written) per launch / the average launch "
                         "duration over the timed region (CUDA events around the K back-to-back launches, slowest "
-                        "rank); launch_us_event_pass: a separate pass with events around every launch"}
+                        "rank); consecutive launches overlap (programmatic dependent launch: the next "
+                        "decode's table build and first tile run under the previous decode's tail, its "
+                        "writes wait for it); launch_us_event_pass: a separate pass with events around "
+                        "every launch, which serialises them"}
 
     # ---- the same K steps captured in ONE CUDA graph and replayed (the C ABI is graph-capturable):
     # shorter launch gaps; reported beside the eager headline, not instead of it
