@@ -195,3 +195,37 @@ def test_back_to_back_decodes_into_one_buffer():
     torch.cuda.synchronize()
     assert torch.equal(buf.view(torch.int16), ref_other)
     assert df11.lib().df11_last_kernel_mask() & 2, "the product kernel ran"
+
+
+def test_decodes_captured_in_cuda_graph():
+    """Block decodes captured in a CUDA graph (the dependent launches become graph edges) replay
+    bit-exactly, including back-to-back decodes through one output buffer."""
+    from paper_2504_11651_b200 import df11
+    dev = torch.device("cuda", 0)
+    ws = [workloads.gaussian_bf16(sh, workloads.seed_for("graph", 0, str(i)))
+          for i, sh in enumerate([(4096, 4096), (1024, 4096), (14336, 512), (3, 1000)])]
+    dts = [df11.to_device(df11.encode(w), dev) for w in ws]
+    refs = [torch.from_numpy(w.reshape(-1).view(np.int16)).to(dev) for w in ws]
+    shared = torch.empty(ws[0].size, dtype=torch.bfloat16, device=dev)
+    plan = df11.BlockPlan(dts)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):                      # warm-up outside the capture (attributes, LUT copies)
+        plan.run(stream=s)
+        df11.decompress(dts[1], out=shared[: ws[1].size], stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.run(stream=s)
+        df11.decompress(dts[0], out=shared, stream=s)
+        df11.decompress(dts[1], out=shared[: ws[1].size], stream=s)
+    for _ in range(3):
+        for o in plan.outputs():
+            o.view(torch.int16).zero_()
+        shared.view(torch.int16).fill_(-1)
+        g.replay()
+        torch.cuda.synchronize()
+        for o, r in zip(plan.outputs(), refs):
+            assert torch.equal(o.reshape(-1).view(torch.int16), r)
+        assert torch.equal(shared[: ws[1].size].view(torch.int16), refs[1])
+        assert torch.equal(shared[ws[1].size:].view(torch.int16), refs[0][ws[1].size:])
