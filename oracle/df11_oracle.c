@@ -62,9 +62,12 @@ uint16_t df11o_compose(uint8_t exponent, uint8_t packed_sign_mantissa)
  *   vf 1 FP16 (IEEE binary16)  16 bits: sign 15, exponent 14..10 (5 bits), mantissa 9..0 (10 bits)
  *   vf 2 FP8 E4M3              8 bits:  sign 7,  exponent 6..3   (4 bits), mantissa 2..0 (3 bits)
  *   vf 3 FP8 E5M2              8 bits:  sign 7,  exponent 6..2   (5 bits), mantissa 1..0 (2 bits)
- * Residual of element i: r = sign << M | mantissa (R = 1 + M bits), stored MSB-first at bits
- * [R*i, R*i + R) of PackedSignMantissa (R25).  For BF16, R = 8 and byte i is sign << 7 | mantissa:
- * the paper's layout. */
+ * Residual of element i: r = sign << M | mantissa (R = 1 + M bits) in PackedSignMantissa (R25):
+ *   R >= 8 (BF16, FP16): the low 8 bits of r are byte i of a byte plane of roundup(n, 16) bytes; the
+ *            R - 8 high bits follow in a bit plane, MSB-first at bits [(R-8) i, (R-8) i + R - 8).
+ *            For BF16 (R = 8) the bit plane is empty and byte i is sign << 7 | mantissa: the paper's
+ *            layout.
+ *   R < 8  (FP8): r MSB-first at bits [R i, R i + R). */
 static const int VF_WORD_BITS[4] = {16, 16, 8, 8};
 static const int VF_EXP_BITS[4] = {8, 5, 4, 5};
 static const int VF_MAN_BITS[4] = {7, 10, 3, 2};
@@ -81,7 +84,32 @@ static uint32_t word_at(const void *w, int vf, uint64_t i)
 static void put_bits(uint8_t *buf, uint64_t bit, uint32_t v, int nbits);
 static uint32_t get_bits(const uint8_t *buf, uint64_t nbytes, uint64_t bit, int nbits);
 
-/* `residual` must be zeroed and hold ceil(R*n/8) bytes. */
+/* bytes of the byte plane of n residuals (R >= 8), 0 otherwise */
+static uint64_t byte_plane_bytes(int R, uint64_t n) { return R >= 8 ? (n + 15) / 16 * 16 : 0; }
+
+static void put_residual(uint8_t *buf, int R, uint64_t n, uint64_t i, uint32_t r)
+{
+    if (R >= 8) {
+        buf[i] = (uint8_t)(r & 0xFFu);
+        if (R > 8) put_bits(buf + byte_plane_bytes(R, n), (uint64_t)(R - 8) * i, r >> 8, R - 8);
+    } else {
+        put_bits(buf, (uint64_t)R * i, r, R);
+    }
+}
+
+static uint32_t get_residual(const uint8_t *buf, uint64_t nbytes, int R, uint64_t n, uint64_t i)
+{
+    if (R >= 8) {
+        uint32_t lo = i < nbytes ? buf[i] : 0u;
+        if (R == 8) return lo;
+        uint64_t hb = byte_plane_bytes(R, n);
+        uint32_t hi = hb < nbytes ? get_bits(buf + hb, nbytes - hb, (uint64_t)(R - 8) * i, R - 8) : 0u;
+        return (hi << 8) | lo;
+    }
+    return get_bits(buf, nbytes, (uint64_t)R * i, R);
+}
+
+/* `residual` must be zeroed and hold the array described above. */
 void df11o_split_v(const void *w, uint64_t n, int vf, uint8_t *exponent, uint8_t *residual)
 {
     int M = VF_MAN_BITS[vf], E = VF_EXP_BITS[vf], R = 1 + M;
@@ -91,7 +119,7 @@ void df11o_split_v(const void *w, uint64_t n, int vf, uint8_t *exponent, uint8_t
         uint32_t expo = (word >> M) & ((1u << E) - 1u);
         uint32_t mant = word & ((1u << M) - 1u);
         exponent[i] = (uint8_t)expo;
-        put_bits(residual, (uint64_t)R * i, (sign << M) | mant, R);
+        put_residual(residual, R, n, i, (sign << M) | mant);
     }
 }
 
@@ -234,14 +262,14 @@ static uint32_t read_gap(const uint8_t *gaps, uint64_t gaps_bytes, uint64_t g)
  * the codeword is complete and names symbol sorted[offset[l] + code - first_code[l]].
  * Returns 0 on success, -1 if the stream runs out (corrupt), -2 on a malformed codebook. */
 int df11o_decode_sequential_range(const uint8_t *stream, uint64_t stream_bytes, const uint8_t *code_len /*256*/,
-                                  const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t start_bit,
-                                  uint64_t first, uint64_t n, int vf, void *out);
+                                  const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t total,
+                                  uint64_t start_bit, uint64_t first, uint64_t n, int vf, void *out);
 
 int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const uint8_t *code_len /*256*/,
                             const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t n, int vf,
                             void *out)
 {
-    return df11o_decode_sequential_range(stream, stream_bytes, code_len, packed_sign_mantissa, psm_bytes, 0, 0, n,
+    return df11o_decode_sequential_range(stream, stream_bytes, code_len, packed_sign_mantissa, psm_bytes, n, 0, 0, n,
                                          vf, out);
 }
 
@@ -249,8 +277,8 @@ int df11o_decode_sequential(const uint8_t *stream, uint64_t stream_bytes, const 
  * `first`, for n elements.  A format block b's first code starts at bit 8nT*b + Gaps[bT] and is element
  * BlockOutputPos[b], so the blocks of a tensor can be decoded independently. */
 int df11o_decode_sequential_range(const uint8_t *stream, uint64_t stream_bytes, const uint8_t *code_len /*256*/,
-                                  const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t start_bit,
-                                  uint64_t first, uint64_t n, int vf, void *out)
+                                  const uint8_t *packed_sign_mantissa, uint64_t psm_bytes, uint64_t total,
+                                  uint64_t start_bit, uint64_t first, uint64_t n, int vf, void *out)
 {
     const int R = 1 + VF_MAN_BITS[vf];
     uint32_t count[33] = {0};
@@ -297,7 +325,7 @@ int df11o_decode_sequential_range(const uint8_t *stream, uint64_t stream_bytes, 
                 found = sorted[offset[l] + (uint32_t)(c - first_code[l])];
         }
         store_word(out, vf, i, df11o_compose_v(vf, (uint32_t)found,
-                                               get_bits(packed_sign_mantissa, psm_bytes, (uint64_t)R * i, R)));
+                                               get_residual(packed_sign_mantissa, psm_bytes, R, total, i)));
     }
     return 0;
 }
@@ -406,8 +434,8 @@ int df11o_decode_alg1(const uint8_t *luts, uint32_t entry_bytes, uint32_t k, uin
                 if (e < 0 || code_len[e] == 0 || e >= (1 << VF_EXP_BITS[vf])) { rc = -4; break; }
                 if (pos < bop[b + 1] && pos < N)
                     store_word(out, vf, pos, df11o_compose_v(vf, (uint32_t)e,
-                                                             get_bits(packed_sign_mantissa, psm_bytes,
-                                                                      (uint64_t)R * pos, R)));
+                                                             get_residual(packed_sign_mantissa, psm_bytes, R, N,
+                                                                          pos)));
                 bit_offset += code_len[e];
                 pos++;
             }

@@ -65,7 +65,7 @@ def _load():
         lib.df11o_pack_gaps.argtypes = [P, U64, P]
         lib.df11o_decode_sequential.argtypes = [P, U64, P, P, U64, U64, I, P]
         lib.df11o_decode_sequential.restype = I
-        lib.df11o_decode_sequential_range.argtypes = [P, U64, P, P, U64, U64, U64, U64, I, P]
+        lib.df11o_decode_sequential_range.argtypes = [P, U64, P, P, U64, U64, U64, U64, U64, I, P]
         lib.df11o_decode_sequential_range.restype = I
         lib.df11o_decode_alg1.argtypes = [P, U32, U32, U32, P, P, U64, P, U64, P, P, U64, U32, U32, U32, U64, I, I,
                                           P]
@@ -97,7 +97,12 @@ def residual_bits(vf) -> int:
 
 
 def residual_array_bytes(N: int, vf) -> int:
+    """PackedSignMantissa bytes (R25): R >= 8: a byte plane of roundup(N, 16) bytes + the (R - 8)-bit
+    plane rounded to 16 bytes; R < 8: one R-bit plane rounded to 16 bytes; + 16 bytes of zero pad."""
     R = residual_bits(vf)
+    if R >= 8:
+        L = _roundup(N, 16)
+        return L + _roundup((R - 8) * L // 8, 16) + 16
     return _roundup(R * _roundup(N, 16) // 8, 16) + 16
 
 
@@ -277,7 +282,8 @@ def decode_sequential_blocks(fmt: dict, b0: int, b1: int, out: np.ndarray) -> No
     start = 8 * n * T * b0 + _read_gap(fmt["gaps"], b0 * T)
     s, psm = fmt["encoded_exponent"], fmt["packed_sign_mantissa"]
     rc = _load().df11o_decode_sequential_range(_ptr(s), s.size, _ptr(fmt["code_lengths"]), _ptr(psm), psm.size,
-                                               start, first, last - first, _vf(fmt), _ptr(out))
+                                               int(fmt["num_elements"]), start, first, last - first, _vf(fmt),
+                                               _ptr(out))
     if rc != 0:
         raise FormatError("corrupt", f"sequential decode failed ({rc})")
 
@@ -341,11 +347,18 @@ def decode_alg1_blocks(fmt: dict, blocks) -> dict:
         _load().df11o_pack_gaps(_ptr(gv), T, _ptr(gaps))
         bop = np.array([0, hi - lo], np.uint32)
         R = residual_bits(_vf(fmt))
-        psm = np.zeros(residual_array_bytes(hi - lo, _vf(fmt)), np.uint8)
-        if R == 8:
-            psm[: hi - lo] = fmt["packed_sign_mantissa"][lo:hi]
+        n_sub = hi - lo
+        psm = np.zeros(residual_array_bytes(n_sub, _vf(fmt)), np.uint8)
+        src = fmt["packed_sign_mantissa"]
+        if R >= 8:                # byte plane slice, then the (R - 8)-bit plane re-aligned to bit 0
+            psm[:n_sub] = src[lo:hi]
+            if R > 8:
+                Lfull, Lsub = _roundup(int(fmt["num_elements"]), 16), _roundup(n_sub, 16)
+                bits = np.unpackbits(src[Lfull:])[(R - 8) * lo: (R - 8) * hi]
+                packed = np.packbits(bits)
+                psm[Lsub: Lsub + packed.size] = packed
         else:                     # the block's residual bits [R lo, R hi), re-aligned to bit 0
-            bits = np.unpackbits(fmt["packed_sign_mantissa"])[R * lo: R * hi]
+            bits = np.unpackbits(src)[R * lo: R * hi]
             packed = np.packbits(bits)
             psm[: packed.size] = packed
         sub = dict(fmt, num_elements=hi - lo, B=1, encoded_exponent=stream, gaps=gaps,

@@ -53,14 +53,24 @@ def _fields_from_value(vf, v):
 
 
 def _residual_fields(res, R, n):
-    bits = np.unpackbits(res)[: R * n].reshape(n, R)
-    return bits.dot(1 << np.arange(R - 1, -1, -1))
+    """Read the residuals back by the R25 layout: R >= 8: byte plane of the low 8 bits (roundup(n, 16)
+    bytes) + the (R - 8)-bit plane MSB-first; R < 8: one R-bit plane MSB-first."""
+    def plane(buf, r):
+        bits = np.unpackbits(buf)[: r * n].reshape(n, r)
+        return bits.dot(1 << np.arange(r - 1, -1, -1)).astype(np.int64)
+    if R < 8:
+        return plane(res, R)
+    lo = res[:n].astype(np.int64)
+    if R == 8:
+        return lo
+    L = (n + 15) // 16 * 16
+    return (plane(res[L:], R - 8) << 8) | lo
 
 
 @pytest.mark.parametrize("vf", sorted(FORMATS))
 def test_split_v_against_values(oracle_mod, vf):
-    """Every bit pattern: exponent symbol and residual (sign << M | mantissa, R bits MSB-first at
-    R*i) equal the fields recovered from the numpy/torch value; infinities and NaNs by class."""
+    """Every bit pattern: exponent symbol and residual (sign << M | mantissa, stored by the R25 layout)
+    equal the fields recovered from the numpy/torch value; infinities and NaNs by class."""
     W, E, M, bias = FORMATS[vf]
     words = workloads.all_patterns(vf)
     exp, res = oracle_mod.split_v(words, vf)
