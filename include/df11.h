@@ -41,9 +41,11 @@ enum { DF11_LUT_AUTO = 0, DF11_LUT_NARROW = 1, DF11_LUT_WIDE = 2 };
 
 /* Value formats (NEXT-4; DESIGN.md §2 and R25-R27).  The paper codes BF16; P:609 names
  * FP16 and FP8 as its limitation.  Every format is split the same way: the exponent field is the
- * Huffman symbol, and the residual r = sign << M | mantissa (R = 1 + M bits) is stored raw, MSB-first
- * at bits [R*i, R*i + R) of PackedSignMantissa (for BF16, R = 8: one byte per element, sign in bit 7,
- * mantissa in bits 6..0, the paper's layout P:430-431).
+ * Huffman symbol, and the residual r = sign << M | mantissa (R = 1 + M bits) is stored raw in
+ * PackedSignMantissa: BF16 (R = 8) one byte per element, sign in bit 7, mantissa in bits 6..0 (the
+ * paper's layout); FP16 (R = 11) the low 8 bits of r as a byte plane of roundup(N, 16) bytes,
+ * then the 3 high bits (sign, m9, m8) MSB-first at bits [3i, 3i + 3) of a plane after it; FP8 (R = 4 / 3)
+ * r MSB-first at bits [R*i, R*i + R).
  *   BF16      16-bit words, exponent bits 14..7  (8), R = 8
  *   FP16      16-bit words, exponent bits 14..10 (5), R = 11
  *   FP8_E4M3  8-bit words,  exponent bits 6..3   (4), R = 4
@@ -81,8 +83,9 @@ typedef struct {
     uint8_t  code_lengths[256];            /* CodeLengths */
     uint8_t  *luts;              uint64_t luts_bytes;                  /* k*2^b*lut_entry_bytes; table 0 = root */
     uint8_t  *encoded_exponent;  uint64_t encoded_exponent_bytes;      /* B*T*n + 16 */
-    uint8_t  *packed_sign_mantissa; uint64_t packed_sign_mantissa_bytes; /* roundup(R*roundup(N,16)/8,16) + 16
-                                                                            (BF16: roundup(N,16) + 16) */
+    uint8_t  *packed_sign_mantissa; uint64_t packed_sign_mantissa_bytes; /* FP8: roundup(R*roundup(N,16)/8,16) + 16;
+                                                                            BF16: roundup(N,16) + 16; FP16:
+                                                                            roundup(N,16) + roundup(3*roundup(N,16)/8,16) + 16 */
     uint8_t  *gaps;              uint64_t gaps_bytes;                  /* roundup(ceil(5BT/8),16) + 16 */
     uint32_t *block_output_pos;                                        /* B+1 entries, [B] = N */
 } df11_host_tensor;

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(1024) alg1_kernel(const __grid_constant__ Batc
         uint32_t len;
         uint32_t e = decode_one(window(bit_offset), len);
         if (pos < bop_hi) {
-            const uint16_t v = (uint16_t)compose_vf(vf, e, load_residual(vf, ts.packed_sign_mantissa, pos));
+            const uint16_t v = (uint16_t)compose_vf(vf, e, load_residual(vf, ts.packed_sign_mantissa, pos, ts.num_elements));
             if (kUseWriteBuffer) s_wbuf[pos - bop_lo] = v;
             else store_word(vf, ts.out, pos, v);
         }

@@ -51,8 +51,8 @@ __host__ __device__ __forceinline__ uint32_t lut_bits_of(const df11_device_tenso
 #endif
 }
 
-// Value formats (df11.h DF11_VF_*, R25): M mantissa bits, E exponent bits, residual R = 1 + M bits at
-// PackedSignMantissa bits [R*i, R*i + R), words of 2 (BF16/FP16) or 1 (FP8) bytes.
+// Value formats (df11.h DF11_VF_*, R25): M mantissa bits, E exponent bits, residual R = 1 + M bits in
+// PackedSignMantissa (load_residual), words of 2 (BF16/FP16) or 1 (FP8) bytes.
 struct VF {
     uint32_t M, E, R, emask, word_bytes;
 };
@@ -68,9 +68,18 @@ __host__ __device__ constexpr VF vf_of(uint32_t value_format) {
 __device__ __forceinline__ uint32_t compose_vf(const VF &f, uint32_t e, uint32_t r) {
     return ((r >> f.M) << (f.E + f.M)) | ((e & f.emask) << f.M) | (r & ((1u << f.M) - 1u));
 }
-// Residual of element i: R bits MSB-first at bit R*i (R <= 11: inside a 3-byte window).
-__device__ __forceinline__ uint32_t load_residual(const VF &f, const uint8_t *__restrict__ psm, uint64_t i) {
+// Residual of element i of a tensor of n elements (R25): R = 8 (BF16) byte i; R = 11 (FP16) byte i of the
+// byte plane (low 8 bits) + the 3 high bits at bit 3i of the plane after roundup(n, 16) bytes; R < 8
+// (FP8) R bits MSB-first at bit R*i.
+__device__ __forceinline__ uint32_t load_residual(const VF &f, const uint8_t *__restrict__ psm, uint64_t i,
+                                                  uint64_t n) {
     if (f.R == 8) return __ldg(psm + i);
+    if (f.R == 11) {
+        const uint64_t bit = 3ull * i;
+        const uint8_t *p = psm + ((n + 15) & ~15ull) + (bit >> 3);
+        const uint32_t v = ((uint32_t)__ldg(p) << 8) | __ldg(p + 1);   // 3 bits inside 2 bytes
+        return (((v >> (13u - (uint32_t)(bit & 7))) & 7u) << 8) | __ldg(psm + i);
+    }
     const uint64_t bit = (uint64_t)f.R * i;
     const uint8_t *p = psm + (bit >> 3);
     const uint32_t v = ((uint32_t)__ldg(p) << 16) | ((uint32_t)__ldg(p + 1) << 8) | __ldg(p + 2);

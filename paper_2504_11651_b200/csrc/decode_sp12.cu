@@ -58,9 +58,11 @@ constexpr uint32_t kOffLen = kOffLut + kLutSmem;                    // CodeLengt
 constexpr uint32_t kOffRLen = kOffLen + 256;                        // CodeLengths[stored symbol]
 constexpr uint32_t kOffGrp = kOffRLen + 256;                        // [groups][kGrpBytes]
 // PackedSignMantissa bytes of one tile staged in SMEM: BF16 ~6.3 KB per tile on LLM weights; FP16
-// (11-bit residuals, NEXT-4) ~8.7 KB: it takes the SMEM left over (tiles above the cap read their
+// (byte plane + 3-bit plane, NEXT-4) ~8.7 KB: it takes the SMEM left over (tiles above the cap read their
 // residuals through L1/L2 instead)
 constexpr uint32_t sm_cap(uint32_t vf) { return vf == DF11_VF_FP16 ? 11200u : 7168u; }
+// FP16 (R25): the tile's byte plane is staged at [0, kFp16HiOff) of the buffer, its 3-bit plane after it
+constexpr uint32_t kFp16HiOff = 8000u;
 // one block per group, so that every per-group / per-warp address is one base register plus an
 // immediate offset
 template <uint32_t kVF>
@@ -83,29 +85,25 @@ struct Lay12 {
 
 // ---- merge helpers of the value formats other than BF16 (NEXT-4, R25): a unit is 16 output bytes
 // (8 FP16 / 16 FP8 words) and its residuals are R * (unit words) / 8 bytes at SMEM byte address o.
-// Eight FP16 words from 8 exponents (bytes of x0, x1) and eight 11-bit residuals s << 10 | m at o.
-__device__ __forceinline__ uint4 unit_fp16(uint32_t x0, uint32_t x1, uint32_t o) {
-    const uint32_t base = o & ~3u, ro = o & 3u;
-    const uint32_t L0 = lds32(base), L1 = lds32(base + 4), L2 = lds32(base + 8);
-    uint32_t L3 = 0;
-    if (ro >= 2) L3 = lds32(base + 12);                // 11 bytes from byte 2 or 3 reach a 4th word
-    // big-endian 32-bit windows at bytes r, r + 4, r + 8: one PRMT each (selector 0x0123 + r * 0x1111)
-    const uint32_t sel = 0x0123u + ro * 0x1111u;
-    const uint32_t H0 = prmt(L0, L1, sel), H1 = prmt(L1, L2, sel), H2 = prmt(L2, L3, sel);   // 88 bits, MSB-first
-    // pair p = residual bits [22p, 22p + 22) as a 32-bit window G (MSB-first): element 2p in G's bits
-    // 31..21, element 2p + 1 in bits 20..10.  F puts them into the two 16-bit halves; a word is then
-    // (s << 15 | m) per half plus the exponents, which PRMT places at bits 10 / 26 from x << 2.
-    auto pair = [](uint32_t G, uint32_t E10) {
-        const uint32_t F = (G >> 21) | ((G << 6) & 0x07FF0000u);
-        return ((F << 5) & 0x80008000u) | (F & 0x03FF03FFu) | E10;
-    };
-    const uint32_t y0 = x0, y1 = x1;                      // stored exponents are e << 2 (to_stored)
-    uint4 r;
-    r.x = pair(H0, prmt(y0, 0u, 0x1404u));
-    r.y = pair(__funnelshift_l(H1, H0, 22), prmt(y0, 0u, 0x3424u));
-    r.z = pair(__funnelshift_l(H2, H1, 12), prmt(y1, 0u, 0x1404u));
-    r.w = pair(H2 << 2, prmt(y1, 0u, 0x3424u));
-    return r;
+// Eight FP16 words from 8 stored exponents (bytes of x0, x1: e << 2), their 8 low residual bytes
+// (byte plane, s0 / s1) and their 3-bit high fields (sign, m9, m8) as 3 whole bytes at SMEM address h
+// (R25).  Per 4 words: the 3-bit fields spread to bytes (W), W * 0x21 puts the sign at bit 7 next to
+// m9 m8 at bits 1..0, the exponent byte is ORed in, and one PRMT interleaves high and low bytes.
+__device__ __forceinline__ uint4 unit_fp16(uint32_t x0, uint32_t x1, uint32_t s0, uint32_t s1, uint32_t h) {
+    const uint32_t base = h & ~3u, r = h & 3u;
+    const uint32_t L0 = lds32(base);
+    uint32_t L1 = 0;
+    if (r >= 2) L1 = lds32(base + 4);                  // 3 bytes from byte 2 or 3 reach the next word
+    const uint32_t H = prmt(L0, L1, 0x0123u + r * 0x1111u);   // the 24 bits MSB-first in H's bits 31..8
+    const uint32_t W0 = (H >> 29) | ((H >> 18) & 0x700u) | ((H >> 7) & 0x70000u) | ((H << 4) & 0x7000000u);
+    const uint32_t W1 = ((H >> 17) & 7u) | ((H >> 6) & 0x700u) | ((H << 5) & 0x70000u) | ((H << 16) & 0x7000000u);
+    const uint32_t Y0 = ((W0 * 0x21u) & 0x83838383u) | x0, Y1 = ((W1 * 0x21u) & 0x83838383u) | x1;
+    uint4 o;
+    o.x = prmt(s0, Y0, 0x5140u);
+    o.y = prmt(s0, Y0, 0x7362u);
+    o.z = prmt(s1, Y1, 0x5140u);
+    o.w = prmt(s1, Y1, 0x7362u);
+    return o;
 }
 // Four FP8 E4M3 bytes from 4 exponents E and the nibbles of residual bytes (b_lo, b_hi) of word r
 // (element 2j in the high nibble of byte j): s << 7 | e << 3 | m.
@@ -225,20 +223,43 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
         // it fits kSmCap; otherwise it is prefetched into L2 and read with LDG in the merge.
         const bool psm_al = (reinterpret_cast<uintptr_t>(ts.packed_sign_mantissa) & 15) == 0;   // bulk copies
         const bool sm_tma = vec_out && !safe && psm_al;
-        // [a0, a1): bytes of the residuals of outputs [l & ~15, (h + 15) & ~15), widened to 16 bytes
+        // [a0, a1): bytes of the residuals of outputs [l & ~15, (h + 15) & ~15), widened to 16 bytes.
+        // FP16 (R25): [a0, a1) is the byte-plane range; its 3-bit plane range is [hib + q0, hib + q1)
+        // with q0 = (3 a0 / 8) & ~15, q1 = roundup(3 a1 / 8, 16), staged at smb + kFp16HiOff.
+        const uint32_t hib = (N + 15u) & ~15u;
         auto sm_range = [&](uint32_t plo, uint32_t phi, uint32_t &a0, uint32_t &a1) {
             const uint32_t l = min(plo, N), h = min(max(min(phi, N), l), l + 8 * kN * kT);
-            a0 = ((l & ~15u) / 8u * kRb) & ~15u;
-            a1 = (((h + 15u) & ~15u) / 8u * kRb + 15u) & ~15u;
-            return sm_tma && a1 > a0 && a1 - a0 <= L::kSmCap;
+            if constexpr (kVF == DF11_VF_FP16) {
+                a0 = l & ~15u;
+                a1 = (h + 15u) & ~15u;
+                const uint32_t q0 = (a0 / 8u * 3u) & ~15u, q1 = (a1 / 8u * 3u + 15u) & ~15u;
+                return sm_tma && a1 > a0 && a1 - a0 <= kFp16HiOff && q1 - q0 <= L::kSmCap - kFp16HiOff;
+            } else {
+                a0 = ((l & ~15u) / 8u * kRb) & ~15u;
+                a1 = (((h + 15u) & ~15u) / 8u * kRb + 15u) & ~15u;
+                return sm_tma && a1 > a0 && a1 - a0 <= L::kSmCap;
+            }
         };
         auto stage_sm = [&](uint32_t plo, uint32_t phi) {
             uint32_t a0, a1;
-            if (sm_range(plo, phi, a0, a1)) {
-                mbar_expect_tx(smbar, a1 - a0);
-                tma_g2s(smb, ts.packed_sign_mantissa + a0, a1 - a0, smbar);
-            } else if (a1 > a0 && psm_al) {
-                prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
+            const bool fits = sm_range(plo, phi, a0, a1);
+            if constexpr (kVF == DF11_VF_FP16) {
+                const uint32_t q0 = (a0 / 8u * 3u) & ~15u, q1 = (a1 / 8u * 3u + 15u) & ~15u;
+                if (fits) {
+                    mbar_expect_tx(smbar, (a1 - a0) + (q1 - q0));
+                    tma_g2s(smb, ts.packed_sign_mantissa + a0, a1 - a0, smbar);
+                    tma_g2s(smb + kFp16HiOff, ts.packed_sign_mantissa + hib + q0, q1 - q0, smbar);
+                } else if (a1 > a0 && psm_al) {
+                    prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
+                    prefetch_l2(ts.packed_sign_mantissa + hib + q0, q1 - q0);
+                }
+            } else {
+                if (fits) {
+                    mbar_expect_tx(smbar, a1 - a0);
+                    tma_g2s(smb, ts.packed_sign_mantissa + a0, a1 - a0, smbar);
+                } else if (a1 > a0 && psm_al) {
+                    prefetch_l2(ts.packed_sign_mantissa + a0, a1 - a0);
+                }
             }
         };
         if (t == 0 && tile < seg_end) stage_sm(nlo, nhi);
@@ -518,7 +539,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                             lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
                             if ((eh & 0xFFFFu) != 0) { sym = from_stored<kVF>(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
                             else sym = walk(a, len);
-                            out[p] = (OutT)compose_vf(kF, sym, load_residual(kF, ts.packed_sign_mantissa, p));
+                            out[p] = (OutT)compose_vf(kF, sym, load_residual(kF, ts.packed_sign_mantissa, p, N));
                             p++;
                             off += len;
                             shift96_long(a, bb, c, len);
@@ -532,7 +553,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                         lds64(t12_addr(a, tab, K_ROW, K_TOP, K_ENT), el, eh);
                         if ((eh & 0xFFFFu) != 0) { sym = from_stored<kVF>(el & 0xFFu); len = ld8(rlenb + (el & 0xFFu)); }
                         else sym = walk(a, len);
-                        out[p] = (OutT)compose_vf(kF, sym, load_residual(kF, ts.packed_sign_mantissa, p));
+                        out[p] = (OutT)compose_vf(kF, sym, load_residual(kF, ts.packed_sign_mantissa, p, N));
                         p++;
                         off += len;
                         shift160_long_ones(a, b1, c, d, e, len);
@@ -642,22 +663,26 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     for (; k < nfull; k++) unit(k);
                     if (lane < (nun & 31u)) unit(nfull);
                 } else {
-                    // other value formats (NEXT-4): residual bits of output e at bit kRb * e - 8 * a0
-                    if (edge)
-                        out[es] = (OutT)compose_vf(kF, from_stored<kVF>(ld8(wreg + (es - F))),
-                                                   res_smem<kRb>(smb, es * kRb - 8u * a0));
                     if constexpr (kVF == DF11_VF_FP16) {
+                        // byte plane of output e at smb + e - a0; its 3 high bits at bit 3 e - 8 q0 of
+                        // the staged 3-bit plane (R25)
+                        const uint32_t q0 = (a0 / 8u * 3u) & ~15u;
+                        if (edge)
+                            out[es] = (OutT)compose_vf(kF, from_stored<kVF>(ld8(wreg + (es - F))),
+                                                       (res_smem<3>(smb + kFp16HiOff, 3u * es - 8u * q0) << 8) |
+                                                           ld8(smb + (es - a0)));
                         // warp-uniform trip count with the unit stride as immediate offsets (as for BF16):
-                        // lane l composes units ua + l + 32k; residual bytes advance 4 * kU * kRb = 352
-                        // per k (measured +1.2 % / +2.0 % at 256x8 / 128x16; FP8 lost 0.4-1.9 % with it)
+                        // lane l composes units ua + l + 32k (FP8 lost 0.4-1.9 % with this form)
                         const uint32_t nun = ub - ua, nfull = nun >> 5;
                         const uint32_t e0b = (ua + lane) * kU;
-                        const uint32_t ob = smb + (e0b / 8u * kRb - a0), xb = wreg + (e0b - F);
+                        const uint32_t sb0 = smb + (e0b - a0), hb0 = smb + kFp16HiOff + (e0b / 8u * 3u - q0);
+                        const uint32_t xb = wreg + (e0b - F);
                         uint4 *opb = reinterpret_cast<uint4 *>(out + e0b);
-                        auto unit = [&](uint32_t k) {
-                            uint32_t x0, x1;
-                            lds64(xb + 32u * kU * k, x0, x1);
-                            opb[32 * k] = unit_fp16(x0, x1, ob + 4u * kU * kRb * k);
+                        auto unit = [&](uint32_t k) {       // units 32 apart: 256 words, 96 bytes of high bits
+                            uint32_t x0, x1, s0, s1;
+                            lds64(xb + 256u * k, x0, x1);
+                            lds64(sb0 + 256u * k, s0, s1);
+                            opb[32 * k] = unit_fp16(x0, x1, s0, s1, hb0 + 96u * k);
                         };
                         uint32_t k = 0;
                         for (; k + 4 <= nfull; k += 4) {
@@ -669,6 +694,10 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                         for (; k < nfull; k++) unit(k);
                         if (lane < (nun & 31u)) unit(nfull);
                     } else {
+                        // FP8: residual bits of output e at bit kRb * e - 8 * a0
+                        if (edge)
+                            out[es] = (OutT)compose_vf(kF, from_stored<kVF>(ld8(wreg + (es - F))),
+                                                       res_smem<kRb>(smb, es * kRb - 8u * a0));
                         for (uint32_t u = ua + lane; u < ub; u += 32) {
                             const uint32_t e0 = u * kU;
                             const uint32_t o = smb + (e0 / 8u * kRb - a0), xa = wreg + (e0 - F);
@@ -741,7 +770,7 @@ __global__ void __launch_bounds__(kCta12, 1) sp12_kernel(const __grid_constant__
                     // residuals of a tile above the SMEM cap (or an unaligned output): per element
                     for (uint32_t e = ra + lane; e < rb; e += 32)
                         out[e] = (OutT)compose_vf(kF, from_stored<kVF>(ld8(wreg + (e - F))),
-                                                  load_residual(kF, ts.packed_sign_mantissa, e));
+                                                  load_residual(kF, ts.packed_sign_mantissa, e, N));
                 }
                 if (t == 0 && has_next) stage_sm(nlo, nhi);
                 __syncwarp();                  // the region's reads are done before the next tile's slots

@@ -6,7 +6,7 @@
 //   (App. I.2; b = 8 by default, b = L for the monolithic table of App. I.1; R6
 //   breadth-first children, R8 wide fallback, R28) -> MSB-first bit packing of EncodedExponent (P:97,
 //   R1) -> Gaps (R12/R13) and BlockOutputPos (R14).  Value formats FP16 / FP8 (NEXT-4,
-//   R25-R27) split the same way: exponent field -> symbol, sign + mantissa -> R-bit residual stream.
+//   R25-R27) split the same way: exponent field -> symbol, sign + mantissa -> residual planes.
 //
 // Built for speed, not for reading against the paper (that is oracle/'s job): every O(N) pass is
 // split over host threads; the bit packer gives every thread a bit range computed by a prefix sum of
@@ -70,7 +70,12 @@ inline uint32_t symbol_of(uint32_t word, const VFmt &f) { return (word >> f.man_
 inline uint32_t residual_of(uint32_t word, const VFmt &f) {
     return ((word >> (f.exp_bits + f.man_bits)) << f.man_bits) | (word & ((1u << f.man_bits) - 1u));
 }
-inline uint64_t residual_bytes(uint64_t n, const VFmt &f) { return roundup(f.R() * roundup(n, 16) / 8, 16) + 16; }
+// PackedSignMantissa (R25): R >= 8 -> a byte plane of the low 8 bits (roundup(n, 16) bytes) followed by
+// the (R - 8)-bit plane of the high bits (FP16: sign, m9, m8), MSB-first; R < 8 -> one R-bit plane.
+inline uint64_t residual_bytes(uint64_t n, const VFmt &f) {
+    const uint64_t L = roundup(n, 16), R = f.R();
+    return R >= 8 ? L + roundup((R - 8) * L / 8, 16) + 16 : roundup(R * L / 8, 16) + 16;
+}
 
 // ------------------------------------------------------------------------------------ histogram
 template <typename W>
@@ -383,7 +388,7 @@ df11_status encode_with_codebook(const W *w, uint64_t n, const VFmt &f, uint32_t
         for (uint64_t i = b; i < e; i++) {
             const uint32_t word = w[i];
             const uint32_t ex = (word >> sh) & em;
-            if (f.R() == 8) psm[i] = (uint8_t)(((word >> 8) & 0x80) | (word & 0x7F));   // BF16
+            if (f.R() >= 8) psm[i] = (uint8_t)residual_of(word, f);   // byte plane; BF16: P:430-431
             // first codeword start at or after chunk / block boundaries
             while (next_chunk < nthreads_fmt && next_chunk * chunk_bits <= bit) {
                 uint64_t gap = bit - next_chunk * chunk_bits;
@@ -414,17 +419,19 @@ df11_status encode_with_codebook(const W *w, uint64_t n, const VFmt &f, uint32_t
         for (uint32_t b = 0; b < B; b++) if (b > 0 && bop[b] == 0 && (uint64_t)b * block_bits > last_start) bop[b] = (uint32_t)n;
         bop[B] = (uint32_t)n;
     }
-    // residual stream of the other value formats: 8 elements = R bytes, MSB-first (R25)
+    // residual bit plane of the other value formats (R25): 8 elements = P bytes, MSB-first; P = R - 8 high
+    // bits after the byte plane (FP16), P = R bits (FP8)
     if (f.R() != 8) {
-        const uint32_t R = f.R();
+        const uint32_t R = f.R(), P = R > 8 ? R - 8 : R, shift = R > 8 ? 8 : 0;
+        uint8_t *plane = psm + (R > 8 ? roundup(n, 16) : 0);
         pool.run((n + 7) / 8, [&](unsigned, uint64_t qb, uint64_t qe) {
             for (uint64_t q = qb; q < qe; q++) {
-                unsigned __int128 acc = 0;                 // 8 * R <= 88 bits
+                uint64_t acc = 0;                          // 8 * P <= 32 bits
                 for (uint64_t j = 0; j < 8; j++) {
                     const uint64_t i = q * 8 + j;
-                    acc = (acc << R) | (i < n ? residual_of(w[i], f) : 0u);
+                    acc = (acc << P) | (i < n ? residual_of(w[i], f) >> shift : 0u);
                 }
-                for (uint32_t j = 0; j < R; j++) psm[q * R + j] = (uint8_t)(acc >> (8 * (R - 1 - j)));
+                for (uint32_t j = 0; j < P; j++) plane[q * P + j] = (uint8_t)(acc >> (8 * (P - 1 - j)));
             }
         });
     }

@@ -3,8 +3,9 @@
 // Produces the DF11 arrays of DESIGN.md §2 from a tensor already in HBM (BF16, or FP16 / FP8 words:
 // NEXT-4, R25), byte-identical to the host encoder (encode.cpp) for the same codebook:
 //   EncodedExponent   canonical Huffman codes of the exponents, MSB-first, tightly packed
-//   PackedSignMantissa sign<<7 | mantissa, one byte per element; other value formats: the
-//                     R-bit residuals sign << M | mantissa, MSB-first (R25)
+//   PackedSignMantissa sign<<7 | mantissa, one byte per element; FP16: the low residual bytes
+//                     as a byte plane + the 3 high bits (sign, m9, m8) as a bit plane; FP8: the R-bit
+//                     residuals sign << M | mantissa, MSB-first (R25)
 //   Gaps              per format thread: bit offset of the first code starting in its n-byte chunk,
 //                     0 if none (R13), packed 5 bits MSB-first (R12)
 //   BlockOutputPos    per block: number of codes starting before the block's first bit
@@ -278,8 +279,9 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
     }
     if (cnt == 0) return;
 
-    // PackedSignMantissa: sign << 7 | mantissa (BF16); other formats: 16 R-bit residuals = 2R bytes at
-    // byte R * base / 8, MSB-first (base is a multiple of 16: every thread's range is whole bytes)
+    // PackedSignMantissa: sign << 7 | mantissa (BF16); FP16: byte plane + 3-bit plane; FP8: 16 R-bit
+    // residuals = 2R bytes at byte R * base / 8, MSB-first (base is a multiple of 16: every thread's
+    // range is whole bytes)
     if constexpr (kVF == DF11_VF_BF16) {
         if (cnt == kPerThread && p.aligned) {
             uint32_t o[kPerThread / 4];
@@ -299,6 +301,20 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(const __grid_constan
             for (int j = 0; j < kPerThread; j++)
                 if (j < cnt) p.psm[base + j] = (uint8_t)(((ELEM(j) >> 8) & 0x80u) | (ELEM(j) & 0x7Fu));
         }
+    } else if constexpr (kVF == DF11_VF_FP16) {
+        // byte plane: the low 8 residual bits at byte i; then the 3-bit plane (sign, m9, m8) at
+        // roundup(N, 16) + 3 i / 8 bits, MSB-first (R25): 16 elements = 6 whole bytes at 3 base / 8
+#pragma unroll
+        for (int j = 0; j < kPerThread; j++)
+            if (j < cnt) p.psm[base + j] = (uint8_t)F::res_of(ELEM(j));
+        uint8_t *dst = p.psm + ((p.n + 15) & ~15ull) + base / 8 * 3;
+        unsigned long long acc = 0;
+#pragma unroll
+        for (int j = 0; j < kPerThread; j++) acc = (acc << 3) | (j < cnt ? (F::res_of(ELEM(j)) >> 8) : 0u);
+        const uint32_t nbytes = (cnt * 3 + 7) / 8;
+#pragma unroll
+        for (uint32_t k = 0; k < 6; k++)
+            if (k < nbytes) dst[k] = (uint8_t)(acc >> (40 - 8 * k));
     } else {
         uint8_t *dst = p.psm + base / 8 * F::R;
         unsigned long long acc = 0;
@@ -472,8 +488,9 @@ extern "C" df11_status df11_encode_device(const void *d_values, const df11_encod
     DF11_TRY(cudaMemsetAsync(ws, 0, plan->workspace_bytes, st), "workspace memset");
     DF11_TRY(cudaMemsetAsync(dst->encoded_exponent, 0, plan->encoded_exponent_bytes, st), "stream memset");
     DF11_TRY(cudaMemsetAsync(dst->gaps, 0, plan->gaps_bytes, st), "gaps memset");
-    {   // residual bytes past the last element's (its partial byte is written whole by the pack kernel)
-        const uint64_t used = N * residual_bits(vf) / 8;
+    {   // residual bytes past the last element's (its partial byte is written whole by the pack kernel);
+        // FP16's two planes (R25) leave gaps between them: zero the whole array
+        const uint64_t used = vf == DF11_VF_FP16 ? 0 : N * residual_bits(vf) / 8;
         DF11_TRY(cudaMemsetAsync(dst->packed_sign_mantissa + used, 0, plan->packed_sign_mantissa_bytes - used, st),
                  "psm memset");
     }
