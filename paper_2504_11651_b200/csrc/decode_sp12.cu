@@ -26,8 +26,12 @@
 //    (the count sits above).
 //  * The merge stores one 8-element unit (16 bytes) per lane and STG.128, so a warp instruction writes
 //    512 contiguous bytes (4 L1 wavefronts; two 16-byte halves per lane 32 bytes apart took 8).
-//  * A tile's PackedSignMantissa range is staged in SMEM by one TMA bulk copy; the first tile's copies
-//    are issued before the table build; per-CTA tile ranges come from df11_plan_cta_ranges (api.cu).
+//  * A tile's PackedSignMantissa range is staged in SMEM by one TMA bulk copy (FP16: two, one per
+//    residual plane); the first tile's copies are issued before the table build; per-CTA tile ranges
+//    come from df11_plan_cta_ranges (api.cu).
+//  * Programmatic dependent launch: a decode that follows a decode on the same stream builds its table
+//    and decodes its first tile on the SMs the previous one leaves in its tail, and waits for it
+//    (griddepcontrol.wait) before each tile's first global write (df11.h states the stream semantics).
 #include <type_traits>
 
 #include "t12_common.cuh"
