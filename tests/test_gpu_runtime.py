@@ -189,6 +189,14 @@ def test_back_to_back_decodes_into_one_buffer():
             bad += not torch.equal(buf[-tiny.size:].view(torch.int16), ref_tiny)
     torch.cuda.synchronize()
     assert bad == 0, f"{bad} of 40 back-to-back pairs lost the second decode's values"
+    # SM-budgeted decodes (df11_decompress_block_budget): the dependent grid's CTAs land on idle SMs at
+    # once and must still wait before writing
+    for ctas in (8, 37):
+        for i in range(10):
+            df11.decompress_block([d_big], outs=[buf], max_ctas=ctas)
+            df11.decompress_block([d_tiny], outs=[buf[-tiny.size:]], max_ctas=ctas)
+            bad += not torch.equal(buf[-tiny.size:].view(torch.int16), ref_tiny)
+    assert bad == 0, f"{bad} budgeted back-to-back pairs lost the second decode's values"
     assert torch.equal(buf[: -small.size].view(torch.int16), ref_big[: -small.size])
     for i in range(21):
         df11.decompress(d_other if i % 2 == 0 else d_big, out=buf)
